@@ -1,0 +1,184 @@
+/*
+ * cofem_b200.h -- C ABI of the B200-native CoFEM hot path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types), so any FFI can bind
+ * it (ctypes here; see INTEGRATION.md for the binding the reference would
+ * add).  Every entry point names the reference interface it replaces; paths
+ * are relative to the reference package /root/reference/pkg/src/sbl/.
+ *
+ * Conventions
+ *   - Phi (the dictionary) is N x D float32, row-major (C order), exactly the
+ *     (N, D) numpy layout of operators.DenseOperator.matrix (operators.py:104).
+ *     Under column sharding a context holds its local D_r columns.
+ *   - Column blocks ("D x Q" in the reference, e.g. the PCG right-hand sides
+ *     B of cg.solve, cg.py:155) are float64 row-major D x Q on the host side:
+ *     coordinate j's Q entries are contiguous, as numpy (D, Q) C-order.
+ *   - Every function returns 0 on success and a negative COFEM_E* code on
+ *     failure; cofem_last_error() returns the message of the last failure on
+ *     the calling thread.  No entry point ever falls back to the CPU.
+ */
+#ifndef COFEM_B200_H
+#define COFEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COFEM_ABI_VERSION 1
+
+enum cofem_status {
+  COFEM_OK = 0,
+  COFEM_EINVAL = -1,      /* bad argument (ShapeMismatchError / ValueError in the reference) */
+  COFEM_ECUDA = -2,       /* CUDA runtime failure */
+  COFEM_ENOMEM = -3,      /* device allocation failed */
+  COFEM_EDIVERGED = -4,   /* non-finite residual: DivergenceError (cg.py:17) */
+  COFEM_ENCCL = -5,       /* NCCL failure / NCCL not loadable */
+  COFEM_ESTATE = -6       /* call order violated (e.g. no dictionary set) */
+};
+
+/* Arithmetic of the column blocks and of the Phi contractions.
+ * FP32: fp32 vectors, fp32 contraction accumulators, fp64 scalar reductions
+ *       (the north_star's "GPU runs fp32").
+ * FP64: Phi stays fp32 in HBM; vectors, contraction accumulators and scalars
+ *       are fp64 (fp32 Phi entries are exact in fp64, so this reproduces the
+ *       reference's float64 arithmetic up to summation order). */
+enum cofem_precision { COFEM_FP32 = 0, COFEM_FP64 = 1 };
+
+/* Preconditioner policy, cg.py:79-108 make_preconditioner(policy, ...). */
+enum cofem_theta { COFEM_THETA_ALL_ONES = 0, COFEM_THETA_JACOBI = 1, COFEM_THETA_NONE = 2,
+                   COFEM_THETA_CUSTOM = 3 };
+
+/* M-step variant, cofem.py:103 m_step / cofem.py:120 m_step_nonneg. */
+enum cofem_variant { COFEM_STANDARD = 0, COFEM_NONNEG = 1 };
+
+typedef struct cofem_ctx cofem_ctx;
+
+/* CgConfig, cg.py:48-67 (theta lives in cofem_em_config / the minv argument). */
+typedef struct {
+  int32_t max_steps;          /* U >= 1 */
+  int32_t printed_recursion;  /* 0: P <- W + eta P (standard PCG); 1: P <- R + eta P */
+  double tolerance;           /* Frobenius ||R||_F / ||B||_F stopping threshold > 0 */
+} cofem_cg_config;
+
+/* CgReport, cg.py:70-76. */
+typedef struct {
+  int32_t steps_taken;
+  int32_t converged;
+  int32_t diverged;            /* 1 => residual turned non-finite at step `steps_taken` */
+  int32_t n_breakdown;         /* number of columns frozen by pi_q == 0 */
+  double final_relative_residual;
+} cofem_cg_report;
+
+/* CofemConfig, cofem.py:30-47 (+ the CG part in a cofem_cg_config). */
+typedef struct {
+  int32_t iterations;   /* T >= 1 */
+  int32_t probes;       /* K >= 1 */
+  int32_t variant;      /* cofem_variant */
+  int32_t theta_policy; /* cofem_theta */
+  double clamp_max;     /* 1e12 */
+  double floor_eps;     /* 1e-12 */
+} cofem_em_config;
+
+/* ---- library ---------------------------------------------------------- */
+int cofem_abi_version(void);
+const char* cofem_last_error(void);
+int cofem_device_count(int* out);
+
+/* ---- context: one dense dictionary shard on one GPU --------------------
+ * Replaces operators.DenseOperator (operators.py:104-129) + the workspace
+ * that cg._pcg_loop (cg.py:111-152) allocates per call.               */
+int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, int precision);
+int cofem_destroy(cofem_ctx* ctx);
+
+/* Upload Phi (N x D_local float32, row stride `ld` elements) from host
+ * memory (or adopt a device pointer when `on_device` != 0; the caller keeps
+ * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */
+int cofem_set_dictionary(cofem_ctx* ctx, const float* phi, int64_t ld, int on_device);
+
+/* Declare this context's place in a column-sharded dictionary: it holds
+ * global columns [col_offset, col_offset + n_cols) of `global_cols`.  Used by
+ * the device generators so every shard draws the same global Phi / probes. */
+int cofem_set_shard(cofem_ctx* ctx, int64_t col_offset, int64_t global_cols);
+
+/* Generate Phi on the device: entries scale * N(0,1) from a counter-based
+ * generator keyed by `seed` (synthetic benchmark dictionaries,
+ * operators.build_dense_gaussian, operators.py:227-232, with a device RNG). */
+int cofem_generate_gaussian_dictionary(cofem_ctx* ctx, uint64_t seed, double scale);
+
+/* Copy Phi back to the host (n_rows x n_cols, row stride n_cols). */
+int cofem_get_dictionary(cofem_ctx* ctx, float* out);
+
+/* ---- multi-GPU: Phi column-sharded across `nranks` processes ----------
+ * 128-byte NCCL unique id from rank 0, broadcast by the host.  With
+ * nranks == 1 the collectives are real single-rank NCCL calls.        */
+int cofem_nccl_get_unique_id(void* out128);
+int cofem_set_comm(cofem_ctx* ctx, const void* unique_id128, int nranks, int rank);
+
+/* ---- operator applications (host float64 buffers) ---------------------
+ * LinearOperator.apply / apply_adjoint, operators.py:61-71.            */
+int cofem_apply(cofem_ctx* ctx, const double* V, int64_t q, double* out);          /* (D,q)->(N,q) */
+int cofem_apply_adjoint(cofem_ctx* ctx, const double* U, int64_t q, double* out);  /* (N,q)->(D,q) */
+/* SystemMatrix.apply, operators.py:267-272: out = beta Phi^T Phi V + alpha .* V */
+int cofem_system_apply(cofem_ctx* ctx, double beta, const double* alpha, const double* V,
+                       int64_t q, double* out);
+/* LinearOperator.column_sq_norms for the dense kind, operators.py:128-129. */
+int cofem_column_sq_norms(cofem_ctx* ctx, double* out);
+
+/* ---- blocked PCG --------------------------------------------------------
+ * cg.solve / cg.solve_blocked (cg.py:155-234) on the dense system
+ * A = beta Phi^T Phi + diag(alpha).  minv is the inverse preconditioner
+ * diagonal, D x n_groups row-major, and group_of_col (length q, may be NULL
+ * when n_groups == 1) maps each column to its group (cg.py:225-228).
+ * B, X: host D x q float64.  breakdown (length q, may be NULL) receives 1 for
+ * columns frozen by pi_q == 0.  Returns COFEM_EDIVERGED with rep->diverged
+ * set when the residual turns non-finite. */
+int cofem_pcg_solve(cofem_ctx* ctx, double beta, const double* alpha, const double* minv,
+                    int32_t n_groups, const int32_t* group_of_col, const double* B, int64_t q,
+                    const cofem_cg_config* cg, double* X, cofem_cg_report* rep,
+                    uint8_t* breakdown);
+
+/* ---- the CoFEM EM loop ---------------------------------------------------
+ * cofem.run_cofem (cofem.py:136-157): T E-steps (cofem.e_step, cofem.py:76)
+ * each solving A X = [p_1..p_K | Phi^T y] by blocked PCG, reading
+ * mu = beta x_{K+1} and s_j = (1/K) sum_k p_jk x_jk (probes.py:28), and the
+ * closed-form M-step (cofem.py:103 / :120) between E-steps.
+ *   y            N float64 observation
+ *   probes       T x D_local x K int8 (+1/-1), the host-drawn Rademacher
+ *                blocks (probes.draw_rademacher, probes.py:13), iteration
+ *                major; NULL => the device draws them (no host parity).
+ *   theta        D_local custom theta (COFEM_THETA_CUSTOM) or NULL
+ * Outputs (host, may be NULL): alpha (the precision used by the final
+ * E-step), mu, s (length D_local), and per-iteration CG steps / residuals
+ * (length T).  On divergence returns COFEM_EDIVERGED and *failed_iteration
+ * / *failed_step name the EM iteration and CG step. */
+int cofem_run(cofem_ctx* ctx, const double* y, double beta, const cofem_em_config* em,
+              const cofem_cg_config* cg, const double* theta, const int8_t* probes,
+              uint64_t device_probe_seed, double* alpha, double* mu, double* s,
+              int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration,
+              int32_t* failed_step);
+
+/* ---- device-timed benchmark hooks ----------------------------------------
+ * Run `n_iter` EM iterations continuing the context's resident state
+ * (bench.py "value": inputs already in HBM), returning device milliseconds
+ * for the whole call and for the dominant kernels of the last call.     */
+typedef struct {
+  double total_ms;          /* CUDA-event time of the n_iter iterations */
+  double fwd_ms;            /* summed device time of Phi X launches */
+  double bwd_ms;            /* summed device time of Phi^T U launches */
+  int64_t fwd_launches;
+  int64_t bwd_launches;
+  int64_t pcg_steps;        /* PCG steps executed */
+  int64_t kernel_launches;  /* all kernels launched by the library */
+} cofem_timing;
+
+int cofem_bench_prepare(cofem_ctx* ctx, const double* y, double beta, const cofem_em_config* em,
+                        const cofem_cg_config* cg, uint64_t device_probe_seed);
+int cofem_bench_iterations(cofem_ctx* ctx, int n_iter, int time_kernels, cofem_timing* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COFEM_B200_H */

@@ -1,0 +1,320 @@
+"""ctypes binding of the C ABI in include/cofem_b200.h.
+
+The shared library is built in-tree (``python -m paper_2105_10439_b200.build``
+or ``__graft_entry__.build()``) into ``paper_2105_10439_b200/_lib/``.  There is
+no CPU fallback: if the library or a GPU is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_float, c_int, c_int8, c_int32, c_int64, c_uint8, c_uint64, c_void_p
+
+import numpy as np
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libcofem_b200.so")
+
+COFEM_OK = 0
+COFEM_EINVAL = -1
+COFEM_ECUDA = -2
+COFEM_ENOMEM = -3
+COFEM_EDIVERGED = -4
+COFEM_ENCCL = -5
+COFEM_ESTATE = -6
+
+FP32, FP64 = 0, 1
+THETA_CODES = {"all-ones": 0, "jacobi": 1, "none": 2}
+THETA_CUSTOM = 3
+VARIANT_CODES = {"standard": 0, "nonneg": 1}
+
+# every symbol include/cofem_b200.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "cofem_abi_version",
+    "cofem_last_error",
+    "cofem_device_count",
+    "cofem_create",
+    "cofem_destroy",
+    "cofem_set_dictionary",
+    "cofem_set_shard",
+    "cofem_generate_gaussian_dictionary",
+    "cofem_get_dictionary",
+    "cofem_nccl_get_unique_id",
+    "cofem_set_comm",
+    "cofem_apply",
+    "cofem_apply_adjoint",
+    "cofem_system_apply",
+    "cofem_column_sq_norms",
+    "cofem_pcg_solve",
+    "cofem_run",
+    "cofem_bench_prepare",
+    "cofem_bench_iterations",
+)
+
+
+class CgConfigC(ctypes.Structure):
+    _fields_ = [("max_steps", c_int32), ("printed_recursion", c_int32), ("tolerance", c_double)]
+
+
+class CgReportC(ctypes.Structure):
+    _fields_ = [
+        ("steps_taken", c_int32),
+        ("converged", c_int32),
+        ("diverged", c_int32),
+        ("n_breakdown", c_int32),
+        ("final_relative_residual", c_double),
+    ]
+
+
+class EmConfigC(ctypes.Structure):
+    _fields_ = [
+        ("iterations", c_int32),
+        ("probes", c_int32),
+        ("variant", c_int32),
+        ("theta_policy", c_int32),
+        ("clamp_max", c_double),
+        ("floor_eps", c_double),
+    ]
+
+
+class TimingC(ctypes.Structure):
+    _fields_ = [
+        ("total_ms", c_double),
+        ("fwd_ms", c_double),
+        ("bwd_ms", c_double),
+        ("fwd_launches", c_int64),
+        ("bwd_launches", c_int64),
+        ("pcg_steps", c_int64),
+        ("kernel_launches", c_int64),
+    ]
+
+
+class CofemError(RuntimeError):
+    """A failure reported by the native library (message from cofem_last_error)."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"cofem error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def _dp(a):
+    return a.ctypes.data_as(POINTER(c_double))
+
+
+def load():
+    """Load the native library; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2105_10439_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    vp = c_void_p
+    sig = {
+        "cofem_abi_version": (c_int, []),
+        "cofem_last_error": (ctypes.c_char_p, []),
+        "cofem_device_count": (c_int, [POINTER(c_int)]),
+        "cofem_create": (c_int, [POINTER(vp), c_int, c_int64, c_int64, c_int]),
+        "cofem_destroy": (c_int, [vp]),
+        "cofem_set_dictionary": (c_int, [vp, vp, c_int64, c_int]),
+        "cofem_set_shard": (c_int, [vp, c_int64, c_int64]),
+        "cofem_generate_gaussian_dictionary": (c_int, [vp, c_uint64, c_double]),
+        "cofem_get_dictionary": (c_int, [vp, POINTER(c_float)]),
+        "cofem_nccl_get_unique_id": (c_int, [vp]),
+        "cofem_set_comm": (c_int, [vp, vp, c_int, c_int]),
+        "cofem_apply": (c_int, [vp, POINTER(c_double), c_int64, POINTER(c_double)]),
+        "cofem_apply_adjoint": (c_int, [vp, POINTER(c_double), c_int64, POINTER(c_double)]),
+        "cofem_system_apply": (c_int, [vp, c_double, POINTER(c_double), POINTER(c_double), c_int64,
+                                       POINTER(c_double)]),
+        "cofem_column_sq_norms": (c_int, [vp, POINTER(c_double)]),
+        "cofem_pcg_solve": (c_int, [vp, c_double, POINTER(c_double), POINTER(c_double), c_int32,
+                                    POINTER(c_int32), POINTER(c_double), c_int64, POINTER(CgConfigC),
+                                    POINTER(c_double), POINTER(CgReportC), POINTER(c_uint8)]),
+        "cofem_run": (c_int, [vp, POINTER(c_double), c_double, POINTER(EmConfigC), POINTER(CgConfigC),
+                              POINTER(c_double), POINTER(c_int8), c_uint64, POINTER(c_double),
+                              POINTER(c_double), POINTER(c_double), POINTER(c_int32), POINTER(c_double),
+                              POINTER(c_int32), POINTER(c_int32)]),
+        "cofem_bench_prepare": (c_int, [vp, POINTER(c_double), c_double, POINTER(EmConfigC),
+                                        POINTER(CgConfigC), c_uint64]),
+        "cofem_bench_iterations": (c_int, [vp, c_int, c_int, POINTER(TimingC)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.cofem_abi_version() != 1:
+        raise ImportError("libcofem_b200 ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def last_error():
+    return load().cofem_last_error().decode(errors="replace")
+
+
+def check(rc):
+    if rc != COFEM_OK:
+        raise CofemError(rc, last_error())
+    return rc
+
+
+def device_count():
+    n = c_int(0)
+    rc = load().cofem_device_count(ctypes.byref(n))
+    return n.value if rc == 0 else 0
+
+
+class Context:
+    """Owns one native cofem_ctx: a dense float32 dictionary shard on one GPU."""
+
+    def __init__(self, n_rows, n_cols, precision=FP32, device=0):
+        lib = load()
+        handle = c_void_p()
+        check(lib.cofem_create(ctypes.byref(handle), int(device), int(n_rows), int(n_cols), int(precision)))
+        self._h = handle
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.precision = precision
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("context already closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            load().cofem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- dictionary
+    def set_dictionary(self, phi):
+        phi = np.ascontiguousarray(phi, dtype=np.float32)
+        if phi.shape != (self.n_rows, self.n_cols):
+            raise ValueError(f"dictionary shape {phi.shape} != {(self.n_rows, self.n_cols)}")
+        check(load().cofem_set_dictionary(self.handle, phi.ctypes.data_as(c_void_p), phi.shape[1], 0))
+
+    def set_shard(self, col_offset, global_cols):
+        check(load().cofem_set_shard(self.handle, int(col_offset), int(global_cols)))
+
+    def generate_gaussian(self, seed, scale):
+        check(load().cofem_generate_gaussian_dictionary(self.handle, int(seed) & (2**64 - 1), float(scale)))
+
+    def get_dictionary(self):
+        out = np.empty((self.n_rows, self.n_cols), dtype=np.float32)
+        check(load().cofem_get_dictionary(self.handle, out.ctypes.data_as(POINTER(c_float))))
+        return out
+
+    def set_comm(self, unique_id: bytes, nranks, rank):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(load().cofem_set_comm(self.handle, ctypes.cast(buf, c_void_p), int(nranks), int(rank)))
+
+    # -- operator applications (float64 host blocks)
+    def apply(self, V):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        out = np.empty((self.n_rows, V.shape[1]))
+        check(load().cofem_apply(self.handle, _dp(V), V.shape[1], _dp(out)))
+        return out
+
+    def apply_adjoint(self, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty((self.n_cols, U.shape[1]))
+        check(load().cofem_apply_adjoint(self.handle, _dp(U), U.shape[1], _dp(out)))
+        return out
+
+    def system_apply(self, beta, alpha, V):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        out = np.empty_like(V)
+        check(load().cofem_system_apply(self.handle, float(beta), _dp(alpha), _dp(V), V.shape[1], _dp(out)))
+        return out
+
+    def column_sq_norms(self):
+        out = np.empty(self.n_cols)
+        check(load().cofem_column_sq_norms(self.handle, _dp(out)))
+        return out
+
+    # -- PCG
+    def pcg_solve(self, beta, alpha, minv, B, max_steps, tolerance, printed=False, groups=None):
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        q = B.shape[1]
+        alpha = np.ascontiguousarray(alpha, dtype=np.float64)
+        minv = np.ascontiguousarray(minv, dtype=np.float64)
+        ngroups = 1 if minv.ndim == 1 else minv.shape[1]
+        gptr = None
+        if ngroups > 1:
+            g = np.ascontiguousarray(groups, dtype=np.int32)
+            gptr = g.ctypes.data_as(POINTER(c_int32))
+        X = np.empty_like(B)
+        rep = CgReportC()
+        brk = np.zeros(q, dtype=np.uint8)
+        cfg = CgConfigC(int(max_steps), 1 if printed else 0, float(tolerance))
+        rc = load().cofem_pcg_solve(self.handle, float(beta), _dp(alpha), _dp(minv), ngroups, gptr, _dp(B), q,
+                                    ctypes.byref(cfg), _dp(X), ctypes.byref(rep),
+                                    brk.ctypes.data_as(POINTER(c_uint8)))
+        if rc not in (COFEM_OK, COFEM_EDIVERGED):
+            check(rc)
+        return X, rep, brk, rc == COFEM_EDIVERGED
+
+    # -- EM loop
+    def run(self, y, beta, iterations, probes, variant, theta_policy, clamp_max, floor_eps, max_steps, tolerance,
+            printed=False, theta=None, probe_blocks=None, device_probe_seed=0):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        em = EmConfigC(int(iterations), int(probes), int(variant), int(theta_policy), float(clamp_max),
+                       float(floor_eps))
+        cg = CgConfigC(int(max_steps), 1 if printed else 0, float(tolerance))
+        th = None
+        if theta is not None:
+            theta = np.ascontiguousarray(theta, dtype=np.float64)
+            th = _dp(theta)
+        pr = None
+        if probe_blocks is not None:
+            probe_blocks = np.ascontiguousarray(probe_blocks, dtype=np.int8)
+            assert probe_blocks.shape == (iterations, self.n_cols, probes)
+            pr = probe_blocks.ctypes.data_as(POINTER(c_int8))
+        d = self.n_cols
+        alpha, mu, s = np.empty(d), np.empty(d), np.empty(d)
+        steps = np.zeros(iterations, dtype=np.int32)
+        resid = np.zeros(iterations)
+        fit, fst = c_int32(0), c_int32(0)
+        rc = load().cofem_run(self.handle, _dp(y), float(beta), ctypes.byref(em), ctypes.byref(cg), th, pr,
+                              int(device_probe_seed) & (2**64 - 1), _dp(alpha), _dp(mu), _dp(s),
+                              steps.ctypes.data_as(POINTER(c_int32)), _dp(resid), ctypes.byref(fit),
+                              ctypes.byref(fst))
+        if rc == COFEM_EDIVERGED:
+            return None, (fit.value, fst.value)
+        check(rc)
+        return (alpha, mu, s, steps, resid), None
+
+    # -- benchmark hooks
+    def bench_prepare(self, y, beta, probes, max_steps, tolerance, theta_policy=0, variant=0, seed=0,
+                      clamp_max=1e12, floor_eps=1e-12):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        em = EmConfigC(1, int(probes), int(variant), int(theta_policy), float(clamp_max), float(floor_eps))
+        cg = CgConfigC(int(max_steps), 0, float(tolerance))
+        check(load().cofem_bench_prepare(self.handle, _dp(y), float(beta), ctypes.byref(em), ctypes.byref(cg),
+                                         int(seed) & (2**64 - 1)))
+
+    def bench_iterations(self, n_iter, time_kernels=False):
+        t = TimingC()
+        check(load().cofem_bench_iterations(self.handle, int(n_iter), 1 if time_kernels else 0, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in TimingC._fields_}
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(load().cofem_nccl_get_unique_id(ctypes.cast(buf, c_void_p)))
+    return buf.raw

@@ -1,0 +1,1008 @@
+// cofem.cu -- context, PCG driver and C ABI of the B200 CoFEM hot path.
+//
+// One context = one dense dictionary shard resident on one GPU plus the PCG
+// workspace.  The PCG loop is driven from the host but never waits on the
+// device inside a solve: every scalar (gamma, eta, delta) is derived on the
+// device, kernels early-exit once the device status says "done", and the host
+// only polls that status LAG steps behind the enqueue front.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/cofem_b200.h"
+#include "kernels.cuh"
+#include "nccl.h"
+#include "pcg.cuh"
+
+using namespace cofem;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess) return fail(COFEM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKR(x)              \
+  do {                      \
+    int r_ = (x);           \
+    if (r_ != 0) return r_; \
+  } while (0)
+
+constexpr int LAG = 3;          // host status poll distance (steps)
+constexpr int QCHUNK = 32;      // max columns per contraction launch
+constexpr int64_t PAD = 256;    // Np, Dp multiples (tile sizes divide it)
+constexpr int MAX_SPLITS = 32;  // split-K partial blocks per contraction
+
+// ---- NCCL, bound at run time so the library loads without it -------------
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok ? 0 : fail(COFEM_ENCCL, "libnccl.so.2 not loadable");
+  g_nccl.tried = true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  void* h = nullptr;
+  for (const char* n : names)
+    if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return fail(COFEM_ENCCL, std::string("dlopen libnccl.so.2 failed: ") + dlerror());
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy;
+  return g_nccl.ok ? 0 : fail(COFEM_ENCCL, "libnccl missing symbols");
+}
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// ---- contraction configurations -------------------------------------------
+// fp32: 4 rows (fwd) / 4 columns (bwd) x QP accumulators per thread
+// fp64: 2 x QP double accumulators per thread
+template <typename T>
+struct Tiles;
+template <>
+struct Tiles<float> {
+  static constexpr int FR = 4, FWM = 2, FWK = 4, FBK = 32, FST = 2;
+  static constexpr int BC = 4, BWN = 2, BWK = 4, BBK = 32, BST = 3;
+};
+template <>
+struct Tiles<double> {
+  static constexpr int FR = 2, FWM = 4, FWK = 2, FBK = 32, FST = 2;
+  static constexpr int BC = 2, BWN = 4, BWK = 2, BBK = 32, BST = 2;
+};
+
+}  // namespace
+
+struct SplitPlan {
+  int nsplit = 1;
+  int per_split = 0;  // rows (bwd) or columns (fwd) per split, multiple of the tile depth
+};
+
+struct cofem_ctx {
+  int device = 0, prec = COFEM_FP32;
+  int64_t N = 0, D = 0, Np = 0, Dp = 0;
+  int64_t col_offset = 0, global_cols = 0;
+  cudaStream_t stream = nullptr;
+  float* phi = nullptr;
+  bool have_phi = false;
+  int sm_count = 148;
+
+  // workspace (T = float or double by precision)
+  int ldq = 0;
+  void *X = nullptr, *R = nullptr, *P = nullptr, *Psi = nullptr;
+  void *V = nullptr, *vpart = nullptr, *ppart = nullptr, *tmpD = nullptr;
+  size_t vpart_cap = 0, ppart_cap = 0;
+  double *alpha = nullptr, *minv = nullptr, *theta = nullptr, *colsq = nullptr;
+  double *mu = nullptr, *s = nullptr, *aty = nullptr, *ybuf = nullptr;
+  int8_t *probes = nullptr, *probe_store = nullptr;
+  int* groups = nullptr;
+  int groups_cap = 0;
+  double* scal = nullptr;  // rho0 | rho1 | rho_new | rn2 | pi | bn2 (ldq each)
+  int* frozen = nullptr;
+  double* partials = nullptr;
+  unsigned* tickets = nullptr;
+  Status* st = nullptr;
+  Status* h_st = nullptr;  // pinned, LAG slots
+  cudaEvent_t ev[LAG] = {};
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int nblk_elem = 0;
+
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // bench state
+  bool bench_ready = false;
+  double beta = 0;
+  cofem_em_config em{};
+  cofem_cg_config cg{};
+  uint64_t dseed = 0;
+  int bench_iter = 0;
+
+  // instrumentation
+  bool time_kernels = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  std::vector<std::pair<int, size_t>> timed;  // (kind 0 fwd / 1 bwd, event index)
+  int64_t launches = 0, fwd_launches = 0, bwd_launches = 0, pcg_steps = 0;
+
+  Scalars sc() const {
+    Scalars s;
+    s.rho[0] = scal;
+    s.rho[1] = scal + ldq;
+    s.rho_new = scal + 2 * ldq;
+    s.rn2 = scal + 3 * ldq;
+    s.pi = scal + 4 * ldq;
+    s.bn2 = scal + 5 * ldq;
+    s.frozen = frozen;
+    s.partials = partials;
+    s.ticket = tickets;
+    return s;
+  }
+  size_t tsize() const { return prec == COFEM_FP64 ? 8 : 4; }
+};
+
+namespace {
+
+int set_dev(cofem_ctx* c) {
+  CK(cudaSetDevice(c->device));
+  return 0;
+}
+
+cudaEvent_t next_event(cofem_ctx* c) {
+  if (c->evnext == c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evnext++];
+}
+
+void free_ws(cofem_ctx* c) {
+  void* ptrs[] = {c->X, c->R, c->P, c->Psi, c->V, c->vpart, c->ppart, c->tmpD, c->scal, c->frozen, c->partials};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  c->X = c->R = c->P = c->Psi = c->V = c->vpart = c->ppart = c->tmpD = nullptr;
+  c->scal = nullptr;
+  c->frozen = nullptr;
+  c->partials = nullptr;
+  c->ldq = 0;
+}
+
+int elem_block(int ldq) { return ldq >= 256 ? ldq : ldq * (256 / ldq); }
+
+// choose split count for a contraction: minimise wave quantisation plus the
+// extra traffic of the split partials relative to the Phi stream
+SplitPlan plan_splits(int64_t nblocks_other, int64_t ntiles, int tile, int slots, double out_bytes_per_split,
+                      double phi_bytes) {
+  SplitPlan best;
+  double best_cost = 1e300;
+  const int smax = (int)std::min<int64_t>(ntiles, MAX_SPLITS);
+  for (int s = 1; s <= smax; ++s) {
+    const int64_t per = (ntiles + s - 1) / s;
+    const int64_t S = (ntiles + per - 1) / per;
+    const int64_t ctas = nblocks_other * S;
+    const double waves = std::ceil((double)ctas / slots);
+    const double t_compute = waves * per / ((double)nblocks_other * ntiles / slots);
+    const double t_part = 2.0 * S * out_bytes_per_split / phi_bytes;
+    const double cost = t_compute + t_part;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best.nsplit = (int)S;
+      best.per_split = (int)(per * tile);
+    }
+  }
+  return best;
+}
+
+template <typename T, int QP>
+struct Kern {
+  using TL = Tiles<T>;
+  using FC = FwdCfg<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST>;
+  using BC = BwdCfg<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST>;
+  static constexpr auto fwd = fwd_kernel<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST>;
+  static constexpr auto bwd = bwd_kernel<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST>;
+  static bool inited;
+  static int fwd_occ, bwd_occ;
+  static int init() {
+    if (inited) return 0;
+    CK(cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM));
+    CK(cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BC::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fwd_occ, fwd, FC::NT, FC::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bwd_occ, bwd, BC::NT, BC::SMEM));
+    if (fwd_occ < 1 || bwd_occ < 1) return fail(COFEM_ECUDA, "contraction kernel cannot be resident");
+    inited = true;
+    return 0;
+  }
+};
+template <typename T, int QP>
+bool Kern<T, QP>::inited = false;
+template <typename T, int QP>
+int Kern<T, QP>::fwd_occ = 0;
+template <typename T, int QP>
+int Kern<T, QP>::bwd_occ = 0;
+
+int ensure_ws(cofem_ctx* c, int ldq) {
+  if (c->ldq == ldq) return 0;
+  free_ws(c);
+  const size_t ts = c->tsize();
+  const size_t dbytes = (size_t)c->Dp * ldq * ts;
+  CK(cudaMalloc(&c->X, dbytes));
+  CK(cudaMalloc(&c->R, dbytes));
+  CK(cudaMalloc(&c->P, dbytes));
+  CK(cudaMalloc(&c->Psi, dbytes));
+  CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * QCHUNK * ts));
+  CK(cudaMalloc(&c->V, (size_t)c->Np * QCHUNK * ts));
+  // split partial capacity: up to MAX_SPLITS partial blocks of a 32-column chunk
+  c->vpart_cap = (size_t)MAX_SPLITS * c->Np * QCHUNK * ts;
+  c->ppart_cap = (size_t)MAX_SPLITS * c->Dp * QCHUNK * ts;
+  CK(cudaMalloc(&c->vpart, c->vpart_cap));
+  CK(cudaMalloc(&c->ppart, c->ppart_cap));
+  CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
+  CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
+  c->nblk_elem = 4 * c->sm_count;
+  CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
+  CK(cudaMemset(c->X, 0, dbytes));
+  CK(cudaMemset(c->R, 0, dbytes));
+  CK(cudaMemset(c->P, 0, dbytes));
+  CK(cudaMemset(c->Psi, 0, dbytes));
+  c->ldq = ldq;
+  return 0;
+}
+
+int ensure_groups(cofem_ctx* c, int n) {
+  if (c->groups_cap >= n) return 0;
+  if (c->groups) cudaFree(c->groups);
+  CK(cudaMalloc(&c->groups, n * sizeof(int)));
+  c->groups_cap = n;
+  return 0;
+}
+
+int allreduce(cofem_ctx* c, void* buf, size_t count, ncclDataType_t dt) {
+  if (c->nranks <= 1 || !c->comm) return 0;
+  ncclResult_t r = g_nccl.allReduce(buf, buf, count, dt, ncclSum, c->comm, c->stream);
+  if (r != ncclSuccess) return fail(COFEM_ENCCL, std::string("ncclAllReduce: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+  return 0;
+}
+
+template <typename T>
+ncclDataType_t nccl_t() {
+  return sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+}
+
+// ---- the two contractions ----------------------------------------------
+// fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
+template <typename T, int QP>
+int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status* st) {
+  using K = Kern<T, QP>;
+  CKR(K::init());
+  const int64_t ntiles = c->Dp / Tiles<T>::FBK;
+  const int64_t mblocks = c->Np / K::FC::BM;
+  SplitPlan sp = plan_splits(mblocks, ntiles, Tiles<T>::FBK, K::fwd_occ * c->sm_count,
+                             (double)c->Np * QP * sizeof(T), (double)c->Np * c->Dp * 4.0);
+  while ((size_t)sp.nsplit * c->Np * QP * sizeof(T) > c->vpart_cap) {  // capacity guard
+    sp.per_split *= 2;
+    sp.nsplit = (int)((c->Dp + sp.per_split - 1) / sp.per_split);
+  }
+  dim3 grid((unsigned)mblocks, (unsigned)sp.nsplit);
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  K::fwd<<<grid, K::FC::NT, K::FC::SMEM, c->stream>>>(c->phi, c->Dp, src, lds, qoff, sp.per_split, c->Dp,
+                                                      (T*)c->vpart, c->Np, st);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({0, c->evnext - 2});
+  }
+  c->launches++;
+  c->fwd_launches++;
+  CK(cudaGetLastError());
+  const int64_t n = c->Np * QP;
+  const int bs = 256;
+  const int gs = (int)std::min<int64_t>((n + bs - 1) / bs, 8 * c->sm_count);
+  k_sum_splits<T><<<gs, bs, 0, c->stream>>>(n, sp.nsplit, (const T*)c->vpart, vout, st);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// bwd: ppart = Phi^T V  (V Np x QP dense); returns number of splits
+template <typename T, int QP>
+int run_bwd(cofem_ctx* c, const T* v, int* nsplit_out, const Status* st) {
+  using K = Kern<T, QP>;
+  CKR(K::init());
+  const int64_t ntiles = c->Np / Tiles<T>::BBK;
+  const int64_t nblocks = c->Dp / K::BC::BN;
+  SplitPlan sp = plan_splits(nblocks, ntiles, Tiles<T>::BBK, K::bwd_occ * c->sm_count,
+                             (double)c->Dp * QP * sizeof(T), (double)c->Np * c->Dp * 4.0);
+  while ((size_t)sp.nsplit * c->Dp * QP * sizeof(T) > c->ppart_cap) {
+    sp.per_split *= 2;
+    sp.nsplit = (int)((c->Np + sp.per_split - 1) / sp.per_split);
+  }
+  dim3 grid((unsigned)nblocks, (unsigned)sp.nsplit);
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  K::bwd<<<grid, K::BC::NT, K::BC::SMEM, c->stream>>>(c->phi, c->Dp, v, QP, 0, sp.per_split, c->Np,
+                                                      (T*)c->ppart, c->Dp, st);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({1, c->evnext - 2});
+  }
+  c->launches++;
+  c->bwd_launches++;
+  CK(cudaGetLastError());
+  *nsplit_out = sp.nsplit;
+  return 0;
+}
+
+template <typename T>
+int fwd_chunk(cofem_ctx* c, int qpc, const T* src, int lds, int qoff, T* vout, const Status* st) {
+  switch (qpc) {
+    case 8: return run_fwd<T, 8>(c, src, lds, qoff, vout, st);
+    case 16: return run_fwd<T, 16>(c, src, lds, qoff, vout, st);
+    case 24: return run_fwd<T, 24>(c, src, lds, qoff, vout, st);
+    case 32: return run_fwd<T, 32>(c, src, lds, qoff, vout, st);
+  }
+  return fail(COFEM_EINVAL, "bad column chunk");
+}
+
+template <typename T>
+int bwd_chunk(cofem_ctx* c, int qpc, const T* v, int* ns, const Status* st) {
+  switch (qpc) {
+    case 8: return run_bwd<T, 8>(c, v, ns, st);
+    case 16: return run_bwd<T, 16>(c, v, ns, st);
+    case 24: return run_bwd<T, 24>(c, v, ns, st);
+    case 32: return run_bwd<T, 32>(c, v, ns, st);
+  }
+  return fail(COFEM_EINVAL, "bad column chunk");
+}
+
+inline int chunk_width(int ldq, int qoff) { return std::min(QCHUNK, ldq - qoff); }
+
+// Psi = beta Phi^T Phi P + alpha .* P for all ldq columns, pi on the fly
+template <typename T>
+int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
+  Scalars sc = c->sc();
+  for (int qoff = 0; qoff < c->ldq; qoff += QCHUNK) {
+    const int qpc = chunk_width(c->ldq, qoff);
+    CKR(fwd_chunk<T>(c, qpc, (const T*)c->P, c->ldq, qoff, (T*)c->V, st));
+    CKR(allreduce(c, c->V, (size_t)c->Np * qpc, nccl_t<T>()));
+    int ns = 1;
+    CKR(bwd_chunk<T>(c, qpc, (const T*)c->V, &ns, st));
+    const int bs = elem_block(qpc);
+    k_combine<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+        c->Dp, c->ldq, qoff, qpc, ns, (const T*)c->ppart, beta, c->alpha, (const T*)c->P, (T*)c->Psi, sc, st);
+    c->launches++;
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+// the blocked PCG on resident R (= B), minv, groups; result in X
+template <typename T>
+int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* groups, const cofem_cg_config* cg,
+               cofem_cg_report* rep) {
+  Scalars sc = c->sc();
+  const int ldq = c->ldq;
+  const int bs = elem_block(ldq);
+  memset(rep, 0, sizeof(*rep));
+  // device status reset; rho[0] = 1
+  Status s0{};
+  CK(cudaMemcpyAsync(c->st, &s0, sizeof(Status), cudaMemcpyHostToDevice, c->stream));
+  std::vector<double> ones(ldq, 1.0);
+  CK(cudaMemcpyAsync(sc.rho[0], ones.data(), ldq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->frozen, 0, ldq * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream));
+
+  k_pcg_init<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
+      c->Dp, ldq, q_real, (T*)c->X, (T*)c->P, (const T*)c->R, c->minv, ngroups, groups, sc);
+  c->launches++;
+  CK(cudaGetLastError());
+  CKR(allreduce(c, sc.bn2, ldq, ncclFloat64));
+  CKR(allreduce(c, sc.rho_new, ldq, ncclFloat64));
+  // entry checks (cg.py:116-122) need ||B||
+  std::vector<double> bn2(ldq);
+  CK(cudaMemcpyAsync(bn2.data(), sc.bn2, ldq * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double b2 = 0;
+  for (double v : bn2) b2 += v;
+  const double bnorm = sqrt(b2);
+  if (bnorm == 0.0) {
+    rep->steps_taken = 0;
+    rep->final_relative_residual = 0.0;
+    rep->converged = 1;
+    return 0;
+  }
+  if (1.0 <= cg->tolerance) {
+    rep->steps_taken = 0;
+    rep->final_relative_residual = 1.0;
+    rep->converged = 1;
+    return 0;
+  }
+  k_direction<T><<<c->nblk_elem, bs, 0, c->stream>>>(c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance,
+                                                      cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
+                                                      ngroups, groups, sc, c->st);
+  c->launches++;
+  CK(cudaGetLastError());
+
+  int u = 1;
+  for (; u <= cg->max_steps; ++u) {
+    if (u > LAG) {
+      const int slot = (u - LAG) % LAG;
+      CK(cudaEventSynchronize(c->ev[slot]));
+      if (c->h_st[slot].done) break;
+    }
+    CKR(system_apply_dev<T>(c, beta, c->st));
+    CKR(allreduce(c, sc.pi, ldq, ncclFloat64));
+    k_update<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
+        c->Dp, ldq, q_real, u & 1, (T*)c->X, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, ngroups, groups,
+        sc, c->st);
+    c->launches++;
+    CK(cudaGetLastError());
+    CKR(allreduce(c, sc.rho_new, 2 * ldq, ncclFloat64));  // rho_new | rn2
+    k_direction<T><<<c->nblk_elem, bs, 0, c->stream>>>(c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance,
+                                                        cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
+                                                        ngroups, groups, sc, c->st);
+    c->launches++;
+    CK(cudaGetLastError());
+    const int slot = u % LAG;
+    CK(cudaMemcpyAsync(&c->h_st[slot], c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->ev[slot], c->stream));
+  }
+  Status fin;
+  CK(cudaMemcpyAsync(&fin, c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->pcg_steps += fin.steps;
+  rep->steps_taken = fin.steps;
+  rep->converged = fin.converged;
+  rep->diverged = fin.diverged;
+  rep->final_relative_residual = fin.delta;
+  std::vector<int> fz(ldq);
+  CK(cudaMemcpy(fz.data(), c->frozen, ldq * sizeof(int), cudaMemcpyDeviceToHost));
+  int nb = 0;
+  for (int q = 0; q < q_real; ++q) nb += fz[q] ? 1 : 0;
+  rep->n_breakdown = nb;
+  if (fin.diverged) return fail(COFEM_EDIVERGED, "non-finite residual at CG step " + std::to_string(fin.steps));
+  return 0;
+}
+
+// host double (rows x q, row stride q) -> device T (rows_pad x ldq, zero padded)
+template <typename T>
+int upload_block(cofem_ctx* c, const double* h, int64_t rows, int64_t q, int64_t rows_pad, int ldq, void* dst) {
+  std::vector<T> tmp((size_t)rows_pad * ldq, T(0));
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t k = 0; k < q; ++k) tmp[i * ldq + k] = (T)h[i * q + k];
+  CK(cudaMemcpyAsync(dst, tmp.data(), tmp.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+template <typename T>
+int download_block(cofem_ctx* c, const void* src, int64_t rows, int64_t q, int ldq, int qoff, double* h) {
+  std::vector<T> tmp((size_t)rows * ldq);
+  CK(cudaMemcpyAsync(tmp.data(), src, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t k = 0; k < q; ++k) h[i * q + k] = (double)tmp[i * ldq + qoff + k];
+  return 0;
+}
+
+int check_ctx(cofem_ctx* c, bool need_phi = true) {
+  if (!c) return fail(COFEM_EINVAL, "null context");
+  if (need_phi && !c->have_phi) return fail(COFEM_ESTATE, "no dictionary set");
+  return set_dev(c);
+}
+
+int ldq_for(int64_t q) { return (int)round_up(std::max<int64_t>(q, 1), 8); }
+
+// ---- apply / adjoint / system apply ---------------------------------------
+template <typename T>
+int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
+  const int ldq = ldq_for(q);
+  CKR(ensure_ws(c, ldq));
+  CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
+  std::vector<double> chunk;
+  for (int qoff = 0; qoff < ldq; qoff += QCHUNK) {
+    const int qpc = chunk_width(ldq, qoff);
+    CKR(fwd_chunk<T>(c, qpc, (const T*)c->P, ldq, qoff, (T*)c->V, nullptr));
+    CKR(allreduce(c, c->V, (size_t)c->Np * qpc, nccl_t<T>()));
+    const int64_t qn = std::min<int64_t>(qpc, q - qoff);
+    if (qn <= 0) break;
+    chunk.assign((size_t)c->N * qn, 0.0);
+    CKR(download_block<T>(c, c->V, c->N, qn, qpc, 0, chunk.data()));
+    for (int64_t i = 0; i < c->N; ++i)
+      for (int64_t k = 0; k < qn; ++k) out[i * q + qoff + k] = chunk[i * qn + k];
+  }
+  return 0;
+}
+
+template <typename T>
+int adjoint_impl(cofem_ctx* c, const double* U, int64_t q, double* out) {
+  const int ldq = ldq_for(q);
+  CKR(ensure_ws(c, ldq));
+  std::vector<double> chunk;
+  for (int qoff = 0; qoff < ldq; qoff += QCHUNK) {
+    const int qpc = chunk_width(ldq, qoff);
+    const int64_t qn = std::min<int64_t>(qpc, q - qoff);
+    if (qn <= 0) break;
+    // gather columns [qoff, qoff+qn) of U into a dense Np x qpc block
+    std::vector<double> sub((size_t)c->N * qn);
+    for (int64_t i = 0; i < c->N; ++i)
+      for (int64_t k = 0; k < qn; ++k) sub[i * qn + k] = U[i * q + qoff + k];
+    CKR(upload_block<T>(c, sub.data(), c->N, qn, c->Np, qpc, c->V));
+    int ns = 1;
+    CKR(bwd_chunk<T>(c, qpc, (const T*)c->V, &ns, nullptr));
+    const int64_t n = c->Dp * qpc;
+    k_sum_splits<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+        n, ns, (const T*)c->ppart, (T*)c->tmpD, nullptr);
+    c->launches++;
+    CK(cudaGetLastError());
+    chunk.assign((size_t)c->D * qn, 0.0);
+    CKR(download_block<T>(c, c->tmpD, c->D, qn, qpc, 0, chunk.data()));
+    for (int64_t j = 0; j < c->D; ++j)
+      for (int64_t k = 0; k < qn; ++k) out[j * q + qoff + k] = chunk[j * qn + k];
+  }
+  return 0;
+}
+
+template <typename T>
+int system_apply_impl(cofem_ctx* c, double beta, const double* alpha, const double* V, int64_t q, double* out) {
+  const int ldq = ldq_for(q);
+  CKR(ensure_ws(c, ldq));
+  std::vector<double> a(c->Dp, 0.0);
+  std::copy(alpha, alpha + c->D, a.begin());
+  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
+  CK(cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream));
+  CKR(system_apply_dev<T>(c, beta, nullptr));
+  CKR(download_block<T>(c, c->Psi, c->D, q, ldq, 0, out));
+  return 0;
+}
+
+// ---- EM loop ---------------------------------------------------------------
+template <typename T>
+int compute_aty(cofem_ctx* c, const double* y_host) {
+  // V[:, 0] = y, other columns 0 -> Phi^T V via the bwd contraction (8-wide)
+  CKR(ensure_ws(c, std::max(c->ldq, 8)));
+  std::vector<T> vb((size_t)c->Np * 8, T(0));
+  for (int64_t i = 0; i < c->N; ++i) vb[i * 8] = (T)y_host[i];
+  CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  int ns = 1;
+  CKR(bwd_chunk<T>(c, 8, (const T*)c->V, &ns, nullptr));
+  const int64_t n = c->Dp * 8;
+  k_sum_splits<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+      n, ns, (const T*)c->ppart, (T*)c->tmpD, nullptr);
+  c->launches++;
+  CK(cudaGetLastError());
+  std::vector<T> out((size_t)c->Dp * 8);
+  CK(cudaMemcpyAsync(out.data(), c->tmpD, out.size() * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<double> aty(c->Dp, 0.0);
+  for (int64_t j = 0; j < c->D; ++j) aty[j] = (double)out[j * 8];
+  CK(cudaMemcpy(c->aty, aty.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int ensure_em_buffers(cofem_ctx* c, int K) {
+  if (c->probes) cudaFree(c->probes);
+  if (c->probe_store) cudaFree(c->probe_store);
+  CK(cudaMalloc(&c->probes, (size_t)c->Dp * K));
+  CK(cudaMalloc(&c->probe_store, (size_t)c->Dp * K));
+  return 0;
+}
+
+template <typename T>
+int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em, const double* theta) {
+  const int K = em->probes;
+  const int ldq = ldq_for(K + 1);
+  CKR(ensure_ws(c, ldq));
+  CKR(ensure_em_buffers(c, K));
+  CKR(compute_aty<T>(c, y));
+  // alpha = 1 (PrecisionState.initial, cofem.py:65), theta by policy
+  std::vector<double> a(c->Dp, 1.0);
+  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  if (em->theta_policy == COFEM_THETA_JACOBI) {
+    k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
+    c->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->theta, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  } else if (em->theta_policy == COFEM_THETA_CUSTOM) {
+    if (!theta) return fail(COFEM_EINVAL, "custom theta policy needs a theta vector");
+    CK(cudaMemcpy(c->theta, theta, c->D * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  k_make_minv<<<(int)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->D, c->Dp, beta, c->alpha, c->theta,
+                                                                   em->theta_policy, c->minv);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+template <typename T>
+int em_iteration(cofem_ctx* c, int t, int T_total, double beta, const cofem_em_config* em,
+                 const cofem_cg_config* cg, const int8_t* probes_host_iter, uint64_t dseed, cofem_cg_report* rep) {
+  const int K = em->probes;
+  const int ldq = c->ldq;
+  if (probes_host_iter) {
+    CK(cudaMemcpyAsync(c->probes, probes_host_iter, (size_t)c->D * K, cudaMemcpyHostToDevice, c->stream));
+  }
+  const int bs = 256;
+  const int64_t n = c->Dp * ldq;
+  k_build_rhs<T><<<(int)std::min<int64_t>((n + bs - 1) / bs, 8 * c->sm_count), bs, 0, c->stream>>>(
+      c->D, c->Dp, ldq, K, probes_host_iter ? c->probes : nullptr, dseed, t, c->col_offset, c->aty, (T*)c->R,
+      c->probe_store);
+  c->launches++;
+  CK(cudaGetLastError());
+  int rc = pcg_device<T>(c, beta, K + 1, 1, nullptr, cg, rep);
+  if (rc != 0) return rc;
+  const int do_update = t < T_total ? 1 : 0;
+  k_em_finish<T><<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(
+      c->D, ldq, K, beta, (const T*)c->X, c->probe_store, c->mu, c->s, c->alpha, c->minv, c->theta,
+      em->theta_policy, do_update, em->variant, em->floor_eps, em->clamp_max);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+template <typename T>
+int run_impl(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em, const cofem_cg_config* cg,
+             const double* theta, const int8_t* probes, uint64_t dseed, double* alpha, double* mu, double* s,
+             int32_t* steps, double* resid, int32_t* fail_it, int32_t* fail_step) {
+  CKR(em_prepare<T>(c, y, beta, em, theta));
+  std::vector<double> alpha_used(c->D, 1.0);
+  for (int t = 1; t <= em->iterations; ++t) {
+    cofem_cg_report rep;
+    // alpha of this E-step is what the caller gets back after the last one
+    if (t == em->iterations && alpha) {
+      CK(cudaMemcpyAsync(alpha_used.data(), c->alpha, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    const int8_t* pt = probes ? probes + (size_t)(t - 1) * c->D * em->probes : nullptr;
+    int rc = em_iteration<T>(c, t, em->iterations, beta, em, cg, pt, dseed, &rep);
+    if (steps) steps[t - 1] = rep.steps_taken;
+    if (resid) resid[t - 1] = rep.final_relative_residual;
+    if (rc == COFEM_EDIVERGED) {
+      if (fail_it) *fail_it = t;
+      if (fail_step) *fail_step = rep.steps_taken;
+      return fail(COFEM_EDIVERGED, "non-finite residual at CG step " + std::to_string(rep.steps_taken) +
+                                       " (EM iteration " + std::to_string(t) + ")");
+    }
+    if (rc != 0) return rc;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  if (alpha) std::copy(alpha_used.begin(), alpha_used.end(), alpha);
+  if (mu) CK(cudaMemcpy(mu, c->mu, c->D * sizeof(double), cudaMemcpyDeviceToHost));
+  if (s) CK(cudaMemcpy(s, c->s, c->D * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int cofem_abi_version(void) { return COFEM_ABI_VERSION; }
+const char* cofem_last_error(void) { return g_err.c_str(); }
+
+int cofem_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return fail(COFEM_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *out = n;
+  return 0;
+}
+
+int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, int precision) {
+  if (!out) return fail(COFEM_EINVAL, "null out");
+  *out = nullptr;
+  if (n_rows < 1 || n_cols < 1) return fail(COFEM_EINVAL, "operator dims must be positive");
+  if (precision != COFEM_FP32 && precision != COFEM_FP64) return fail(COFEM_EINVAL, "precision must be FP32 or FP64");
+  cofem_ctx* c = new cofem_ctx();
+  c->device = device;
+  c->prec = precision;
+  c->N = n_rows;
+  c->D = n_cols;
+  c->Np = round_up(n_rows, PAD);
+  c->Dp = round_up(n_cols, PAD);
+  c->global_cols = n_cols;
+  auto bail = [&](int rc) {
+    cofem_destroy(c);
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(COFEM_ECUDA, "stream create failed"));
+  if (cudaMalloc(&c->phi, (size_t)c->Np * c->Dp * sizeof(float)) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "dictionary allocation failed"));
+  cudaMemset(c->phi, 0, (size_t)c->Np * c->Dp * sizeof(float));
+  double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty};
+  for (double** p : dvecs) {
+    if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
+    cudaMemset(*p, 0, c->Dp * sizeof(double));
+  }
+  if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
+  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "pinned status"));
+  for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+  *out = c;
+  return 0;
+}
+
+int cofem_destroy(cofem_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_ws(c);
+  void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
+                  c->probes, c->probe_store, c->groups, c->tickets, c->st};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  for (int i = 0; i < LAG; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  if (c->comm && g_nccl.ok) g_nccl.commDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_device) {
+  CKR(check_ctx(c, false));
+  if (!phi || ld < c->D) return fail(COFEM_EINVAL, "dictionary pointer / leading dimension");
+  CK(cudaMemcpy2DAsync(c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->have_phi = true;
+  return 0;
+}
+
+int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {
+  if (!c) return fail(COFEM_EINVAL, "null context");
+  if (col_offset < 0 || col_offset + c->D > global_cols || col_offset % 4 != 0)
+    return fail(COFEM_EINVAL, "shard must be 4-aligned and inside the global columns");
+  c->col_offset = col_offset;
+  c->global_cols = global_cols;
+  return 0;
+}
+
+int cofem_generate_gaussian_dictionary(cofem_ctx* c, uint64_t seed, double scale) {
+  CKR(check_ctx(c, false));
+  const int64_t total = c->N * ((c->D + 3) / 4);
+  const int gs = (int)std::min<int64_t>((total + 255) / 256, 64 * c->sm_count);
+  k_gen_gaussian<<<gs, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->col_offset, seed, scale);
+  c->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  c->have_phi = true;
+  return 0;
+}
+
+int cofem_get_dictionary(cofem_ctx* c, float* out) {
+  CKR(check_ctx(c));
+  CK(cudaMemcpy2D(out, c->D * sizeof(float), c->phi, c->Dp * sizeof(float), c->D * sizeof(float), c->N,
+                  cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int cofem_nccl_get_unique_id(void* out128) {
+  CKR(nccl_load());
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(COFEM_ENCCL, "ncclGetUniqueId failed");
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
+  CKR(check_ctx(c, false));
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
+  CKR(nccl_load());
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = g_nccl.commInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) return fail(COFEM_ENCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+  c->nranks = nranks;
+  c->rank = rank;
+  return 0;
+}
+
+#define DISPATCH(c, fn, ...) ((c)->prec == COFEM_FP64 ? fn<double>(__VA_ARGS__) : fn<float>(__VA_ARGS__))
+
+int cofem_apply(cofem_ctx* c, const double* V, int64_t q, double* out) {
+  CKR(check_ctx(c));
+  if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
+  return DISPATCH(c, apply_impl, c, V, q, out);
+}
+
+int cofem_apply_adjoint(cofem_ctx* c, const double* U, int64_t q, double* out) {
+  CKR(check_ctx(c));
+  if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
+  return DISPATCH(c, adjoint_impl, c, U, q, out);
+}
+
+int cofem_system_apply(cofem_ctx* c, double beta, const double* alpha, const double* V, int64_t q, double* out) {
+  CKR(check_ctx(c));
+  if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
+  if (!(beta > 0)) return fail(COFEM_EINVAL, "beta must be positive");
+  return DISPATCH(c, system_apply_impl, c, beta, alpha, V, q, out);
+}
+
+int cofem_column_sq_norms(cofem_ctx* c, double* out) {
+  CKR(check_ctx(c));
+  k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
+  c->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+template <typename T>
+int pcg_solve_impl(cofem_ctx* c, double beta, const double* alpha, const double* minv, int32_t ngroups,
+                   const int32_t* group_of_col, const double* B, int64_t q, const cofem_cg_config* cg, double* X,
+                   cofem_cg_report* rep, uint8_t* breakdown) {
+  const int ldq = ldq_for(q);
+  if (ldq > 1024) return fail(COFEM_EINVAL, "at most 1024 right-hand sides per solve");
+  CKR(ensure_ws(c, ldq));
+  std::vector<double> a(c->Dp, 0.0);
+  std::copy(alpha, alpha + c->D, a.begin());
+  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  // minv: D x ngroups (groups > 1 stored in a dedicated buffer)
+  double* minv_dev = c->minv;
+  double* minv_tmp = nullptr;
+  if (ngroups > 1) {
+    CK(cudaMalloc(&minv_tmp, (size_t)c->Dp * ngroups * sizeof(double)));
+    minv_dev = minv_tmp;
+  }
+  std::vector<double> m((size_t)c->Dp * ngroups, 0.0);
+  std::copy(minv, minv + (size_t)c->D * ngroups, m.begin());
+  CK(cudaMemcpy(minv_dev, m.data(), m.size() * sizeof(double), cudaMemcpyHostToDevice));
+  int* gdev = nullptr;
+  if (ngroups > 1) {
+    std::vector<int> g(ldq, 0);
+    for (int64_t k = 0; k < q; ++k) g[k] = group_of_col[k];
+    CKR(ensure_groups(c, ldq));
+    CK(cudaMemcpy(c->groups, g.data(), ldq * sizeof(int), cudaMemcpyHostToDevice));
+    gdev = c->groups;
+  }
+  CKR(upload_block<T>(c, B, c->D, q, c->Dp, ldq, c->R));
+  // pcg_device reads c->minv: temporarily swap in the grouped one
+  double* saved = c->minv;
+  c->minv = minv_dev;
+  int rc = pcg_device<T>(c, beta, (int)q, ngroups, gdev, cg, rep);
+  c->minv = saved;
+  if (minv_tmp) cudaFree(minv_tmp);
+  if (rc != 0 && rc != COFEM_EDIVERGED) return rc;
+  CKR(download_block<T>(c, c->X, c->D, q, ldq, 0, X));
+  if (breakdown) {
+    std::vector<int> fz(ldq);
+    CK(cudaMemcpy(fz.data(), c->frozen, ldq * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < q; ++k) breakdown[k] = fz[k] ? 1 : 0;
+  }
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int cofem_pcg_solve(cofem_ctx* c, double beta, const double* alpha, const double* minv, int32_t n_groups,
+                    const int32_t* group_of_col, const double* B, int64_t q, const cofem_cg_config* cg, double* X,
+                    cofem_cg_report* rep, uint8_t* breakdown) {
+  CKR(check_ctx(c));
+  if (!alpha || !minv || !B || !X || !cg || !rep || q < 1) return fail(COFEM_EINVAL, "null argument");
+  if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
+  if (n_groups < 1 || (n_groups > 1 && !group_of_col)) return fail(COFEM_EINVAL, "bad groups");
+  return DISPATCH(c, pcg_solve_impl, c, beta, alpha, minv, n_groups, group_of_col, B, q, cg, X, rep, breakdown);
+}
+
+int cofem_run(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em, const cofem_cg_config* cg,
+              const double* theta, const int8_t* probes, uint64_t dseed, double* alpha, double* mu, double* s,
+              int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration, int32_t* failed_step) {
+  CKR(check_ctx(c));
+  if (!y || !em || !cg) return fail(COFEM_EINVAL, "null argument");
+  if (em->iterations < 1 || em->probes < 1) return fail(COFEM_EINVAL, "iterations and probes must be >= 1");
+  if (em->probes + 1 > 1024) return fail(COFEM_EINVAL, "too many probes");
+  if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
+  if (!(beta > 0) || !std::isfinite(beta)) return fail(COFEM_EINVAL, "beta must be positive and finite");
+  return DISPATCH(c, run_impl, c, y, beta, em, cg, theta, probes, dseed, alpha, mu, s, cg_steps, cg_residuals,
+                  failed_iteration, failed_step);
+}
+
+int cofem_bench_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em,
+                        const cofem_cg_config* cg, uint64_t dseed) {
+  CKR(check_ctx(c));
+  if (!y || !em || !cg) return fail(COFEM_EINVAL, "null argument");
+  int rc = DISPATCH(c, em_prepare, c, y, beta, em, nullptr);
+  if (rc) return rc;
+  c->beta = beta;
+  c->em = *em;
+  c->cg = *cg;
+  c->dseed = dseed;
+  c->bench_iter = 0;
+  c->bench_ready = true;
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int cofem_bench_iterations(cofem_ctx* c, int n_iter, int time_kernels, cofem_timing* out) {
+  CKR(check_ctx(c));
+  if (!c->bench_ready) return fail(COFEM_ESTATE, "cofem_bench_prepare first");
+  c->time_kernels = time_kernels != 0;
+  c->evnext = 0;
+  c->timed.clear();
+  c->launches = c->fwd_launches = c->bwd_launches = c->pcg_steps = 0;
+  CK(cudaEventRecord(c->t0, c->stream));
+  for (int i = 0; i < n_iter; ++i) {
+    cofem_cg_report rep;
+    ++c->bench_iter;
+    // never let the benchmark reach the final (non-updating) iteration
+    const int t_total = c->bench_iter + 1;
+    int rc = DISPATCH(c, em_iteration, c, c->bench_iter, t_total, c->beta, &c->em, &c->cg, nullptr, c->dseed, &rep);
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(c->t1, c->stream));
+  CK(cudaEventSynchronize(c->t1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+  memset(out, 0, sizeof(*out));
+  out->total_ms = ms;
+  for (auto& tk : c->timed) {
+    float d = 0;
+    cudaEventElapsedTime(&d, c->evpool[tk.second], c->evpool[tk.second + 1]);
+    if (tk.first == 0) out->fwd_ms += d;
+    else out->bwd_ms += d;
+  }
+  out->fwd_launches = c->fwd_launches;
+  out->bwd_launches = c->bwd_launches;
+  out->pcg_steps = c->pcg_steps;
+  out->kernel_launches = c->launches;
+  c->time_kernels = false;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""GPU-resident dictionary operators and the implicit SBL system matrix.
+
+Mirrors /root/reference/pkg/src/sbl/operators.py for the dense kind (the hot
+path of this build): ``LinearOperator`` (:40-101), ``DenseOperator``
+(:104-129), ``SystemMatrix`` (:248-272), ``build_dense_gaussian`` (:227-232)
+and ``ShapeMismatchError`` (:21-27).
+
+Every application runs on the GPU through the C ABI (include/cofem_b200.h).
+The dictionary is stored once per precision mode as float32 in HBM (the
+reference keeps float64; a float64 matrix is rounded to float32 on upload --
+dictionaries built by this package are generated float32-exact).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+class ShapeMismatchError(ValueError):
+    """Input array shape is inconsistent with the operator (operators.py:21-27)."""
+
+    def __init__(self, what, expected, actual):
+        super().__init__(f"{what}: expected shape {expected}, got {actual}")
+        self.expected = expected
+        self.actual = actual
+
+
+def _as_columns(V, nrows, what):
+    V = np.asarray(V, dtype=np.float64)
+    single = V.ndim == 1
+    if single:
+        V = V[:, None]
+    if V.ndim != 2 or V.shape[0] != nrows:
+        raise ShapeMismatchError(what, (nrows, "Q"), np.shape(V))
+    return V, single
+
+
+PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64}
+
+
+class LinearOperator:
+    """An implicit N x D real matrix with apply / adjoint (operators.py:40-101)."""
+
+    kind = "abstract"
+
+    def __init__(self, n_rows, n_cols):
+        if n_rows < 1 or n_cols < 1:
+            raise ValueError(f"operator dims must be positive, got {n_rows} x {n_cols}")
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+
+    def _apply(self, V):
+        raise NotImplementedError
+
+    def _apply_adjoint(self, U):
+        raise NotImplementedError
+
+    def apply(self, V):
+        """Phi @ V for a (D,) vector or (D, Q) matrix."""
+        V, single = _as_columns(V, self.n_cols, f"{self.kind} apply")
+        out = self._apply(V)
+        return out[:, 0] if single else out
+
+    def apply_adjoint(self, U):
+        """Phi^T @ U for an (N,) vector or (N, Q) matrix."""
+        U, single = _as_columns(U, self.n_rows, f"{self.kind} apply_adjoint")
+        out = self._apply_adjoint(U)
+        return out[:, 0] if single else out
+
+    def column_sq_norms(self):
+        raise NotImplementedError
+
+
+class DenseOperator(LinearOperator):
+    """Explicit dense dictionary, resident in HBM as float32 (operators.py:104-129).
+
+    ``context(precision)`` returns the native context holding the matrix
+    (created on first use; one per precision mode).
+    """
+
+    kind = "explicit-dense"
+
+    def __init__(self, matrix, kind=None, device=0):
+        matrix = np.array(matrix)
+        if matrix.ndim != 2:
+            raise ValueError("dense operator needs a 2-D matrix")
+        super().__init__(*matrix.shape)
+        if matrix.dtype != np.float32:
+            matrix = matrix.astype(np.float64)
+        matrix.flags.writeable = False
+        self.matrix = matrix
+        self.device = device
+        if kind is not None:
+            self.kind = kind
+        self._ctx = {}
+
+    def context(self, precision="fp32"):
+        code = PRECISIONS[precision]
+        ctx = self._ctx.get(code)
+        if ctx is None:
+            ctx = _lib.Context(self.n_rows, self.n_cols, code, self.device)
+            ctx.set_dictionary(self.matrix)
+            self._ctx[code] = ctx
+        return ctx
+
+    def release(self):
+        """Free the device copies of the dictionary."""
+        for ctx in self._ctx.values():
+            ctx.close()
+        self._ctx.clear()
+
+    def _apply(self, V):
+        return self.context("fp64").apply(V)
+
+    def _apply_adjoint(self, U):
+        return self.context("fp64").apply_adjoint(U)
+
+    def materialize(self):
+        return np.array(self.matrix, dtype=np.float64)
+
+    def column_sq_norms(self):
+        return self.context("fp64").column_sq_norms()
+
+
+def build_dense_gaussian(n_rows, dim, rng):
+    """Dense dictionary with i.i.d. N(0, 1/N) entries (operators.py:227-232).
+
+    Drawn float32 (``rng.standard_normal(dtype=float32)``), so the float32
+    copy in HBM is exact and the float64 oracle sees identical entries.
+    """
+    if not 1 <= n_rows <= dim:
+        raise ValueError(f"need 1 <= N <= D, got N={n_rows}, D={dim}")
+    entries = rng.standard_normal((n_rows, dim), dtype=np.float32) * np.float32(1.0 / np.sqrt(n_rows))
+    return DenseOperator(entries, kind="dense-gaussian")
+
+
+class SystemMatrix:
+    """Implicit A = beta Phi^T Phi + diag(alpha), SPD by construction (operators.py:248-272)."""
+
+    def __init__(self, op, beta, alpha):
+        if beta <= 0:
+            raise ValueError(f"beta must be positive, got {beta}")
+        alpha = np.array(alpha, dtype=np.float64)
+        if alpha.shape != (op.n_cols,):
+            raise ShapeMismatchError("alpha", (op.n_cols,), alpha.shape)
+        if not np.all(alpha > 0):
+            raise ValueError("alpha entries must all be positive")
+        alpha.flags.writeable = False
+        self.op = op
+        self.beta = float(beta)
+        self.alpha = alpha
+
+    @property
+    def dim(self):
+        return self.op.n_cols
+
+    def apply(self, V, precision="fp64"):
+        """A @ V on the GPU without materialising A."""
+        V, single = _as_columns(V, self.dim, "system apply")
+        out = self.op.context(precision).system_apply(self.beta, self.alpha, V)
+        return out[:, 0] if single else out

@@ -1,0 +1,105 @@
+"""Synthetic workloads of BASELINE.json (seeded stand-ins for the paper's data).
+
+Stream layout follows the reference's simulate.build_problem
+(/root/reference/pkg/src/sbl/simulate.py:242-249): dictionary from
+substream(seed, 0), spikes from substream(seed, 1), noise from
+substream(seed, 2); probes come from substream(seed, 3) inside run_cofem.
+The dense dictionary is drawn float32 (N(0,1) scaled by 1/sqrt(N)) so the
+GPU copy is exact; spike amplitudes are N(0, 1) as BASELINE.json specifies.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .cg import CgConfig
+from .cofem import CofemConfig
+from .operators import DenseOperator
+from .problem import SblProblem, substream
+
+
+@dataclass(frozen=True)
+class DenseCsConfig:
+    name: str
+    N: int
+    D: int
+    frac: float      # fraction of nonzero coefficients
+    sigma: float     # noise std; beta = 1 / sigma^2
+    K: int           # probes
+    T: int           # EM iterations
+    U: int           # PCG step cap
+    tol: float       # PCG tolerance
+    seed: int = 0
+
+    @property
+    def beta(self):
+        return 1.0 / self.sigma**2
+
+    @property
+    def n_spikes(self):
+        return int(round(self.frac * self.D))
+
+    def cofem_config(self, precision="fp32", **over):
+        cg = CgConfig(max_steps=self.U, tolerance=self.tol, precision=precision)
+        kw = dict(iterations=self.T, probes=self.K, cg=cg, seed=self.seed)
+        kw.update(over)
+        return CofemConfig(**kw)
+
+
+# BASELINE.json "configs" (dense Gaussian compressed sensing rows)
+CONFIGS = {
+    "dense-small": DenseCsConfig("dense-small", 256, 1024, 0.05, 0.01, 20, 50, 100, 1e-5),
+    "dense-mid": DenseCsConfig("dense-mid", 4096, 16384, 0.02, 0.01, 20, 30, 200, 1e-5),
+    "dense-large": DenseCsConfig("dense-large", 16384, 65536, 0.01, 0.01, 20, 20, 200, 1e-5),
+}
+
+
+def gaussian_dictionary(N, D, seed):
+    """N x D float32, entries N(0, 1/N), from substream(seed, 0)."""
+    rng = substream(seed, 0)
+    phi = rng.standard_normal((N, D), dtype=np.float32)
+    phi *= np.float32(1.0 / np.sqrt(N))
+    return phi
+
+
+def sparse_signal(D, n_spikes, seed):
+    """z with n_spikes uniformly placed N(0,1) entries, from substream(seed, 1)."""
+    rng = substream(seed, 1)
+    z = np.zeros(D)
+    if n_spikes:
+        support = rng.choice(D, size=n_spikes, replace=False)
+        z[support] = rng.standard_normal(n_spikes)
+    return z
+
+
+def observe(phi, z, sigma, seed):
+    """y = Phi z + sigma * N(0, I) in float64, noise from substream(seed, 2)."""
+    nz = np.flatnonzero(z)
+    y = phi[:, nz].astype(np.float64) @ z[nz]
+    return y + sigma * substream(seed, 2).standard_normal(phi.shape[0])
+
+
+def dense_cs_problem(cfg: DenseCsConfig, phi=None):
+    """(SblProblem, z_true, phi) for a dense Gaussian CS configuration."""
+    if phi is None:
+        phi = gaussian_dictionary(cfg.N, cfg.D, cfg.seed)
+    z = sparse_signal(cfg.D, cfg.n_spikes, cfg.seed)
+    y = observe(phi, z, cfg.sigma, cfg.seed)
+    return SblProblem(y, DenseOperator(phi, kind="dense-gaussian"), cfg.beta), z, phi
+
+
+def nrmse(z_hat, z_true):
+    """||zhat - z*|| / ||z*|| as a percentage (simulate.py:105-113)."""
+    z_hat = np.asarray(z_hat, dtype=np.float64)
+    z_true = np.asarray(z_true, dtype=np.float64)
+    denom = np.linalg.norm(z_true)
+    if denom == 0.0:
+        raise ValueError("ground truth is identically zero")
+    return 100.0 * np.linalg.norm(z_hat - z_true) / denom
+
+
+def nmse(z_hat, z_true):
+    """||zhat - z*||^2 / ||z*||^2 (the north_star's NMSE)."""
+    return (nrmse(z_hat, z_true) / 100.0) ** 2
