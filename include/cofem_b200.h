@@ -44,8 +44,12 @@ enum cofem_status {
  *       (the north_star's "GPU runs fp32").
  * FP64: Phi stays fp32 in HBM; vectors, contraction accumulators and scalars
  *       are fp64 (fp32 Phi entries are exact in fp64, so this reproduces the
- *       reference's float64 arithmetic up to summation order). */
-enum cofem_precision { COFEM_FP32 = 0, COFEM_FP64 = 1 };
+ *       reference's float64 arithmetic up to summation order).
+ * OZAKI: fp64 vectors and scalars; the two Phi contractions run on the int8
+ *       tensor cores (tcgen05.mma.kind::i8) over a 32-bit fixed-point copy of
+ *       Phi (four signed digit planes, 4 B / entry) with exact int32
+ *       accumulation -- float64-grade results at tensor-core rate. */
+enum cofem_precision { COFEM_FP32 = 0, COFEM_FP64 = 1, COFEM_OZAKI = 2 };
 
 /* Preconditioner policy, cg.py:79-108 make_preconditioner(policy, ...). */
 enum cofem_theta { COFEM_THETA_ALL_ONES = 0, COFEM_THETA_JACOBI = 1, COFEM_THETA_NONE = 2,

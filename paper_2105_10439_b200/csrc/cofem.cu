@@ -15,8 +15,13 @@
 #include <vector>
 
 #include "../../include/cofem_b200.h"
+#include <cuda.h>
+
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "nccl.h"
+#include "ozaki.cuh"
 #include "pcg.cuh"
 
 using namespace cofem;
@@ -78,6 +83,32 @@ int nccl_load() {
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+int encode_u8_3d(CUtensorMap* m, void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+                 uint32_t b2) {
+  if (!g_encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(COFEM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode = (EncodeTiledFn)fn;
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0, d0 * d1};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COFEM_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
+
 // ---- contraction configurations -------------------------------------------
 // fp32: 4 rows (fwd) / 4 columns (bwd) x QP accumulators per thread
 // fp64: 2 x QP double accumulators per thread
@@ -130,6 +161,17 @@ struct cofem_ctx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int nblk_elem = 0;
 
+  // Ozaki (int8 tensor-core) contraction state
+  bool oz_ready = false;
+  int8_t* phiq = nullptr;        // [4][Np][Dp] signed digit planes
+  double *rowscale = nullptr, *colscale = nullptr;  // Np, Dp powers of two
+  int8_t *pq = nullptr, *vq = nullptr;              // operand planes [4][QW][Dp] / [4][QW][Np]
+  double* opscale = nullptr;                        // QCHUNK column scales
+  unsigned long long* colmax = nullptr;             // QCHUNK
+  CUtensorMap map_phi_fwd{}, map_phi_bwd{};
+  CUtensorMap map_p[5]{}, map_v[5]{};               // by QW / 8
+  bool map_p_ok[5] = {}, map_v_ok[5] = {};
+
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -162,7 +204,7 @@ struct cofem_ctx {
     s.ticket = tickets;
     return s;
   }
-  size_t tsize() const { return prec == COFEM_FP64 ? 8 : 4; }
+  size_t tsize() const { return prec == COFEM_FP32 ? 4 : 8; }
 };
 
 namespace {
@@ -293,10 +335,136 @@ ncclDataType_t nccl_t() {
   return sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
 }
 
+// ---- Ozaki int8 tensor-core contractions -----------------------------------
+int ensure_oz(cofem_ctx* c) {
+  if (c->oz_ready) return 0;
+  if (!c->phiq) {
+    CK(cudaMalloc(&c->phiq, (size_t)4 * c->Np * c->Dp));
+    CK(cudaMalloc(&c->rowscale, c->Np * sizeof(double)));
+    CK(cudaMalloc(&c->colscale, c->Dp * sizeof(double)));
+    CK(cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp));
+    CK(cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np));
+    CK(cudaMalloc(&c->opscale, QCHUNK * sizeof(double)));
+    CK(cudaMalloc(&c->colmax, QCHUNK * sizeof(unsigned long long)));
+    CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
+    CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
+  }
+  oz::k_phi_rowscale<<<(unsigned)c->Np, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->rowscale);
+  oz::k_phi_colscale<<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->Dp, c->rowscale,
+                                                                              c->colscale);
+  oz::k_phi_planes<<<16 * c->sm_count, 256, 0, c->stream>>>(c->phi, c->Dp, c->Np, c->Dp, c->rowscale, c->colscale,
+                                                            c->phiq);
+  c->launches += 3;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+  c->oz_ready = true;
+  return 0;
+}
+
+template <int QW>
+int oz_init_kernels() {
+  static bool done = false;
+  if (done) return 0;
+  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)oz::Cfg<QW>::SMEM));
+  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)oz::Cfg<QW>::SMEM));
+  done = true;
+  return 0;
+}
+
+// quantise columns [qoff, qoff+QW) of M (k_real rows, row stride ldm) into planes
+template <typename T, int QW>
+int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int64_t k_pad, const double* pre,
+                int8_t* planes, const Status* st) {
+  CK(cudaMemsetAsync(c->colmax, 0, QCHUNK * sizeof(unsigned long long), c->stream));
+  const int bs = QW * (256 / QW);
+  oz::k_colmax<T><<<2 * c->sm_count, bs, 0, c->stream>>>(k_real, ldm, qoff, QW, M, pre, c->colmax, st);
+  const int64_t n = k_pad * QW;
+  oz::k_quantize<T><<<(unsigned)std::min<int64_t>((n + 255) / 256, 16 * c->sm_count), 256, 0, c->stream>>>(
+      k_real, k_pad, ldm, qoff, QW, M, pre, c->colmax, c->opscale, planes, st);
+  c->launches += 2;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// one persistent contraction launch; out = fp64 split partials [S][rows][QW]
+template <int QW, bool BWD>
+int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int64_t k_total, const double* row_scale,
+                double* out, int* nsplit_out, const Status* st) {
+  CKR(oz_init_kernels<QW>());
+  const int64_t n_mblocks = n_rows_out / oz::BM;
+  const int64_t ntiles = k_total / oz::KT;
+  SplitPlan sp = plan_splits(n_mblocks, ntiles, oz::KT, c->sm_count, (double)n_rows_out * QW * 8.0,
+                             (double)c->Np * c->Dp * 4.0);
+  // exact int32 accumulation: |digit products| <= 2^14, so keep K <= 2^16 per item
+  while (sp.per_split > 65536 || (size_t)sp.nsplit * n_rows_out * QW * 8 > (BWD ? c->ppart_cap : c->vpart_cap)) {
+    if (sp.per_split > 65536) sp.per_split = 65536;
+    else sp.per_split *= 2;
+    sp.nsplit = (int)((k_total + sp.per_split - 1) / sp.per_split);
+  }
+  const int n_items = (int)(n_mblocks * sp.nsplit);
+  const int grid = std::min(n_items, c->sm_count);
+  const CUtensorMap& map_a = BWD ? c->map_phi_bwd : c->map_phi_fwd;
+  cudaEvent_t e0 = nullptr;
+  if (c->time_kernels) {
+    e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  oz::contract_kernel<QW, BWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+      map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, row_scale, c->opscale, out, n_rows_out, st);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({BWD ? 1 : 0, c->evnext - 2});
+  }
+  (void)e0;
+  c->launches++;
+  if (BWD) c->bwd_launches++;
+  else c->fwd_launches++;
+  CK(cudaGetLastError());
+  *nsplit_out = sp.nsplit;
+  return 0;
+}
+
+template <int QW>
+int oz_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, const Status* st) {
+  CKR(ensure_oz(c));
+  const int slot = QW / 8;
+  if (!c->map_p_ok[slot]) {
+    CKR(encode_u8_3d(&c->map_p[slot], c->pq, c->Dp, QW, 4, oz::KT, QW, 4));
+    c->map_p_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, st)));
+  int ns = 1;
+  CKR((oz_contract<QW, false>(c, c->map_p[slot], c->Np, c->Dp, c->rowscale, (double*)c->vpart, &ns, st)));
+  const int64_t n = c->Np * QW;
+  k_sum_splits<double><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+      n, ns, (const double*)c->vpart, vout, st);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+template <int QW>
+int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
+  CKR(ensure_oz(c));
+  const int slot = QW / 8;
+  if (!c->map_v_ok[slot]) {
+    CKR(encode_u8_3d(&c->map_v[slot], c->vq, c->Np, QW, 4, oz::KT, QW, 4));
+    c->map_v_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->rowscale, c->vq, st)));
+  return oz_contract<QW, true>(c, c->map_v[slot], c->Dp, c->Np, c->colscale, (double*)c->ppart, nsplit_out, st);
+}
+
 // ---- the two contractions ----------------------------------------------
 // fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
 template <typename T, int QP>
 int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status* st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (c->prec == COFEM_OZAKI) return oz_fwd<QP>(c, src, lds, qoff, vout, st);
+  }
   using K = Kern<T, QP>;
   CKR(K::init());
   const int64_t ntiles = c->Dp / Tiles<T>::FBK;
@@ -334,6 +502,9 @@ int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status
 // bwd: ppart = Phi^T V  (V Np x QP dense); returns number of splits
 template <typename T, int QP>
 int run_bwd(cofem_ctx* c, const T* v, int* nsplit_out, const Status* st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (c->prec == COFEM_OZAKI) return oz_bwd<QP>(c, v, nsplit_out, st);
+  }
   using K = Kern<T, QP>;
   CKR(K::init());
   const int64_t ntiles = c->Np / Tiles<T>::BBK;
@@ -727,7 +898,8 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   if (!out) return fail(COFEM_EINVAL, "null out");
   *out = nullptr;
   if (n_rows < 1 || n_cols < 1) return fail(COFEM_EINVAL, "operator dims must be positive");
-  if (precision != COFEM_FP32 && precision != COFEM_FP64) return fail(COFEM_EINVAL, "precision must be FP32 or FP64");
+  if (precision != COFEM_FP32 && precision != COFEM_FP64 && precision != COFEM_OZAKI)
+    return fail(COFEM_EINVAL, "precision must be FP32, FP64 or OZAKI");
   cofem_ctx* c = new cofem_ctx();
   c->device = device;
   c->prec = precision;
@@ -773,7 +945,8 @@ int cofem_destroy(cofem_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
-                  c->probes, c->probe_store, c->groups, c->tickets, c->st};
+                  c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
+                  c->pq, c->vq, c->opscale, c->colmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -795,6 +968,7 @@ int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_devi
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->have_phi = true;
+  c->oz_ready = false;
   return 0;
 }
 
@@ -816,6 +990,7 @@ int cofem_generate_gaussian_dictionary(cofem_ctx* c, uint64_t seed, double scale
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
   c->have_phi = true;
+  c->oz_ready = false;
   return 0;
 }
 
@@ -848,7 +1023,7 @@ int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
   return 0;
 }
 
-#define DISPATCH(c, fn, ...) ((c)->prec == COFEM_FP64 ? fn<double>(__VA_ARGS__) : fn<float>(__VA_ARGS__))
+#define DISPATCH(c, fn, ...) ((c)->prec == COFEM_FP32 ? fn<float>(__VA_ARGS__) : fn<double>(__VA_ARGS__))
 
 int cofem_apply(cofem_ctx* c, const double* V, int64_t q, double* out) {
   CKR(check_ctx(c));

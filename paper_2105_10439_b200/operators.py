@@ -37,7 +37,7 @@ def _as_columns(V, nrows, what):
     return V, single
 
 
-PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64}
+PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}
 
 
 class LinearOperator:

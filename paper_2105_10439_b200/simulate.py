@@ -41,7 +41,7 @@ class DenseCsConfig:
     def n_spikes(self):
         return int(round(self.frac * self.D))
 
-    def cofem_config(self, precision="fp32", **over):
+    def cofem_config(self, precision="ozaki", **over):
         cg = CgConfig(max_steps=self.U, tolerance=self.tol, precision=precision)
         kw = dict(iterations=self.T, probes=self.K, cg=cg, seed=self.seed)
         kw.update(over)

@@ -1,0 +1,123 @@
+"""Host-side logic of the drop-in API (no GPU): validation, probe streams,
+preconditioner construction, generators.  Mirrors the validation cases of the
+reference's tests (test_cg.py, test_cofem.py, test_operators.py)."""
+
+import numpy as np
+import pytest
+
+from oracle import cofem_oracle as O
+from paper_2105_10439_b200 import (
+    CgConfig,
+    CofemConfig,
+    DenseOperator,
+    PosteriorEstimate,
+    Preconditioner,
+    PrecisionState,
+    SblProblem,
+    ShapeMismatchError,
+    SystemMatrix,
+    draw_probe_blocks,
+    draw_rademacher,
+    estimate_diagonal_rademacher,
+    m_step,
+    m_step_nonneg,
+    make_preconditioner,
+    substream,
+)
+from paper_2105_10439_b200 import simulate as S
+from paper_2105_10439_b200.probes import draw_rademacher_int8
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        CgConfig(max_steps=0)
+    with pytest.raises(ValueError):
+        CgConfig(tolerance=0.0)
+    with pytest.raises(ValueError):
+        CgConfig(precision="fp16")
+    with pytest.raises(ValueError, match="iterations"):
+        CofemConfig(iterations=0)
+    with pytest.raises(ValueError, match="variant"):
+        CofemConfig(variant="laplace")
+    with pytest.raises(ValueError, match="filter_percentile"):
+        CofemConfig(filter_percentile=1.5)
+
+
+def test_preconditioner_validation_and_policies():
+    with pytest.raises(ValueError):
+        Preconditioner(m=np.array([1.0, 0.0]))
+    np.testing.assert_array_equal(Preconditioner.identity(3).m, np.ones(3))
+    op = DenseOperator(np.zeros((4, 5)))
+    np.testing.assert_array_equal(make_preconditioner("all-ones", op, 1e4, np.ones(5)).m, np.full(5, 10001.0))
+    np.testing.assert_array_equal(make_preconditioner("none", op, 1e4, np.ones(5)).m, np.ones(5))
+    custom = make_preconditioner(np.arange(1.0, 6.0), op, 2.0, np.ones(5))
+    np.testing.assert_array_equal(custom.m, 2.0 * np.arange(1.0, 6.0) + 1.0)
+    with pytest.raises(ValueError, match="custom theta"):
+        make_preconditioner(np.array([1.0, -2.0, 3.0, 4.0, 5.0]), op, 2.0, np.ones(5))
+    with pytest.raises(ValueError, match="theta policy"):
+        make_preconditioner("spectral", op, 2.0, np.ones(5))
+    with pytest.raises(ValueError, match="alpha"):
+        make_preconditioner("all-ones", op, 2.0, np.zeros(5))
+
+
+def test_system_and_problem_validation():
+    op = DenseOperator(np.eye(4))
+    with pytest.raises(ValueError, match="beta"):
+        SystemMatrix(op, 0.0, np.ones(4))
+    with pytest.raises(ShapeMismatchError):
+        SystemMatrix(op, 1.0, np.ones(5))
+    with pytest.raises(ValueError, match="alpha"):
+        SystemMatrix(op, 1.0, np.array([1.0, 1.0, 0.0, 1.0]))
+    with pytest.raises(ShapeMismatchError):
+        SblProblem(np.ones(3), op, 1.0)
+    with pytest.raises(ValueError, match="beta"):
+        SblProblem(np.ones(4), op, -1.0)
+    with pytest.raises(ValueError):
+        DenseOperator(np.empty((0, 3)))
+    dense = DenseOperator(np.ones((2, 3)))
+    with pytest.raises(ValueError):
+        dense.matrix[0, 0] = 2.0
+
+
+def test_probe_stream_matches_reference_draws():
+    # the int8 draw consumes the generator exactly like probes.py:13-17
+    a = draw_rademacher_int8(257, 9, substream(7, 3))
+    b = O.draw_rademacher(257, 9, substream(7, 3))
+    np.testing.assert_array_equal(a.astype(np.float64), b)
+    np.testing.assert_array_equal(draw_rademacher(257, 9, substream(7, 3)), b)
+    # T sequential blocks, as run_cofem draws them (cofem.py:143-151)
+    blocks = draw_probe_blocks(64, 5, 4, seed=11)
+    rng = substream(11, 3)
+    for t in range(4):
+        np.testing.assert_array_equal(blocks[t].astype(np.float64), O.draw_rademacher(64, 5, rng))
+    with pytest.raises(ValueError):
+        draw_rademacher(0, 3, substream(0, 0))
+
+
+def test_estimator_and_m_steps_match_oracle(rng):
+    probes = draw_rademacher(12, 7, rng)
+    np.testing.assert_array_equal(estimate_diagonal_rademacher(probes, probes), np.ones(12))
+    X = rng.standard_normal((12, 7))
+    np.testing.assert_allclose(estimate_diagonal_rademacher(probes, X),
+                               O.estimate_diagonal_rademacher(probes, X), rtol=1e-15)
+    state = PrecisionState.initial(2)
+    upd = m_step(PosteriorEstimate(mu=np.array([1.0, 0.0]), s=np.array([0.0, -1.0])), state)
+    np.testing.assert_array_equal(upd.alpha, [1.0, state.clamp_max])
+    assert upd.iteration == 2
+    mu = rng.standard_normal(50) * 3
+    s = rng.random(50) - 0.2
+    np.testing.assert_allclose(m_step_nonneg(PosteriorEstimate(mu, s), PrecisionState.initial(50)).alpha,
+                               O.m_step_nonneg(mu, s), rtol=1e-14)
+
+
+def test_simulate_generators_are_deterministic():
+    c = S.CONFIGS["dense-small"]
+    p1, z1, phi1 = S.dense_cs_problem(c)
+    p2, z2, phi2 = S.dense_cs_problem(c)
+    np.testing.assert_array_equal(phi1, phi2)
+    np.testing.assert_array_equal(np.asarray(p1.y), np.asarray(p2.y))
+    assert phi1.dtype == np.float32 and phi1.shape == (c.N, c.D)
+    assert np.count_nonzero(z1) == c.n_spikes
+    assert 0.8 / c.N <= phi1.astype(np.float64).var() <= 1.2 / c.N
+    assert p1.beta == pytest.approx(1e4)
+    assert S.nrmse(z1, z1) == 0.0
