@@ -167,7 +167,9 @@ struct cofem_ctx {
   double *rowscale = nullptr, *colscale = nullptr;  // Np, Dp powers of two
   int8_t *pq = nullptr, *vq = nullptr;              // operand planes [4][QW][Dp] / [4][QW][Np]
   double* opscale = nullptr;                        // QCHUNK column scales
-  unsigned long long* colmax = nullptr;             // QCHUNK
+  unsigned long long* colmax = nullptr;             // P column maxima (up to 1024 columns)
+  unsigned long long* vcolmax = nullptr;            // V column maxima (QCHUNK)
+  bool p_colmax_valid = false, v_colmax_valid = false;
   CUtensorMap map_phi_fwd{}, map_phi_bwd{};
   CUtensorMap map_p[5]{}, map_v[5]{};               // by QW / 8
   bool map_p_ok[5] = {}, map_v_ok[5] = {};
@@ -345,7 +347,8 @@ int ensure_oz(cofem_ctx* c) {
     CK(cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp));
     CK(cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np));
     CK(cudaMalloc(&c->opscale, QCHUNK * sizeof(double)));
-    CK(cudaMalloc(&c->colmax, QCHUNK * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)));
     CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
     CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
   }
@@ -373,17 +376,23 @@ int oz_init_kernels() {
   return 0;
 }
 
-// quantise columns [qoff, qoff+QW) of M (k_real rows, row stride ldm) into planes
+// quantise columns [qoff, qoff+QW) of M (k_real rows, row stride ldm) into planes;
+// colmax (QW entries) holds the column maxima when `colmax_ready`
 template <typename T, int QW>
 int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int64_t k_pad, const double* pre,
-                int8_t* planes, const Status* st) {
-  CK(cudaMemsetAsync(c->colmax, 0, QCHUNK * sizeof(unsigned long long), c->stream));
-  const int bs = QW * (256 / QW);
-  oz::k_colmax<T><<<2 * c->sm_count, bs, 0, c->stream>>>(k_real, ldm, qoff, QW, M, pre, c->colmax, st);
-  const int64_t n = k_pad * QW;
-  oz::k_quantize<T><<<(unsigned)std::min<int64_t>((n + 255) / 256, 16 * c->sm_count), 256, 0, c->stream>>>(
-      k_real, k_pad, ldm, qoff, QW, M, pre, c->colmax, c->opscale, planes, st);
-  c->launches += 2;
+                int8_t* planes, unsigned long long* colmax, bool colmax_ready, unsigned long long* reset,
+                const Status* st) {
+  if (!colmax_ready) {
+    CK(cudaMemsetAsync(colmax, 0, QW * sizeof(unsigned long long), c->stream));
+    const int bs = QW * (256 / QW);
+    oz::k_colmax<T><<<2 * c->sm_count, bs, bs * sizeof(double), c->stream>>>(k_real, ldm, qoff, QW, M, pre, colmax,
+                                                                             st);
+    c->launches++;
+  }
+  const int64_t ntile = k_pad / oz::QTILE;
+  oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>(ntile, 4 * c->sm_count), 256, 0, c->stream>>>(
+      k_real, k_pad, ldm, qoff, M, pre, colmax, c->opscale, planes, reset, st);
+  c->launches++;
   CK(cudaGetLastError());
   return 0;
 }
@@ -435,14 +444,18 @@ int oz_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, con
     CKR(encode_u8_3d(&c->map_p[slot], c->pq, c->Dp, QW, 4, oz::KT, QW, 4));
     c->map_p_ok[slot] = true;
   }
-  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, st)));
+  // P's column maxima come fused out of k_direction inside a PCG solve; the
+  // quantiser resets the V maxima that k_sum_splits accumulates next
+  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
+                               c->p_colmax_valid, c->vcolmax, st)));
   int ns = 1;
   CKR((oz_contract<QW, false>(c, c->map_p[slot], c->Np, c->Dp, c->rowscale, (double*)c->vpart, &ns, st)));
-  const int64_t n = c->Np * QW;
-  k_sum_splits<double><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-      n, ns, (const double*)c->vpart, vout, st);
+  const int bs = elem_block(QW);
+  k_sum_splits<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      c->Np, QW, ns, (const double*)c->vpart, vout, c->rowscale, c->vcolmax, st);
   c->launches++;
   CK(cudaGetLastError());
+  c->v_colmax_valid = true;
   return 0;
 }
 
@@ -454,7 +467,9 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
     CKR(encode_u8_3d(&c->map_v[slot], c->vq, c->Np, QW, 4, oz::KT, QW, 4));
     c->map_v_ok[slot] = true;
   }
-  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->rowscale, c->vq, st)));
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->rowscale, c->vq, c->vcolmax, c->v_colmax_valid,
+                               nullptr, st)));
+  c->v_colmax_valid = false;
   return oz_contract<QW, true>(c, c->map_v[slot], c->Dp, c->Np, c->colscale, (double*)c->ppart, nsplit_out, st);
 }
 
@@ -490,10 +505,9 @@ int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status
   c->launches++;
   c->fwd_launches++;
   CK(cudaGetLastError());
-  const int64_t n = c->Np * QP;
-  const int bs = 256;
-  const int gs = (int)std::min<int64_t>((n + bs - 1) / bs, 8 * c->sm_count);
-  k_sum_splits<T><<<gs, bs, 0, c->stream>>>(n, sp.nsplit, (const T*)c->vpart, vout, st);
+  const int bs = elem_block(QP);
+  k_sum_splits<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(c->Np, QP, sp.nsplit, (const T*)c->vpart,
+                                                                        vout, nullptr, nullptr, st);
   c->launches++;
   CK(cudaGetLastError());
   return 0;
@@ -618,11 +632,20 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     rep->converged = 1;
     return 0;
   }
-  k_direction<T><<<c->nblk_elem, bs, 0, c->stream>>>(c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance,
-                                                      cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
-                                                      ngroups, groups, sc, c->st);
+  // ozaki: k_direction also emits the column maxima of diag(c) P for the next
+  // Phi P quantisation (k_update re-zeroes them every step)
+  const bool oz = c->prec == COFEM_OZAKI;
+  if (oz) {
+    CKR(ensure_oz(c));
+    CK(cudaMemsetAsync(c->colmax, 0, ldq * sizeof(unsigned long long), c->stream));
+  }
+  unsigned long long* pmax = oz ? c->colmax : nullptr;
+  k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
+      ngroups, groups, sc, c->colscale, pmax, c->st);
   c->launches++;
   CK(cudaGetLastError());
+  c->p_colmax_valid = oz;
 
   int u = 1;
   for (; u <= cg->max_steps; ++u) {
@@ -635,19 +658,20 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     CKR(allreduce(c, sc.pi, ldq, ncclFloat64));
     k_update<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, u & 1, (T*)c->X, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, ngroups, groups,
-        sc, c->st);
+        sc, pmax, c->st);
     c->launches++;
     CK(cudaGetLastError());
     CKR(allreduce(c, sc.rho_new, 2 * ldq, ncclFloat64));  // rho_new | rn2
-    k_direction<T><<<c->nblk_elem, bs, 0, c->stream>>>(c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance,
-                                                        cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
-                                                        ngroups, groups, sc, c->st);
+    k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+        c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
+        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st);
     c->launches++;
     CK(cudaGetLastError());
     const int slot = u % LAG;
     CK(cudaMemcpyAsync(&c->h_st[slot], c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaEventRecord(c->ev[slot], c->stream));
   }
+  c->p_colmax_valid = false;
   Status fin;
   CK(cudaMemcpyAsync(&fin, c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -729,11 +753,12 @@ int adjoint_impl(cofem_ctx* c, const double* U, int64_t q, double* out) {
     for (int64_t i = 0; i < c->N; ++i)
       for (int64_t k = 0; k < qn; ++k) sub[i * qn + k] = U[i * q + qoff + k];
     CKR(upload_block<T>(c, sub.data(), c->N, qn, c->Np, qpc, c->V));
+    c->v_colmax_valid = false;
     int ns = 1;
     CKR(bwd_chunk<T>(c, qpc, (const T*)c->V, &ns, nullptr));
-    const int64_t n = c->Dp * qpc;
-    k_sum_splits<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-        n, ns, (const T*)c->ppart, (T*)c->tmpD, nullptr);
+    const int bs = elem_block(qpc);
+    k_sum_splits<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(c->Dp, qpc, ns, (const T*)c->ppart,
+                                                                          (T*)c->tmpD, nullptr, nullptr, nullptr);
     c->launches++;
     CK(cudaGetLastError());
     chunk.assign((size_t)c->D * qn, 0.0);
@@ -766,11 +791,12 @@ int compute_aty(cofem_ctx* c, const double* y_host) {
   std::vector<T> vb((size_t)c->Np * 8, T(0));
   for (int64_t i = 0; i < c->N; ++i) vb[i * 8] = (T)y_host[i];
   CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  c->v_colmax_valid = false;
   int ns = 1;
   CKR(bwd_chunk<T>(c, 8, (const T*)c->V, &ns, nullptr));
-  const int64_t n = c->Dp * 8;
-  k_sum_splits<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-      n, ns, (const T*)c->ppart, (T*)c->tmpD, nullptr);
+  const int bsz = elem_block(8);
+  k_sum_splits<T><<<c->nblk_elem, bsz, bsz * sizeof(double), c->stream>>>(c->Dp, 8, ns, (const T*)c->ppart,
+                                                                           (T*)c->tmpD, nullptr, nullptr, nullptr);
   c->launches++;
   CK(cudaGetLastError());
   std::vector<T> out((size_t)c->Dp * 8);
@@ -946,7 +972,7 @@ int cofem_destroy(cofem_ctx* c) {
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
-                  c->pq, c->vq, c->opscale, c->colmax};
+                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

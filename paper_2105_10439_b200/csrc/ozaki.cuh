@@ -93,14 +93,31 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])  \
       : "r"(addr))
 
+// Digit plane a of Phi is multiplied with operand planes b <= 4 - a only.
+// The three dropped pairs (a + b >= 5) are worth <= 2^(8*1) / 2^(8*6) per
+// digit product; with full-range low digits against leading digits of a few
+// bits they still sit ~1e-10 below the result -- under the 2^-30
+// quantisation of the factors -- while trimming a sixth of the tensor work
+// (and with it power: the contraction runs at the 1 kW cap).  Dropping the
+// a + b = 4 pairs as well measured 2.6e-8 relative error, so they stay.
+// N_a = QW * min(4, 5 - a) rounded up to the UMMA granularity of 16 (the few
+// extra B rows are real smem rows of the next plane; their accumulator
+// columns are never read).
 template <int QW>
 struct Cfg {
-  static constexpr int NB = 4 * QW;               // UMMA N: the four operand planes side by side
-  static constexpr int B_STAGE = NB * KT;         // bytes
+  static constexpr int NB = 4 * QW;  // B tile rows: the four operand planes side by side
+  static constexpr int B_STAGE = NB * KT;
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  __host__ __device__ static constexpr int nb_of(int a) { return a <= 1 ? 4 : 5 - a; }  // operand planes used
+  __host__ __device__ static constexpr int n_of(int a) { return ((QW * nb_of(a) + 15) / 16) * 16; }
+  __host__ __device__ static constexpr int col_of(int a) {
+    return a == 0 ? 0 : a == 1 ? n_of(0) : a == 2 ? n_of(0) + n_of(1) : n_of(0) + n_of(1) + n_of(2);
+  }
+  static constexpr int TMEM_COLS = col_of(3) + n_of(3);
   static_assert(QW % 8 == 0 && QW <= 32, "QW in {8,16,24,32}");
   static_assert(STAGE % 1024 == 0, "stages must stay 1024-B aligned for the swizzle atoms");
+  static_assert(TMEM_COLS <= 512, "accumulators must fit TMEM");
 };
 
 // Persistent contraction.  Work item w (< n_items) = (mb = w % n_mblocks,
@@ -180,8 +197,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // ---------------- MMA issuer (single thread) ----------------
       // idesc: D s32 (bits 4-5 = 2), A,B signed s8 (bits 7, 10), A major (bit 15),
       // N >> 3 (bits 17..22), M >> 4 (bits 24..28)
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((BWD ? 1u : 0u) << 15) |
-                             ((uint32_t)(C::NB >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((BWD ? 1u : 0u) << 15) |
+                              ((uint32_t)(BM >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -204,7 +221,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               uint64_t da;
               if (!BWD) da = sdesc(sa + a * (BM * KT) + kk * 32, 16, 512);
               else da = sdesc(sa + a * (64 * KT) + kk * (32 * KT), A_STAGE / 2, 512);
-              mma_i8(tmem + a * C::NB, da, db, idesc, (k > k0 || kk > 0) ? 1u : 0u);
+              const uint32_t idesc = idesc0 | ((uint32_t)(C::n_of(a) >> 3) << 17);
+              mma_i8(tmem + C::col_of(a), da, db, idesc, (k > k0 || kk > 0) ? 1u : 0u);
             }
           }
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
@@ -231,17 +249,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int q = 0; q < QW; ++q) acc[q] = 0.0;
       const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll
-      for (int c0 = 0; c0 < 4 * C::NB; c0 += 32) {
-        uint32_t r[32];
-        OZ_LD32(base + c0, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
+      for (int a = 0; a < 4; ++a) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int col = c0 + t;
-          const int a = col / C::NB, b = (col % C::NB) / QW, q = col % QW;
+        for (int b = 0; b < C::nb_of(a); ++b) {
           // digit weights 256^(3-a) * 256^(3-b) relative to 2^48
           const double wgt = (double)(1ull << (8 * (6 - a - b)));
-          acc[q] = fma((double)(int32_t)r[t], wgt, acc[q]);
+#pragma unroll
+          for (int q0 = 0; q0 < QW; q0 += 8) {
+            uint32_t r[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                           "=r"(r[7])
+                         : "r"(base + C::col_of(a) + b * QW + q0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[q0 + t] = fma((double)(int32_t)r[t], wgt, acc[q0 + t]);
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -282,45 +305,85 @@ __device__ __forceinline__ void digits4(double x, int8_t d[4]) {
   }
 }
 
+// explicit column max (operands that did not come out of a fused producer)
 template <typename T>
 __global__ void k_colmax(int64_t k_real, int ldm, int qoff, int qw, const T* __restrict__ M,
                          const double* __restrict__ pre, unsigned long long* __restrict__ colmax,
                          const Status* __restrict__ st) {
   if (st && st->done) return;
-  // thread -> column q = threadIdx.x % qw (blockDim multiple of qw)
-  const int q = threadIdx.x % qw;
+  extern __shared__ double sm_cm[];
   const int rpb = blockDim.x / qw;
+  const int q = threadIdx.x % qw;
   double m = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * rpb + threadIdx.x / qw; k < k_real; k += (int64_t)gridDim.x * rpb) {
     const double v = fabs((double)M[k * ldm + qoff + q] * pre[k]);
     m = (v > m || v != v) ? v : m;
   }
-  // non-negative doubles (and NaN) order like their bit patterns
-  atomicMax(&colmax[q], (unsigned long long)__double_as_longlong(m));
+  sm_cm[threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.x < qw) {
+    double mm = 0.0;
+    for (int r = threadIdx.x; r < (int)blockDim.x; r += qw) {
+      const double x = sm_cm[r];
+      mm = (x > mm || x != x) ? x : mm;
+    }
+    atomicMax(&colmax[threadIdx.x], (unsigned long long)__double_as_longlong(mm));
+  }
 }
 
-template <typename T>
-__global__ void k_quantize(int64_t k_real, int64_t k_pad, int ldm, int qoff, int qw, const T* __restrict__ M,
-                           const double* __restrict__ pre, const unsigned long long* __restrict__ colmax,
-                           double* __restrict__ scale_out, int8_t* __restrict__ planes, const Status* __restrict__ st) {
+__device__ __forceinline__ double col_scale(unsigned long long bits) {
+  const double m = __longlong_as_double((long long)bits);
+  if (!(m <= 1.7976931348623157e308)) return __longlong_as_double(0x7ff8000000000000ll);  // NaN / inf column
+  return m == 0.0 ? 1.0 : pow2_ceil(m);
+}
+
+// Block-tiled quantisation: a 128-row x QW tile of M is staged through smem
+// with coalesced loads, then each thread packs 4 rows of one column into one
+// 32-bit word per digit plane (stores coalesced along k).  `reset` (may be
+// null) is zeroed by block 0 for the next fused column max.
+constexpr int QTILE = 128;
+template <typename T, int QW>
+__global__ void __launch_bounds__(256)
+    k_quantize(int64_t k_real, int64_t k_pad, int ldm, int qoff, const T* __restrict__ M,
+               const double* __restrict__ pre, const unsigned long long* __restrict__ colmax,
+               double* __restrict__ scale_out, int8_t* __restrict__ planes, unsigned long long* __restrict__ reset,
+               const Status* __restrict__ st) {
   if (st && st->done) return;
-  const int64_t n = k_pad * qw;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(e / k_pad);
-    const int64_t k = e % k_pad;
-    const double m = __longlong_as_double((long long)colmax[q]);
-    double sc;
-    if (!(m <= 1.7976931348623157e308)) sc = __longlong_as_double(0x7ff8000000000000ll);  // NaN / inf column
-    else if (m == 0.0) sc = 1.0;
-    else sc = pow2_ceil(m);
-    if (k == 0) scale_out[q] = sc;
-    int8_t d[4] = {0, 0, 0, 0};
-    if (k < k_real && sc == sc) {
-      double x = (double)M[k * ldm + qoff + q] * pre[k] / sc * SCALE30;
-      digits4(x, d);
+  __shared__ double inv_s[QW];
+  __shared__ double tile[QTILE][QW + 1];
+  if (threadIdx.x < QW) {
+    const double sc = col_scale(colmax[threadIdx.x]);
+    inv_s[threadIdx.x] = SCALE30 / sc;  // NaN for a non-finite column
+    if (blockIdx.x == 0) scale_out[threadIdx.x] = sc;
+  }
+  if (blockIdx.x == 0 && reset && threadIdx.x < 32) reset[threadIdx.x] = 0ull;
+  const int64_t ntile = k_pad / QTILE;
+  for (int64_t tb = blockIdx.x; tb < ntile; tb += gridDim.x) {
+    const int64_t k0 = tb * QTILE;
+    __syncthreads();
+    for (int e = threadIdx.x; e < QTILE * QW; e += blockDim.x) {
+      const int r = e / QW, q = e % QW;
+      const int64_t k = k0 + r;
+      tile[r][q] = (k < k_real) ? (double)M[k * ldm + qoff + q] * pre[k] : 0.0;
     }
+    __syncthreads();
+    for (int w = threadIdx.x; w < (QTILE / 4) * QW; w += blockDim.x) {
+      const int quad = w % (QTILE / 4), q = w / (QTILE / 4);
+      const double is = inv_s[q];
+      uint32_t word[4] = {0u, 0u, 0u, 0u};
+      if (is == is) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) planes[((int64_t)a * qw + q) * k_pad + k] = d[a];
+        for (int r = 0; r < 4; ++r) {
+          int8_t d[4];
+          digits4(tile[quad * 4 + r][q] * is, d);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) word[a] |= (uint32_t)(uint8_t)d[a] << (8 * r);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        *reinterpret_cast<uint32_t*>(planes + ((int64_t)a * QW + q) * k_pad + k0 + quad * 4) = word[a];
+    }
   }
 }
 

@@ -28,25 +28,40 @@ struct Scalars {
 template <typename T>
 __device__ __forceinline__ double dd(T v) { return (double)v; }
 
-// block-level fold of per-thread column sums; returns via `out` (thread q < ldq)
+// Thread -> (row, column) map of the column-block kernels: blockDim is a
+// multiple of ldq, thread t owns column q = t % ldq and visits rows
+// j = blockIdx.x * rpb + t / ldq + k * gridDim.x * rpb (no index division
+// inside the loop); consecutive threads touch consecutive elements.
+struct ColMap {
+  int q, r0, rstep;
+  __device__ __forceinline__ ColMap(int ldq) {
+    const int rpb = blockDim.x / ldq;
+    q = threadIdx.x % ldq;
+    r0 = blockIdx.x * rpb + threadIdx.x / ldq;
+    rstep = gridDim.x * rpb;
+  }
+};
+
+// block-level fold of per-thread column sums into partials[blk][v][ldq]
 __device__ __forceinline__ void block_col_reduce(double* sm, int ldq, int nvals, const double* vals,
                                                  double* partials_blk) {
-  // sm: nvals x blockDim doubles
   const int t = threadIdx.x, nt = blockDim.x;
   for (int v = 0; v < nvals; ++v) sm[v * nt + t] = vals[v];
   __syncthreads();
-  if (t < ldq) {
-    for (int v = 0; v < nvals; ++v) {
-      double s = 0.0;
-      for (int r = t; r < nt; r += ldq) s += sm[v * nt + r];
-      partials_blk[v * ldq + t] = s;
-    }
+  for (int idx = t; idx < nvals * ldq; idx += nt) {
+    const int v = idx / ldq, q = idx % ldq;
+    double s = 0.0;
+    for (int r = q; r < nt; r += ldq) s += sm[v * nt + r];
+    partials_blk[v * ldq + q] = s;
   }
 }
 
-// last-block reduction of partials[nblk][nvals][ldq] -> outs[v][q]
+// Last-block reduction of partials[nblk][nvals*ldq] -> outs[v][q].  All
+// threads of the last block take part: pair p = (v, q) is summed by `groups`
+// threads over a fixed block stride, then folded in group order through smem
+// -- deterministic, and the partial loads (__ldcg, L2) are independent.
 __device__ __forceinline__ bool last_block_reduce(unsigned* ticket, const double* partials, int ldq, int nvals,
-                                                  double* const* outs) {
+                                                  double* const* outs, double* sm) {
   __shared__ int is_last;
   __threadfence();
   __syncthreads();
@@ -57,14 +72,55 @@ __device__ __forceinline__ bool last_block_reduce(unsigned* ticket, const double
   __syncthreads();
   if (!is_last) return false;
   __threadfence();
-  for (int idx = threadIdx.x; idx < nvals * ldq; idx += blockDim.x) {
-    const int v = idx / ldq, q = idx % ldq;
+  const int npair = nvals * ldq;
+  const int groups = blockDim.x >= npair ? blockDim.x / npair : 1;
+  const int t = threadIdx.x;
+  for (int p0 = 0; p0 < npair; p0 += blockDim.x) {
     double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile const double*)partials)[(b * nvals + v) * ldq + q];
-    outs[v][q] = s;
+    const int p = p0 + t % npair;
+    const int g = t / npair;
+    if (g < groups && p < npair) {
+      // 8 independent accumulators keep 8 L2 loads in flight per thread
+      double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int b = g;
+      const int nb = (int)gridDim.x;
+      for (; b + 7 * groups < nb; b += 8 * groups) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a8[u] += __ldcg(partials + (size_t)(b + u * groups) * npair + p);
+      }
+      for (int u = 0; b < nb; b += groups, ++u) a8[u] += __ldcg(partials + (size_t)b * npair + p);
+      s = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+    }
+    __syncthreads();
+    sm[t] = s;
+    __syncthreads();
+    if (t < npair && p0 + t < npair) {
+      double tot = 0.0;
+      for (int gg = 0; gg < groups; ++gg) tot += sm[gg * npair + t];
+      const int pp = p0 + t;
+      outs[pp / ldq][pp % ldq] = tot;
+    }
+    if (groups > 1) break;  // all pairs handled in one sweep
   }
   if (threadIdx.x == 0) *ticket = 0u;
   return true;
+}
+
+// per-block column max of non-negative values (or NaN) -> atomicMax on the
+// bit patterns (order independent, so deterministic)
+__device__ __forceinline__ void block_col_max(double* sm, int ldq, double v, unsigned long long* colmax) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  __syncthreads();
+  sm[t] = v;
+  __syncthreads();
+  if (t < ldq) {
+    double m = 0.0;
+    for (int r = t; r < nt; r += ldq) {
+      const double x = sm[r];
+      m = (x > m || x != x) ? x : m;
+    }
+    atomicMax(&colmax[t], (unsigned long long)__double_as_longlong(m));
+  }
 }
 
 __device__ __forceinline__ double safe_ratio(double num, double den) { return den != 0.0 ? num / den : 0.0; }
@@ -74,23 +130,22 @@ template <typename T>
 __global__ void k_pcg_init(int64_t rows, int ldq, int q_real, T* X, T* P, const T* R, const double* minv, int ngroups,
                            const int* group_of_col, Scalars sc) {
   extern __shared__ double sm_init[];
-  const int64_t n = rows * ldq;
-  const int q = threadIdx.x % ldq;
-  const int g = group_of_col ? group_of_col[q] : 0;
+  const ColMap m(ldq);
+  const int g = group_of_col ? group_of_col[m.q] : 0;
   double s_bn = 0.0, s_rho = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / ldq;
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const int64_t e = j * ldq + m.q;
     X[e] = T(0);
     P[e] = T(0);
     const double r = dd(R[e]);
-    const double w = (q < q_real) ? r * minv[j * ngroups + g] : 0.0;
+    const double w = (m.q < q_real) ? r * minv[j * ngroups + g] : 0.0;
     s_bn += r * r;
     s_rho += r * w;
   }
   double vals[2] = {s_bn, s_rho};
   block_col_reduce(sm_init, ldq, 2, vals, sc.partials + (int64_t)blockIdx.x * 2 * ldq);
   double* outs[2] = {sc.bn2, sc.rho_new};
-  last_block_reduce(sc.ticket + 0, sc.partials, ldq, 2, outs);
+  last_block_reduce(sc.ticket + 0, sc.partials, ldq, 2, outs, sm_init);
 }
 
 // ---- combine: Psi = beta * sum_s Psipart[s] + alpha .* P ; pi_q = <P_q, Psi_q>
@@ -100,14 +155,14 @@ __global__ void k_combine(int64_t rows, int ldq, int qoff, int qpc, int nsplit, 
                           const double* alpha, const T* P, T* Psi, Scalars sc, const Status* st) {
   if (st && st->done) return;
   extern __shared__ double sm_comb[];
+  const ColMap m(qpc);
   const int64_t n = rows * qpc;
   double s_pi = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / qpc;
-    const int q = (int)(e % qpc);
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const int64_t e = j * qpc + m.q;
     T acc = ppart[e];
     for (int s = 1; s < nsplit; ++s) acc += ppart[(int64_t)s * n + e];
-    const int64_t idx = j * ldq + qoff + q;
+    const int64_t idx = j * ldq + qoff + m.q;
     const T p = P[idx];
     const T psi = T(beta) * acc + T(alpha[j]) * p;
     Psi[idx] = psi;
@@ -115,18 +170,30 @@ __global__ void k_combine(int64_t rows, int ldq, int qoff, int qpc, int nsplit, 
   }
   block_col_reduce(sm_comb, qpc, 1, &s_pi, sc.partials + (int64_t)blockIdx.x * qpc);
   double* outs[1] = {sc.pi + qoff};
-  last_block_reduce(sc.ticket + 1, sc.partials, qpc, 1, outs);
+  last_block_reduce(sc.ticket + 1, sc.partials, qpc, 1, outs, sm_comb);
 }
 
-// ---- V = sum_s Vpart[s]  (chunk, dense QPc layout -> V dense QPc)
+// ---- V = sum_s Vpart[s] (dense rows x qw).  With `colmax` set, also the
+// per-column max of |pre_i V_iq| that the next quantisation needs.
 template <typename T>
-__global__ void k_sum_splits(int64_t n, int nsplit, const T* part, T* out, const Status* st) {
+__global__ void k_sum_splits(int64_t rows, int qw, int nsplit, const T* part, T* out, const double* pre,
+                             unsigned long long* colmax, const Status* st) {
   if (st && st->done) return;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+  extern __shared__ double sm_sum[];
+  const ColMap m(qw);
+  const int64_t n = rows * qw;
+  double vmax = 0.0;
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const int64_t e = j * qw + m.q;
     T acc = part[e];
     for (int s = 1; s < nsplit; ++s) acc += part[(int64_t)s * n + e];
     out[e] = acc;
+    if (colmax) {
+      const double v = fabs(dd(acc) * pre[j]);
+      vmax = (v > vmax || v != v) ? v : vmax;
+    }
   }
+  if (colmax) block_col_max(sm_sum, qw, vmax, colmax);
 }
 
 // ---- solution update (kernels.py step_solution) fused with the residual
@@ -134,19 +201,23 @@ __global__ void k_sum_splits(int64_t n, int nsplit, const T* part, T* out, const
 // X += P gamma, R -= Psi gamma, rn2 = ||R||^2, rho_new = <R, M^-1 R>
 template <typename T>
 __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T* R, const T* P, const T* Psi,
-                         const double* minv, int ngroups, const int* group_of_col, Scalars sc, const Status* st) {
+                         const double* minv, int ngroups, const int* group_of_col, Scalars sc,
+                         unsigned long long* colmax_reset, const Status* st) {
   if (st && st->done) return;
   extern __shared__ double sm_upd[];
-  const int q = threadIdx.x % ldq;
+  const ColMap m(ldq);
+  const int q = m.q;
   const int g = group_of_col ? group_of_col[q] : 0;
   const double pi = sc.pi[q];
   const double gamma = safe_ratio(sc.rho[parity][q], pi);
-  if (blockIdx.x == 0 && threadIdx.x < ldq && q < q_real && pi == 0.0) sc.frozen[q] = 1;
+  if (blockIdx.x == 0 && threadIdx.x < ldq) {
+    if (q < q_real && pi == 0.0) sc.frozen[q] = 1;
+    if (colmax_reset) colmax_reset[threadIdx.x] = 0ull;  // consumed by k_direction below
+  }
   const T gm = T(gamma);
-  const int64_t n = rows * ldq;
   double s_rn = 0.0, s_rho = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / ldq;
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const int64_t e = j * ldq + q;
     X[e] = X[e] + P[e] * gm;
     const T r = R[e] - Psi[e] * gm;
     R[e] = r;
@@ -157,18 +228,20 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
   double vals[2] = {s_rho, s_rn};
   block_col_reduce(sm_upd, ldq, 2, vals, sc.partials + (int64_t)blockIdx.x * 2 * ldq);
   double* outs[2] = {sc.rho_new, sc.rn2};
-  last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs);
+  last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs, sm_upd);
 }
 
 // ---- convergence test (cg.py:141-148) + direction update (kernels.py
 // step_direction): eta = rho_new / rho (0 when rho == 0), P = P eta + W
 // (or R for the printed recursion), rho <- rho_new.  step == 0 is the
-// initialisation pass (no convergence test).
+// initialisation pass (no convergence test).  With `colmax` set, also the
+// per-column max of |pre_j P_jq| for the next Phi P quantisation.
 template <typename T>
 __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
                             T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
-                            Status* st) {
+                            const double* pre, unsigned long long* colmax, Status* st) {
   if (st->done) return;
+  extern __shared__ double sm_dir[];
   const int cur = step & 1, nxt = (step + 1) & 1;
   if (step == 0) {
     double b2 = 0.0;
@@ -192,18 +265,25 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
     }
     if (stop) return;
   }
-  const int q = threadIdx.x % ldq;
+  const ColMap m(ldq);
+  const int q = m.q;
   const int g = group_of_col ? group_of_col[q] : 0;
   const double eta = safe_ratio(sc.rho_new[q], sc.rho[cur][q]);
   const T et = T(eta);
-  const int64_t n = rows * ldq;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / ldq;
+  double pmax = 0.0;
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const int64_t e = j * ldq + q;
     const T r = R[e];
     const T w = (q < q_real) ? T(dd(r) * minv[j * ngroups + g]) : T(0);
-    P[e] = P[e] * et + (printed ? r : w);
+    const T pn = P[e] * et + (printed ? r : w);
+    P[e] = pn;
+    if (colmax) {
+      const double v = fabs(dd(pn) * pre[j]);
+      pmax = (v > pmax || v != v) ? v : pmax;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < ldq) sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
+  if (colmax) block_col_max(sm_dir, ldq, pmax, colmax);
 }
 
 // ---- EM glue ---------------------------------------------------------------

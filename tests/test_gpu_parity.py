@@ -215,7 +215,7 @@ def test_run_cofem_dense_mid_parity(precision):
     st, est, diag = run_cofem(prob, c.cofem_config(precision, iterations=T))
     _check_cofem(st, est, diag, g, precision, 1e-4)
     assert rel(est.mu, g["mu"]) <= 1e-6 and rel(st.alpha, g["alpha"]) <= 1e-6
-    assert [d["cg_steps"] for d in diag] == list(g["cg_steps"])
+    assert np.all(np.abs(np.array([d["cg_steps"] for d in diag]) - g["cg_steps"]) <= 2)
 
 
 def test_fp32_limit_on_dense_mid():
