@@ -236,7 +236,9 @@ void free_ws(cofem_ctx* c) {
   c->ldq = 0;
 }
 
-int elem_block(int ldq) { return ldq >= 256 ? ldq : ldq * (256 / ldq); }
+// column-block kernels: blockDim a multiple of ldq near 512 (few blocks -> a
+// short deterministic final reduction; 4 rows per thread trip for MLP)
+int elem_block(int ldq) { return ldq >= 512 ? ldq : ldq * (512 / ldq); }
 
 // choose split count for a contraction: minimise wave quantisation plus the
 // extra traffic of the split partials relative to the Phi stream
@@ -307,7 +309,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->ppart, c->ppart_cap));
   CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
-  c->nblk_elem = 4 * c->sm_count;
+  c->nblk_elem = 2 * c->sm_count;
   CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
   CK(cudaMemset(c->X, 0, dbytes));
   CK(cudaMemset(c->R, 0, dbytes));

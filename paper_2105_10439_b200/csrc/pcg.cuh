@@ -32,6 +32,8 @@ __device__ __forceinline__ double dd(T v) { return (double)v; }
 // multiple of ldq, thread t owns column q = t % ldq and visits rows
 // j = blockIdx.x * rpb + t / ldq + k * gridDim.x * rpb (no index division
 // inside the loop); consecutive threads touch consecutive elements.
+constexpr int UNR = 4;  // rows per thread per loop trip: independent loads in flight
+
 struct ColMap {
   int q, r0, rstep;
   __device__ __forceinline__ ColMap(int ldq) {
@@ -158,15 +160,29 @@ __global__ void k_combine(int64_t rows, int ldq, int qoff, int qpc, int nsplit, 
   const ColMap m(qpc);
   const int64_t n = rows * qpc;
   double s_pi = 0.0;
-  for (int64_t j = m.r0; j < rows; j += m.rstep) {
-    const int64_t e = j * qpc + m.q;
-    T acc = ppart[e];
-    for (int s = 1; s < nsplit; ++s) acc += ppart[(int64_t)s * n + e];
-    const int64_t idx = j * ldq + qoff + m.q;
-    const T p = P[idx];
-    const T psi = T(beta) * acc + T(alpha[j]) * p;
-    Psi[idx] = psi;
-    s_pi += dd(p) * dd(psi);
+  for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
+    T acc[UNR], p[UNR];
+    double al[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {  // issue every load of UNR rows first
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const int64_t e = j * qpc + m.q;
+        acc[u] = ppart[e];
+        for (int s = 1; s < nsplit; ++s) acc[u] += ppart[(int64_t)s * n + e];
+        p[u] = P[j * ldq + qoff + m.q];
+        al[u] = alpha[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const T psi = T(beta) * acc[u] + T(al[u]) * p[u];
+        Psi[j * ldq + qoff + m.q] = psi;
+        s_pi += dd(p[u]) * dd(psi);
+      }
+    }
   }
   block_col_reduce(sm_comb, qpc, 1, &s_pi, sc.partials + (int64_t)blockIdx.x * qpc);
   double* outs[1] = {sc.pi + qoff};
@@ -216,14 +232,34 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
   }
   const T gm = T(gamma);
   double s_rn = 0.0, s_rho = 0.0;
-  for (int64_t j = m.r0; j < rows; j += m.rstep) {
-    const int64_t e = j * ldq + q;
-    X[e] = X[e] + P[e] * gm;
-    const T r = R[e] - Psi[e] * gm;
-    R[e] = r;
-    const double rd = dd(r);
-    s_rn += rd * rd;
-    if (q < q_real) s_rho += rd * (rd * minv[j * ngroups + g]);
+  for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
+    T x[UNR], p[UNR], r[UNR], ps[UNR];
+    double mv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const int64_t e = j * ldq + q;
+        x[u] = X[e];
+        p[u] = P[e];
+        r[u] = R[e];
+        ps[u] = Psi[e];
+        mv[u] = minv[j * ngroups + g];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const int64_t e = j * ldq + q;
+        X[e] = x[u] + p[u] * gm;
+        const T rn = r[u] - ps[u] * gm;
+        R[e] = rn;
+        const double rd = dd(rn);
+        s_rn += rd * rd;
+        if (q < q_real) s_rho += rd * (rd * mv[u]);
+      }
+    }
   }
   double vals[2] = {s_rho, s_rn};
   block_col_reduce(sm_upd, ldq, 2, vals, sc.partials + (int64_t)blockIdx.x * 2 * ldq);
@@ -271,15 +307,32 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
   const double eta = safe_ratio(sc.rho_new[q], sc.rho[cur][q]);
   const T et = T(eta);
   double pmax = 0.0;
-  for (int64_t j = m.r0; j < rows; j += m.rstep) {
-    const int64_t e = j * ldq + q;
-    const T r = R[e];
-    const T w = (q < q_real) ? T(dd(r) * minv[j * ngroups + g]) : T(0);
-    const T pn = P[e] * et + (printed ? r : w);
-    P[e] = pn;
-    if (colmax) {
-      const double v = fabs(dd(pn) * pre[j]);
-      pmax = (v > pmax || v != v) ? v : pmax;
+  for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
+    T r[UNR], p[UNR];
+    double mv[UNR], pr[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const int64_t e = j * ldq + q;
+        r[u] = R[e];
+        p[u] = P[e];
+        mv[u] = minv[j * ngroups + g];
+        pr[u] = colmax ? pre[j] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t j = j0 + (int64_t)u * m.rstep;
+      if (j < rows) {
+        const T w = (q < q_real) ? T(dd(r[u]) * mv[u]) : T(0);
+        const T pn = p[u] * et + (printed ? r[u] : w);
+        P[j * ldq + q] = pn;
+        if (colmax) {
+          const double v = fabs(dd(pn) * pr[u]);
+          pmax = (v > pmax || v != v) ? v : pmax;
+        }
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < ldq) sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
