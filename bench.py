@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "CoFEM EM iters/sec at D=65536,N=16384,K=20 (fp32)"
+METRICS = {"conv-large": "CoFEM EM iters/sec, convolution dictionary N=D=2^22, 256 taps, K=30"}
 UNIT = "EM iter/s"
 
 
@@ -191,6 +192,8 @@ def run_ours(args):
     from paper_2105_10439_b200 import simulate as S
 
     world, rank, local = dist_env()
+    if args.config in S.CONV_CONFIGS:
+        return run_ours_conv(args)
     c = S.CONFIGS[args.config]
     dist = None
     if world > 1:
@@ -325,6 +328,89 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_ours_conv(args):
+    """BASELINE config 3: banded int8 tensor-core convolution, single GPU."""
+    import torch
+
+    from paper_2105_10439_b200 import _lib, run_cofem
+    from paper_2105_10439_b200 import simulate as S
+
+    world, rank, local = dist_env()
+    if world > 1:
+        raise SystemExit("conv configs run on one GPU this round (time-sharded halo exchange not built)")
+    c = S.CONV_CONFIGS[args.config]
+    prob, z = S.conv_problem(c)
+    h = prob.op.gpu_taps()
+    ctx = _lib.Context.convolution(c.D, h, _lib.OZAKI, 0)
+    dseed = 0xC0FE
+    ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
+    if args.warmup:
+        ctx.bench_iterations(args.warmup)
+    ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
+    torch.cuda.synchronize(0)
+    with ClockSampler(0) as clk:
+        tim = ctx.bench_iterations(args.steps, time_kernels=True)
+    total_ms = tim["total_ms"]
+    value = args.steps / (total_ms / 1e3)
+    pcg_steps = tim["pcg_steps"]
+    qw = 32 if c.K + 1 > 24 else 24
+    alg_bytes = 4.0 * qw * c.D + 8.0 * qw * c.D  # operand digit planes in, fp64 result out
+    fwd_avg = tim["fwd_ms"] / max(tim["fwd_launches"], 1)
+    bwd_avg = tim["bwd_ms"] / max(tim["bwd_launches"], 1)
+    dom, avg_ms = ("bwd (Phi^T U band)", bwd_avg) if tim["bwd_ms"] >= tim["fwd_ms"] else ("fwd (Phi P band)", fwd_avg)
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    line = {
+        "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "i8 x i8 -> exact i32 (ozaki) / f64",
+        "data": "synthetic (Bernoulli(0.01) x Exp(1) spikes, exp(-t/20) filter, sigma=0.05)",
+        "config": {"workload": f"{args.config}: causal convolution N=D={c.D}, {c.ntaps} taps, K={c.K}, "
+                               f"PCG cap {c.U} tol {c.tol}", "D": c.D, "K": c.K, "taps": c.ntaps},
+        "pcg_steps_per_sec": pcg_steps / (total_ms / 1e3), "pcg_steps_per_em_iteration": pcg_steps / args.steps,
+        "gpu_launches": int(tim["kernel_launches"]), "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": profiled_traffic(args.config, args.precision),
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
+                     "contraction_share_of_step": (tim["fwd_ms"] + tim["bwd_ms"]) / tim["total_ms"]},
+    }
+    ctx.close()
+    if not args.no_e2e:
+        cfg = c.cofem_config("ozaki", iterations=args.steps)
+        t0 = time.perf_counter()
+        st, est, diag = run_cofem(prob, cfg)
+        el = time.perf_counter() - t0
+        prob.op.release()
+        line["e2e"] = {"value": args.steps / el, "unit": UNIT, "h2d_bytes_per_step": 8.0 * c.D / args.steps + c.D * c.K,
+                       "d2h_bytes_per_step": 24.0 * c.D / args.steps, "seconds": el,
+                       "pcg_steps": int(sum(d["cg_steps"] for d in diag))}
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_sample_conv(c, prob, args.cpu_seconds, pcg_steps / args.steps)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_sample_conv(c, prob, seconds, steps_per_em):
+    """The reference algorithm (oracle: FFT convolution like operators.py:209-219,
+    float64, numpy/scipy threads) on the full-size convolution system."""
+    from oracle import cofem_oracle as O
+
+    op = O.conv_op(c.D, c.taps())
+    probes = O.draw_rademacher(c.D, c.K, O.substream(c.seed, 3))
+    rhs = np.concatenate([probes, op.adjoint(np.asarray(prob.y)[:, None])], axis=1)
+    alpha = np.ones(c.D)
+    minv = 1.0 / (c.beta + alpha)
+    fn = lambda V: O.system_apply(op, c.beta, alpha, V)  # noqa: E731
+    steps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        O.pcg_solve(fn, rhs, minv, O.CgConfig(max_steps=1, tolerance=1e-300))
+        steps += 1
+    per = (time.perf_counter() - t0) / steps
+    return {"value": 1.0 / (per * steps_per_em), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{steps} PCG steps of the full D={c.D}, Q={c.K + 1} convolution system with the bit-exact "
+                      f"numpy oracle (scipy.fft rfft/irfft like the reference); {per * 1e3:.0f} ms/PCG step x "
+                      f"{steps_per_em:.1f} PCG steps per EM iteration"}
 
 
 def run_reference(args):

@@ -97,6 +97,15 @@ int cofem_device_count(int* out);
 int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, int precision);
 int cofem_destroy(cofem_ctx* ctx);
 
+/* Causal convolution dictionary (operators.ConvolutionOperator,
+ * operators.py:182-225; BASELINE config 3): the D x D lower-triangular
+ * Toeplitz matrix Phi_ij = taps[i - j] for 0 <= i - j < ntaps.  Applied as
+ * banded int8 tensor-core contractions (Phi and Phi^T), so it requires
+ * precision COFEM_OZAKI.  The reference's filter (1 - rho)^m is passed
+ * truncated where it falls below the fixed-point resolution. */
+int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const double* taps, int64_t ntaps,
+                             int precision);
+
 /* Upload Phi (N x D_local float32, row stride `ld` elements) from host
  * memory (or adopt a device pointer when `on_device` != 0; the caller keeps
  * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */

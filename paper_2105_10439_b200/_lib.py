@@ -36,6 +36,7 @@ EXPORTED = (
     "cofem_device_count",
     "cofem_create",
     "cofem_destroy",
+    "cofem_create_convolution",
     "cofem_set_dictionary",
     "cofem_set_shard",
     "cofem_generate_gaussian_dictionary",
@@ -123,6 +124,7 @@ def load():
         "cofem_device_count": (c_int, [POINTER(c_int)]),
         "cofem_create": (c_int, [POINTER(vp), c_int, c_int64, c_int64, c_int]),
         "cofem_destroy": (c_int, [vp]),
+        "cofem_create_convolution": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_double), c_int64, c_int]),
         "cofem_set_dictionary": (c_int, [vp, vp, c_int64, c_int]),
         "cofem_set_shard": (c_int, [vp, c_int64, c_int64]),
         "cofem_generate_gaussian_dictionary": (c_int, [vp, c_uint64, c_double]),
@@ -174,14 +176,25 @@ def device_count():
 class Context:
     """Owns one native cofem_ctx: a dense float32 dictionary shard on one GPU."""
 
-    def __init__(self, n_rows, n_cols, precision=FP32, device=0):
+    def __init__(self, n_rows, n_cols, precision=FP32, device=0, _handle=None):
         lib = load()
-        handle = c_void_p()
-        check(lib.cofem_create(ctypes.byref(handle), int(device), int(n_rows), int(n_cols), int(precision)))
+        handle = _handle
+        if handle is None:
+            handle = c_void_p()
+            check(lib.cofem_create(ctypes.byref(handle), int(device), int(n_rows), int(n_cols), int(precision)))
         self._h = handle
         self.n_rows = int(n_rows)
         self.n_cols = int(n_cols)
         self.precision = precision
+
+    @classmethod
+    def convolution(cls, dim, taps, precision=OZAKI, device=0):
+        """Causal Toeplitz dictionary with the given filter taps (banded int8 path)."""
+        taps = np.ascontiguousarray(taps, dtype=np.float64)
+        handle = c_void_p()
+        check(load().cofem_create_convolution(ctypes.byref(handle), int(device), int(dim), _dp(taps), taps.size,
+                                              int(precision)))
+        return cls(dim, dim, precision, device, _handle=handle)
 
     @property
     def handle(self):

@@ -174,6 +174,13 @@ struct cofem_ctx {
   CUtensorMap map_p[5]{}, map_v[5]{};               // by QW / 8
   bool map_p_ok[5] = {}, map_v_ok[5] = {};
 
+  // operator kind: dense dictionary or banded Toeplitz convolution
+  int kind = 0;                                      // 0 dense, 1 convolution
+  int conv_L = 0, conv_lpad = 0;                     // taps, taps-1 rounded up to 64
+  int8_t *band_fwd = nullptr, *band_adj = nullptr;   // [4][128][128 + lpad] digit planes
+  double* hrows = nullptr;                           // Dp copies of the band's power-of-two scale
+  CUtensorMap map_band_fwd{}, map_band_adj{};
+
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -302,10 +309,12 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->Psi, dbytes));
   CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * QCHUNK * ts));
   CK(cudaMalloc(&c->V, (size_t)c->Np * QCHUNK * ts));
-  // split partial capacity: up to MAX_SPLITS partial blocks of a 32-column chunk
-  c->vpart_cap = (size_t)MAX_SPLITS * c->Np * QCHUNK * ts;
-  c->ppart_cap = (size_t)MAX_SPLITS * c->Dp * QCHUNK * ts;
-  CK(cudaMalloc(&c->vpart, c->vpart_cap));
+  // split partial capacity: up to MAX_SPLITS partial blocks of a 32-column
+  // chunk for dense dictionaries; the banded operator writes one partial
+  const int max_splits = c->kind == 1 ? 1 : MAX_SPLITS;
+  c->vpart_cap = c->kind == 1 ? 0 : (size_t)max_splits * c->Np * QCHUNK * ts;
+  c->ppart_cap = (size_t)max_splits * c->Dp * QCHUNK * ts;
+  if (c->vpart_cap) CK(cudaMalloc(&c->vpart, c->vpart_cap));
   CK(cudaMalloc(&c->ppart, c->ppart_cap));
   CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
@@ -370,9 +379,11 @@ template <int QW>
 int oz_init_kernels() {
   static bool done = false;
   if (done) return 0;
-  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)oz::Cfg<QW>::SMEM));
-  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)oz::Cfg<QW>::SMEM));
+  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_BAND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)oz::Cfg<QW>::SMEM));
   done = true;
   return 0;
@@ -422,8 +433,9 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
     e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  oz::contract_kernel<QW, BWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-      map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, row_scale, c->opscale, out, n_rows_out, st);
+  oz::contract_kernel<QW, BWD ? oz::MODE_BWD : oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+      map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
+      n_rows_out, nullptr, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -475,11 +487,80 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   return oz_contract<QW, true>(c, c->map_v[slot], c->Dp, c->Np, c->colscale, (double*)c->ppart, nsplit_out, st);
 }
 
+// ---- banded Toeplitz (convolution) contractions ----------------------------
+// (Phi p)_i = sum_m h_m p_{i-m}: every 128-row output tile multiplies the same
+// lower band [4][128][128 + lpad] with the operand window starting lpad rows
+// earlier; (Phi^T u)_j = sum_m h_m u_{j+m} uses the upper band and the window
+// starting at the tile.  Ends of the sequence arrive as TMA zero fill.
+template <int QW>
+int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, const Status* st) {
+  CKR(oz_init_kernels<QW>());
+  const int slot = QW / 8;
+  if (!c->map_p_ok[slot]) {
+    CKR(encode_u8_3d(&c->map_p[slot], c->pq, c->Dp, QW, 4, oz::KT, QW, 4));
+    c->map_p_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
+                               c->p_colmax_valid, c->vcolmax, st)));
+  const int nmb = (int)(c->Np / oz::BM);
+  const int grid = std::min(nmb, c->sm_count);
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+      c->map_band_fwd, c->map_p[slot], nmb, nmb, oz::BM + c->conv_lpad, (int)c->Dp, -c->conv_lpad, c->hrows,
+      c->opscale, vout, c->Np, c->N, c->vcolmax, st);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({0, c->evnext - 2});
+  }
+  c->launches++;
+  c->fwd_launches++;
+  CK(cudaGetLastError());
+  c->v_colmax_valid = true;
+  return 0;
+}
+
+template <int QW>
+int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
+  CKR(oz_init_kernels<QW>());
+  const int slot = QW / 8;
+  if (!c->map_v_ok[slot]) {
+    CKR(encode_u8_3d(&c->map_v[slot], c->vq, c->Np, QW, 4, oz::KT, QW, 4));
+    c->map_v_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
+                               nullptr, st)));
+  c->v_colmax_valid = false;
+  const int nmb = (int)(c->Dp / oz::BM);
+  const int grid = std::min(nmb, c->sm_count);
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+      c->map_band_adj, c->map_v[slot], nmb, nmb, oz::BM + c->conv_lpad, (int)c->Np, 0, c->hrows, c->opscale,
+      (double*)c->ppart, c->Dp, c->D, nullptr, st);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({1, c->evnext - 2});
+  }
+  c->launches++;
+  c->bwd_launches++;
+  CK(cudaGetLastError());
+  *nsplit_out = 1;
+  return 0;
+}
+
 // ---- the two contractions ----------------------------------------------
 // fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
 template <typename T, int QP>
 int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status* st) {
   if constexpr (std::is_same<T, double>::value) {
+    if (c->kind == 1) return conv_fwd<QP>(c, src, lds, qoff, vout, st);
     if (c->prec == COFEM_OZAKI) return oz_fwd<QP>(c, src, lds, qoff, vout, st);
   }
   using K = Kern<T, QP>;
@@ -519,6 +600,7 @@ int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status
 template <typename T, int QP>
 int run_bwd(cofem_ctx* c, const T* v, int* nsplit_out, const Status* st) {
   if constexpr (std::is_same<T, double>::value) {
+    if (c->kind == 1) return conv_bwd<QP>(c, v, nsplit_out, st);
     if (c->prec == COFEM_OZAKI) return oz_bwd<QP>(c, v, nsplit_out, st);
   }
   using K = Kern<T, QP>;
@@ -638,7 +720,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   // Phi P quantisation (k_update re-zeroes them every step)
   const bool oz = c->prec == COFEM_OZAKI;
   if (oz) {
-    CKR(ensure_oz(c));
+    if (c->kind == 0) CKR(ensure_oz(c));
     CK(cudaMemsetAsync(c->colmax, 0, ldq * sizeof(unsigned long long), c->stream));
   }
   unsigned long long* pmax = oz ? c->colmax : nullptr;
@@ -829,9 +911,11 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   std::vector<double> a(c->Dp, 1.0);
   CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
   if (em->theta_policy == COFEM_THETA_JACOBI) {
-    k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
-    c->launches++;
-    CK(cudaGetLastError());
+    if (c->kind == 0) {
+      k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
+      c->launches++;
+      CK(cudaGetLastError());
+    }
     CK(cudaMemcpyAsync(c->theta, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   } else if (em->theta_policy == COFEM_THETA_CUSTOM) {
     if (!theta) return fail(COFEM_EINVAL, "custom theta policy needs a theta vector");
@@ -967,6 +1051,115 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   return 0;
 }
 
+namespace {
+// signed base-256 digits of round(x), host side (same decomposition as oz::digits4)
+void host_digits4(double x, int8_t d[4]) {
+  long long v = llrint(x);
+  for (int a = 3; a >= 0; --a) {
+    const int8_t lo = (int8_t)(v & 0xFF);
+    d[a] = lo;
+    v = (v - lo) >> 8;
+  }
+}
+double host_pow2_ceil(double m) {
+  int e;
+  const double f = frexp(m, &e);
+  return f == 0.5 ? ldexp(1.0, e - 1) : ldexp(1.0, e);
+}
+}  // namespace
+
+int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const double* taps, int64_t ntaps,
+                             int precision) {
+  if (!out || !taps) return fail(COFEM_EINVAL, "null argument");
+  *out = nullptr;
+  if (dim < 1 || ntaps < 1 || ntaps > dim) return fail(COFEM_EINVAL, "need 1 <= ntaps <= dim");
+  if (precision != COFEM_OZAKI) return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI precision");
+  if (ntaps > 65536 - 256) return fail(COFEM_EINVAL, "at most 65280 taps");
+  double hmax = 0.0;
+  for (int64_t m = 0; m < ntaps; ++m) {
+    if (!std::isfinite(taps[m])) return fail(COFEM_EINVAL, "taps must be finite");
+    hmax = std::max(hmax, std::fabs(taps[m]));
+  }
+  if (hmax == 0.0) return fail(COFEM_EINVAL, "all-zero filter");
+  cofem_ctx* c = new cofem_ctx();
+  c->kind = 1;
+  c->device = device;
+  c->prec = precision;
+  c->N = c->D = dim;
+  c->Np = c->Dp = round_up(dim, PAD);
+  c->global_cols = dim;
+  c->conv_L = (int)ntaps;
+  c->conv_lpad = (int)round_up(ntaps - 1, oz::KT);
+  auto bail = [&](int rc) {
+    cofem_destroy(c);
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(COFEM_ECUDA, "stream create failed"));
+  double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty, &c->colscale, &c->hrows};
+  for (double** p : dvecs) {
+    if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
+    cudaMemset(*p, 0, c->Dp * sizeof(double));
+  }
+  if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
+  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "pinned status"));
+  for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  // operand buffers of the int8 path
+  if (cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp) != cudaSuccess ||
+      cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np) != cudaSuccess ||
+      cudaMalloc(&c->opscale, QCHUNK * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "operand buffers"));
+  // band digit planes: lower band (Phi) and upper band (Phi^T), one scale 2^e >= max |h|
+  const double hs = host_pow2_ceil(hmax);
+  const int nk = oz::BM + c->conv_lpad;
+  std::vector<int8_t> bf((size_t)4 * oz::BM * nk, 0), ba((size_t)4 * oz::BM * nk, 0);
+  for (int r = 0; r < oz::BM; ++r)
+    for (int col = 0; col < nk; ++col) {
+      const int mf = r + c->conv_lpad - col, ma = col - r;
+      int8_t d[4];
+      if (mf >= 0 && mf < ntaps) {
+        host_digits4(taps[mf] / hs * 1073741824.0, d);
+        for (int a = 0; a < 4; ++a) bf[((size_t)a * oz::BM + r) * nk + col] = d[a];
+      }
+      if (ma >= 0 && ma < ntaps) {
+        host_digits4(taps[ma] / hs * 1073741824.0, d);
+        for (int a = 0; a < 4; ++a) ba[((size_t)a * oz::BM + r) * nk + col] = d[a];
+      }
+    }
+  if (cudaMalloc(&c->band_fwd, bf.size()) != cudaSuccess || cudaMalloc(&c->band_adj, ba.size()) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "band planes"));
+  cudaMemcpy(c->band_fwd, bf.data(), bf.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->band_adj, ba.data(), ba.size(), cudaMemcpyHostToDevice);
+  int rc = encode_u8_3d(&c->map_band_fwd, c->band_fwd, nk, oz::BM, 4, oz::KT, oz::BM, 4);
+  if (!rc) rc = encode_u8_3d(&c->map_band_adj, c->band_adj, nk, oz::BM, 4, oz::KT, oz::BM, 4);
+  if (rc) return bail(rc);
+  // scales: output rows carry hs; operands are not pre-scaled (ones)
+  std::vector<double> hv(c->Dp, hs), ones(c->Dp, 1.0), csq(c->Dp, 0.0);
+  // column j of the lower-triangular Toeplitz matrix holds taps[0 : min(L, D - j)]
+  std::vector<double> cum(ntaps + 1, 0.0);
+  for (int64_t m = 0; m < ntaps; ++m) cum[m + 1] = cum[m] + taps[m] * taps[m];
+  for (int64_t j = 0; j < dim; ++j) csq[j] = cum[std::min<int64_t>(ntaps, dim - j)];
+  cudaMemcpy(c->hrows, hv.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->colscale, ones.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+  c->have_phi = true;
+  c->oz_ready = true;
+  *out = c;
+  return 0;
+}
+
 int cofem_destroy(cofem_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
@@ -974,7 +1167,7 @@ int cofem_destroy(cofem_ctx* c) {
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
-                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax};
+                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -991,6 +1184,7 @@ int cofem_destroy(cofem_ctx* c) {
 
 int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_device) {
   CKR(check_ctx(c, false));
+  if (c->kind != 0) return fail(COFEM_EINVAL, "not a dense dictionary context");
   if (!phi || ld < c->D) return fail(COFEM_EINVAL, "dictionary pointer / leading dimension");
   CK(cudaMemcpy2DAsync(c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
@@ -1011,6 +1205,7 @@ int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {
 
 int cofem_generate_gaussian_dictionary(cofem_ctx* c, uint64_t seed, double scale) {
   CKR(check_ctx(c, false));
+  if (c->kind != 0) return fail(COFEM_EINVAL, "not a dense dictionary context");
   const int64_t total = c->N * ((c->D + 3) / 4);
   const int gs = (int)std::min<int64_t>((total + 255) / 256, 64 * c->sm_count);
   k_gen_gaussian<<<gs, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->col_offset, seed, scale);
@@ -1024,6 +1219,7 @@ int cofem_generate_gaussian_dictionary(cofem_ctx* c, uint64_t seed, double scale
 
 int cofem_get_dictionary(cofem_ctx* c, float* out) {
   CKR(check_ctx(c));
+  if (c->kind != 0) return fail(COFEM_EINVAL, "not a dense dictionary context");
   CK(cudaMemcpy2D(out, c->D * sizeof(float), c->phi, c->Dp * sizeof(float), c->D * sizeof(float), c->N,
                   cudaMemcpyDeviceToHost));
   return 0;
@@ -1040,6 +1236,7 @@ int cofem_nccl_get_unique_id(void* out128) {
 
 int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
   CKR(check_ctx(c, false));
+  if (c->kind != 0 && nranks > 1) return fail(COFEM_EINVAL, "time-sharded convolution is not implemented yet");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
   CKR(nccl_load());
   ncclUniqueId id;
@@ -1074,6 +1271,10 @@ int cofem_system_apply(cofem_ctx* c, double beta, const double* alpha, const dou
 
 int cofem_column_sq_norms(cofem_ctx* c, double* out) {
   CKR(check_ctx(c));
+  if (c->kind == 1) {
+    CK(cudaMemcpy(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+  }
   k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
   c->launches++;
   CK(cudaGetLastError());

@@ -124,14 +124,23 @@ struct Cfg {
 // split s = w / n_mblocks): output rows [mb*128, +128), K range
 // [s*k_per_split, min(+k_per_split, k_total)).  Writes fp64
 // out[s][row][0:QW] = sum_k Phi(.)[row][k] * op[k][q] (already scaled).
-//   BWD == false: rows are i, K is j; row scale r_i, operand column scales scol
-//   BWD == true : rows are j, K is i; row scale c_j
-template <int QW, bool BWD>
+//   MODE_FWD : rows are i, K is j; row scale r_i (A = digit planes, K-major)
+//   MODE_BWD : rows are j, K is i; row scale c_j (A = the same planes, MN-major)
+//   MODE_BAND: banded Toeplitz operator (convolution dictionaries): every
+//     output tile sees the same 128 x k_per_split band matrix, so A's TMA
+//     coordinate is relative to the tile: K range [mb*128 + band_offset,
+//     + k_per_split); operand rows outside [0, K) arrive as TMA zero fill.
+// Rows >= rows_real are written as zeros; out_colmax (may be null) collects
+// the column maxima of |out| for the next quantisation (single-split modes).
+enum { MODE_FWD = 0, MODE_BWD = 1, MODE_BAND = 2 };
+template <int QW, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     contract_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                    int n_mblocks, int n_items, int k_per_split, int k_total, const double* __restrict__ row_scale,
-                    const double* __restrict__ op_scale, double* __restrict__ out, int64_t out_rows,
-                    const Status* __restrict__ st) {
+                    int n_mblocks, int n_items, int k_per_split, int k_total, int band_offset,
+                    const double* __restrict__ row_scale, const double* __restrict__ op_scale,
+                    double* __restrict__ out, int64_t out_rows, int64_t rows_real,
+                    unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st) {
+  constexpr bool BWD = MODE == MODE_BWD;
   using C = Cfg<QW>;
   if (st && st->done) return;
   extern __shared__ unsigned char smem_raw[];
@@ -171,14 +180,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int mb = w % n_mblocks, s = w / n_mblocks;
-        const int k0 = s * k_per_split;
-        const int k1 = min(k0 + k_per_split, k_total);
+        const int k0 = MODE == MODE_BAND ? mb * BM + band_offset : s * k_per_split;
+        const int k1 = MODE == MODE_BAND ? k0 + k_per_split : min(k0 + k_per_split, k_total);
         for (int k = k0; k < k1; k += KT) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sa = sm + stage * C::STAGE;
           unsigned char* sb = sa + A_STAGE;
           mbar_expect_tx(&full[stage], C::STAGE);
-          if (!BWD) {
+          if (MODE == MODE_BAND) {
+            tma_load_3d(sa, &map_a, &full[stage], k - k0, 0, 0);
+          } else if (!BWD) {
             tma_load_3d(sa, &map_a, &full[stage], k, mb * BM, 0);
           } else {
             tma_load_3d(sa, &map_a, &full[stage], mb * BM, k, 0);
@@ -202,9 +213,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0, tphase = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-        const int s = w / n_mblocks;
-        const int k0 = s * k_per_split;
-        const int k1 = min(k0 + k_per_split, k_total);
+        const int mb = w % n_mblocks, s = w / n_mblocks;
+        const int k0 = MODE == MODE_BAND ? mb * BM + band_offset : s * k_per_split;
+        const int k1 = MODE == MODE_BAND ? k0 + k_per_split : min(k0 + k_per_split, k_total);
         mbar_wait(tempty, tphase ^ 1);  // epilogue has drained the accumulators
         tphase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -270,11 +281,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(tempty);
       const int64_t row = (int64_t)mb * BM + row_in_tile;
-      const double rs = row_scale[row] * (1.0 / (SCALE30 * SCALE30));
+      const double rs = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
       double* o = out + ((int64_t)s * out_rows + row) * QW;
 #pragma unroll
       for (int q = 0; q < QW; q += 2) {
-        *reinterpret_cast<double2*>(o + q) = make_double2(acc[q] * rs * op_scale[q], acc[q + 1] * rs * op_scale[q + 1]);
+        const double v0 = acc[q] * rs * op_scale[q], v1 = acc[q + 1] * rs * op_scale[q + 1];
+        *reinterpret_cast<double2*>(o + q) = make_double2(v0, v1);
+        if (out_colmax) {  // warp max over its 32 rows, one atomic per warp and column
+          double m0 = fabs(v0), m1 = fabs(v1);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double o0 = __shfl_xor_sync(0xffffffffu, m0, off), o1 = __shfl_xor_sync(0xffffffffu, m1, off);
+            m0 = (o0 > m0 || o0 != o0) ? o0 : m0;
+            m1 = (o1 > m1 || o1 != o1) ? o1 : m1;
+          }
+          if (lane == 0) {
+            atomicMax(&out_colmax[q], (unsigned long long)__double_as_longlong(m0));
+            atomicMax(&out_colmax[q + 1], (unsigned long long)__double_as_longlong(m1));
+          }
+        }
       }
     }
   }

@@ -124,6 +124,87 @@ class DenseOperator(LinearOperator):
         return self.context("fp64").column_sq_norms()
 
 
+class ConvolutionOperator(LinearOperator):
+    """Causal convolution with a filter h: the D x D lower-triangular Toeplitz
+    matrix Phi_ij = h[i - j] (operators.py:182-225).
+
+    ``ConvolutionOperator(dim, decay)`` is the reference's filter
+    h[m] = (1 - decay)^m, m < D; ``ConvolutionOperator.from_taps(dim, taps)``
+    takes any FIR filter (BASELINE config 3: exp(-t/20), 256 taps, unit norm).
+    On the GPU both Phi and Phi^T run as banded int8 tensor-core contractions
+    (precision "ozaki"); taps below 2^-34 of the largest one are dropped there
+    (they are under the 2^-30 fixed-point resolution of the band).
+    """
+
+    kind = "exp-convolution"
+
+    def __init__(self, dim, decay=None, taps=None, device=0):
+        super().__init__(dim, dim)
+        if taps is None:
+            if decay is None or not 0.0 < decay < 1.0:
+                raise ValueError(f"decay must lie in (0, 1), got {decay}")
+            self.decay = float(decay)
+            taps = (1.0 - self.decay) ** np.arange(dim, dtype=np.float64)
+        else:
+            self.decay = None
+            self.kind = "fir-convolution"
+            taps = np.asarray(taps, dtype=np.float64)
+            if taps.ndim != 1 or not 1 <= taps.size <= dim:
+                raise ValueError("taps must be a 1-D array of length 1..dim")
+        taps = np.array(taps, dtype=np.float64)
+        taps.flags.writeable = False
+        self.filter = taps
+        self.device = device
+        self._ctx = {}
+
+    @classmethod
+    def from_taps(cls, dim, taps, device=0):
+        return cls(dim, taps=taps, device=device)
+
+    def gpu_taps(self):
+        h = self.filter
+        keep = np.flatnonzero(np.abs(h) >= np.abs(h).max() * 2.0**-34)
+        return h[: keep[-1] + 1] if keep.size else h[:1]
+
+    def context(self, precision="ozaki"):
+        if precision != "ozaki":
+            raise NotImplementedError("convolution dictionaries run in the 'ozaki' precision mode")
+        ctx = self._ctx.get(precision)
+        if ctx is None:
+            ctx = _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
+            self._ctx[precision] = ctx
+        return ctx
+
+    def release(self):
+        for ctx in self._ctx.values():
+            ctx.close()
+        self._ctx.clear()
+
+    def _apply(self, V):
+        return self.context().apply(V)
+
+    def _apply_adjoint(self, U):
+        return self.context().apply_adjoint(U)
+
+    def materialize(self):
+        d, h = self.n_cols, self.filter
+        m = np.zeros((d, d))
+        for j in range(d):
+            n = min(h.size, d - j)
+            m[j:j + n, j] = h[:n]
+        return m
+
+    def column_sq_norms(self):
+        """Truncated geometric / FIR sums: column j holds h[0 : min(L, D - j)]."""
+        c = np.concatenate([[0.0], np.cumsum(self.filter * self.filter)])
+        return c[np.minimum(self.filter.size, self.n_cols - np.arange(self.n_cols))]
+
+
+def build_exp_convolution(dim, decay):
+    """Lower-triangular convolution with filter (1-rho)^m, m = 0..D-1 (operators.py:243-245)."""
+    return ConvolutionOperator(dim, decay)
+
+
 def build_dense_gaussian(n_rows, dim, rng):
     """Dense dictionary with i.i.d. N(0, 1/N) entries (operators.py:227-232).
 
@@ -156,8 +237,10 @@ class SystemMatrix:
     def dim(self):
         return self.op.n_cols
 
-    def apply(self, V, precision="fp64"):
+    def apply(self, V, precision=None):
         """A @ V on the GPU without materialising A."""
         V, single = _as_columns(V, self.dim, "system apply")
+        if precision is None:
+            precision = "ozaki" if isinstance(self.op, ConvolutionOperator) else "fp64"
         out = self.op.context(precision).system_apply(self.beta, self.alpha, V)
         return out[:, 0] if single else out

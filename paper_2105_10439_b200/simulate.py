@@ -56,6 +56,66 @@ CONFIGS = {
 }
 
 
+@dataclass(frozen=True)
+class ConvConfig:
+    """BASELINE config 3: calcium-imaging-style deconvolution (synthetic)."""
+
+    name: str
+    D: int           # N = D time samples
+    ntaps: int       # h[t] = exp(-t / tau), t < ntaps, unit L2 norm
+    tau: float
+    p: float         # Bernoulli spike probability per sample (Exp(1) amplitudes)
+    sigma: float
+    K: int
+    T: int
+    U: int
+    tol: float
+    seed: int = 0
+
+    @property
+    def N(self):
+        return self.D
+
+    @property
+    def beta(self):
+        return 1.0 / self.sigma**2
+
+    def taps(self):
+        h = np.exp(-np.arange(self.ntaps, dtype=np.float64) / self.tau)
+        return h / np.linalg.norm(h)
+
+    def cofem_config(self, precision="ozaki", **over):
+        cg = CgConfig(max_steps=self.U, tolerance=self.tol, precision=precision)
+        kw = dict(iterations=self.T, probes=self.K, cg=cg, seed=self.seed)
+        kw.update(over)
+        return CofemConfig(**kw)
+
+
+CONV_CONFIGS = {
+    "conv-large": ConvConfig("conv-large", 2**22, 256, 20.0, 0.01, 0.05, 30, 30, 200, 1e-5),
+    "conv-mid": ConvConfig("conv-mid", 2**16, 256, 20.0, 0.01, 0.05, 30, 5, 200, 1e-5),
+}
+
+
+def spike_train(D, p, seed):
+    """Nonnegative spikes: Bernoulli(p) support, Exp(1) amplitudes, substream(seed, 1)."""
+    rng = substream(seed, 1)
+    support = rng.random(D) < p
+    return np.where(support, rng.exponential(1.0, D), 0.0)
+
+
+def conv_problem(cfg: ConvConfig):
+    """(SblProblem, z_true) for a convolution configuration; y computed in float64."""
+    from scipy.signal import fftconvolve
+
+    from .operators import ConvolutionOperator
+
+    h = cfg.taps()
+    z = spike_train(cfg.D, cfg.p, cfg.seed)
+    y = fftconvolve(z, h)[: cfg.D] + cfg.sigma * substream(cfg.seed, 2).standard_normal(cfg.D)
+    return SblProblem(y, ConvolutionOperator.from_taps(cfg.D, h), cfg.beta), z
+
+
 def gaussian_dictionary(N, D, seed):
     """N x D float32, entries N(0, 1/N), from substream(seed, 0)."""
     rng = substream(seed, 0)

@@ -151,6 +151,29 @@ def make_variants():
                         **out)
 
 
+def make_conv():
+    """Reference ConvolutionOperator (operators.py:182-225): apply / adjoint /
+    column norms, and run_cofem on the reference's own convolution workload
+    (simulate.build_problem with dictionary='convolution')."""
+    from sbl.operators import ConvolutionOperator
+    from sbl.simulate import ExperimentSpec, build_problem
+
+    rng = np.random.default_rng(77)
+    op = ConvolutionOperator(512, 0.04)
+    V = rng.standard_normal((512, 21))
+    U = rng.standard_normal((512, 5))
+    out = {"V": V, "U": U, "fwd": op.apply(V), "adj": op.apply_adjoint(U), "colsq": op.column_sq_norms()}
+    spec = ExperimentSpec(dictionary="convolution", D=512, rho=0.04, seed=400,  # data seed; cofem seed 0
+                          cofem=sbl.CofemConfig(iterations=20, probes=20,
+                                                cg=sbl.CgConfig(max_steps=400, tolerance=1e-6)))
+    problem, z = build_problem(spec)
+    state, est, diag = ref_cofem.run_cofem(problem, spec.cofem)
+    out.update(y=np.asarray(problem.y), z=z, beta=np.array(problem.beta), alpha=state.alpha, mu=est.mu,
+               s=est.s, cg_steps=np.array([r["cg_steps"] for r in diag]))
+    print(f"conv cofem steps {[r['cg_steps'] for r in diag]}")
+    np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **out)
+
+
 def make_known_answers():
     """Known-answer values the reference's own tests pin (test_cofem.py:187-190,
     test_cg.py:450-466, test_operators.py:392-394), recomputed from the reference."""
@@ -166,9 +189,11 @@ def make_known_answers():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid"}
+    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid", "conv"}
     if "known" in which:
         make_known_answers()
+    if "conv" in which:
+        make_conv()
     if "pcg" in which:
         make_pcg()
     if "variants" in which:

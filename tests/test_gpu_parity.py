@@ -303,3 +303,54 @@ def test_dense_large_pcg_residual_and_determinism():
     assert true_res <= 5 * c.tol
     X64, rep64, _, _ = ctx64.pcg_solve(c.beta, alpha, minv, B, 60, c.tol)
     assert rel(X1, X64) <= 1e-4
+
+
+# --------------------------------------------------- convolution dictionary --
+def test_convolution_apply_matches_reference_golden():
+    from paper_2105_10439_b200 import build_exp_convolution
+
+    g = golden("conv_cases.npz")
+    op = build_exp_convolution(512, 0.04)
+    assert rel(op.apply(g["V"]), g["fwd"]) <= 5e-9
+    assert rel(op.apply_adjoint(g["U"]), g["adj"]) <= 5e-9
+    np.testing.assert_allclose(op.context().column_sq_norms(), g["colsq"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("dim,ntaps,q", [(4096, 256, 31), (1000, 37, 5), (300, 300, 2), (64, 1, 8)])
+def test_fir_convolution_matches_numpy(dim, ntaps, q):
+    from paper_2105_10439_b200 import ConvolutionOperator
+
+    rng = np.random.default_rng(dim + ntaps)
+    h = np.exp(-np.arange(ntaps) / 20.0)
+    h /= np.linalg.norm(h)
+    op = ConvolutionOperator.from_taps(dim, h)
+    V = rng.standard_normal((dim, q))
+    U = rng.standard_normal((dim, q))
+    ref_f = np.stack([np.convolve(V[:, k], h)[:dim] for k in range(q)], axis=1)
+    ref_a = np.stack([np.correlate(np.concatenate([U[:, k], np.zeros(ntaps - 1)]), h, "valid") for k in range(q)],
+                     axis=1)
+    assert rel(op.apply(V), ref_f) <= 5e-9
+    assert rel(op.apply_adjoint(U), ref_a) <= 5e-9
+    A = 9.0 * ref_a
+    alpha = rng.random(dim) + 0.5
+    sysm = SystemMatrix(op, 9.0, alpha)
+    want = 9.0 * np.stack([np.correlate(np.concatenate([ref_f[:, k], np.zeros(ntaps - 1)]), h, "valid")
+                           for k in range(q)], axis=1) + alpha[:, None] * V
+    assert rel(sysm.apply(V), want) <= 5e-9
+    del A
+
+
+def test_run_cofem_convolution_parity():
+    """The reference's own convolution workload (D=512, rho=0.04, 20 EM
+    iterations): mu and alpha within 1e-4, identical support."""
+    from paper_2105_10439_b200 import build_exp_convolution
+
+    g = golden("conv_cases.npz")
+    prob = SblProblem(g["y"], build_exp_convolution(512, 0.04), float(g["beta"]))
+    cfg = CofemConfig(iterations=20, probes=20, seed=0, cg=CgConfig(max_steps=400, tolerance=1e-6))
+    st, est, diag = run_cofem(prob, cfg)
+    emu, ea = rel(est.mu, g["mu"]), rel(st.alpha, g["alpha"])
+    assert emu <= 1e-4 and ea <= 1e-4, (emu, ea, [d["cg_steps"] for d in diag], list(g["cg_steps"]))
+    np.testing.assert_array_equal(st.alpha < PRUNE, g["alpha"] < PRUNE)
+    nref, nour = S.nmse(g["mu"], g["z"]), S.nmse(est.mu, g["z"])
+    assert abs(nour - nref) <= 0.01 * nref

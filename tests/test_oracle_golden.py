@@ -107,3 +107,38 @@ def test_oracle_divergence_and_entry_cases():
     assert rep.steps_taken == 0 and rep.converged and rep.final_relative_residual == 0.0
     rep = O.pcg_solve(fn, np.ones((4, 1)), np.ones(4), O.CgConfig(max_steps=5, tolerance=1.5))
     assert rep.steps_taken == 0 and rep.final_relative_residual == 1.0
+
+
+def test_oracle_convolution_matches_reference():
+    """oracle conv_op (FFT path) and the run_cofem loop on the reference's own
+    convolution workload (simulate.build_problem, dictionary='convolution')."""
+    g = golden("conv_cases.npz")
+    op = O.conv_op(512, (1.0 - 0.04) ** np.arange(512, dtype=np.float64))  # operators.py:196
+    np.testing.assert_array_equal(op.apply(g["V"]), g["fwd"])
+    np.testing.assert_array_equal(op.adjoint(g["U"]), g["adj"])
+    np.testing.assert_allclose(op.col_sq_norms(), g["colsq"], rtol=1e-14)
+    cfg = O.CofemConfig(iterations=20, probes=20, seed=0, cg=O.CgConfig(max_steps=400, tolerance=1e-6))
+    alpha, mu, s, diag = O.run_cofem(op, g["y"], float(g["beta"]), cfg)
+    assert [d["cg_steps"] for d in diag] == list(g["cg_steps"])
+    np.testing.assert_array_equal(mu, g["mu"])
+    np.testing.assert_array_equal(alpha, g["alpha"])
+
+
+def test_convolution_operator_host_side_matches_reference():
+    from paper_2105_10439_b200 import ConvolutionOperator, build_exp_convolution
+
+    g = golden("conv_cases.npz")
+    op = build_exp_convolution(512, 0.04)
+    np.testing.assert_allclose(op.column_sq_norms(), g["colsq"], rtol=1e-14)
+    small = ConvolutionOperator(3, 0.5)
+    np.testing.assert_allclose(small.column_sq_norms(), [1.3125, 1.25, 1.0], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(small.materialize(), [[1, 0, 0], [0.5, 1, 0], [0.25, 0.5, 1]])
+    np.testing.assert_allclose(build_exp_convolution(4, 0.04).filter, [1.0, 0.96, 0.9216, 0.884736], atol=1e-15)
+    fir = ConvolutionOperator.from_taps(10, [1.0, -0.5, 0.25])
+    np.testing.assert_allclose(fir.column_sq_norms()[-2:], [1.25, 1.0])
+    with pytest.raises(ValueError):
+        ConvolutionOperator(8, 0.0)
+    with pytest.raises(ValueError):
+        ConvolutionOperator(8, 1.0)
+    with pytest.raises(ValueError):
+        ConvolutionOperator.from_taps(2, [1.0, 2.0, 3.0])
