@@ -419,9 +419,11 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
   const int64_t ntiles = k_total / oz::KT;
   SplitPlan sp = plan_splits(n_mblocks, ntiles, oz::KT, c->sm_count, (double)n_rows_out * QW * 8.0,
                              (double)c->Np * c->Dp * 4.0);
-  // exact int32 accumulation: |digit products| <= 2^14, so keep K <= 2^16 per item
-  while (sp.per_split > 65536 || (size_t)sp.nsplit * n_rows_out * QW * 8 > (BWD ? c->ppart_cap : c->vpart_cap)) {
-    if (sp.per_split > 65536) sp.per_split = 65536;
+  // exact int32 accumulation: <= 4 digit products of <= 2^14 per significance
+  // block, so keep K <= 2^15 per item
+  while (sp.per_split > oz::MAX_K_PER_ITEM ||
+         (size_t)sp.nsplit * n_rows_out * QW * 8 > (BWD ? c->ppart_cap : c->vpart_cap)) {
+    if (sp.per_split > oz::MAX_K_PER_ITEM) sp.per_split = oz::MAX_K_PER_ITEM;
     else sp.per_split *= 2;
     sp.nsplit = (int)((k_total + sp.per_split - 1) / sp.per_split);
   }
@@ -492,6 +494,27 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
 // lower band [4][128][128 + lpad] with the operand window starting lpad rows
 // earlier; (Phi^T u)_j = sum_m h_m u_{j+m} uses the upper band and the window
 // starting at the tile.  Ends of the sequence arrive as TMA zero fill.
+// launch the band contraction: smem-resident band when it fits, else the
+// streaming MODE_BAND of contract_kernel
+template <int QW>
+void launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
+                 double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
+  const int grid = std::min(nmb, c->sm_count);
+  const size_t sm = oz::BandCfg<QW>::smem(nk);
+  if (sm <= 227 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(oz::band_kernel<QW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr = true;
+    }
+    oz::band_kernel<QW><<<grid, oz::NTHREADS, sm, c->stream>>>(map_a, map_b, nmb, nk, offset, c->hrows, c->opscale,
+                                                                out, rows_real, colmax, st);
+  } else {
+    oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+        map_a, map_b, nmb, nmb, nk, 0, offset, c->hrows, c->opscale, out, out_rows, rows_real, colmax, st);
+  }
+}
+
 template <int QW>
 int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, const Status* st) {
   CKR(oz_init_kernels<QW>());
@@ -503,14 +526,12 @@ int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, c
   CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
                                c->p_colmax_valid, c->vcolmax, st)));
   const int nmb = (int)(c->Np / oz::BM);
-  const int grid = std::min(nmb, c->sm_count);
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-      c->map_band_fwd, c->map_p[slot], nmb, nmb, oz::BM + c->conv_lpad, (int)c->Dp, -c->conv_lpad, c->hrows,
-      c->opscale, vout, c->Np, c->N, c->vcolmax, st);
+  launch_band<QW>(c, c->map_band_fwd, c->map_p[slot], nmb, oz::BM + c->conv_lpad, -c->conv_lpad, vout, c->Np,
+                  c->N, c->vcolmax, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -535,14 +556,12 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
                                nullptr, st)));
   c->v_colmax_valid = false;
   const int nmb = (int)(c->Dp / oz::BM);
-  const int grid = std::min(nmb, c->sm_count);
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-      c->map_band_adj, c->map_v[slot], nmb, nmb, oz::BM + c->conv_lpad, (int)c->Np, 0, c->hrows, c->opscale,
-      (double*)c->ppart, c->Dp, c->D, nullptr, st);
+  launch_band<QW>(c, c->map_band_adj, c->map_v[slot], nmb, oz::BM + c->conv_lpad, 0, (double*)c->ppart, c->Dp,
+                  c->D, nullptr, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -1074,7 +1093,7 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   *out = nullptr;
   if (dim < 1 || ntaps < 1 || ntaps > dim) return fail(COFEM_EINVAL, "need 1 <= ntaps <= dim");
   if (precision != COFEM_OZAKI) return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI precision");
-  if (ntaps > 65536 - 256) return fail(COFEM_EINVAL, "at most 65280 taps");
+  if (ntaps > oz::MAX_K_PER_ITEM - 2 * oz::BM) return fail(COFEM_EINVAL, "at most 32512 taps");
   double hmax = 0.0;
   for (int64_t m = 0; m < ntaps; ++m) {
     if (!std::isfinite(taps[m])) return fail(COFEM_EINVAL, "taps must be finite");

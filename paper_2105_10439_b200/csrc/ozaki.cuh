@@ -94,31 +94,121 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "r"(addr))
 
 // Digit plane a of Phi is multiplied with operand planes b <= 4 - a only.
-// The three dropped pairs (a + b >= 5) are worth <= 2^(8*1) / 2^(8*6) per
-// digit product; with full-range low digits against leading digits of a few
-// bits they still sit ~1e-10 below the result -- under the 2^-30
-// quantisation of the factors -- while trimming a sixth of the tensor work
-// (and with it power: the contraction runs at the 1 kW cap).  Dropping the
-// a + b = 4 pairs as well measured 2.6e-8 relative error, so they stay.
-// N_a = QW * min(4, 5 - a) rounded up to the UMMA granularity of 16 (the few
-// extra B rows are real smem rows of the next plane; their accumulator
-// columns are never read).
+// The three dropped pairs (a + b >= 5) sit ~1e-10 below the result -- under
+// the 2^-30 quantisation of the factors -- and trimming them cuts a sixth of
+// the tensor work (and power: the contraction runs at the 1 kW cap); dropping
+// also a + b = 4 was measured to cost 2.6e-8, so those stay.
+//
+// Significance-aligned accumulation: the MMA for plane a writes its N = QW
+// nb(a) columns at TMEM offset a QW, so operand plane b lands in column block
+// s = a + b and every product of equal significance accumulates in the same
+// block.  Five blocks (s = 0..4) hold the whole result; columns past block 4
+// (from rounding N up to the UMMA granularity of 16) only ever collect pruned
+// s >= 5 products and are never read.  A set is <= 160 columns, so TMEM holds
+// two sets and the epilogue of one tile overlaps the MMAs of the next.  The
+// epilogue zeroes its set with tcgen05.st after reading it, so every MMA just
+// accumulates.  Exactness: |block| <= 4 pairs * 2^14 * K < 2^31 for K <= 2^15.
 template <int QW>
 struct Cfg {
   static constexpr int NB = 4 * QW;  // B tile rows: the four operand planes side by side
   static constexpr int B_STAGE = NB * KT;
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1280;
   __host__ __device__ static constexpr int nb_of(int a) { return a <= 1 ? 4 : 5 - a; }  // operand planes used
   __host__ __device__ static constexpr int n_of(int a) { return ((QW * nb_of(a) + 15) / 16) * 16; }
-  __host__ __device__ static constexpr int col_of(int a) {
-    return a == 0 ? 0 : a == 1 ? n_of(0) : a == 2 ? n_of(0) + n_of(1) : n_of(0) + n_of(1) + n_of(2);
-  }
-  static constexpr int TMEM_COLS = col_of(3) + n_of(3);
+  static constexpr int SET_COLS = 256;  // TMEM columns per accumulator set (two sets)
   static_assert(QW % 8 == 0 && QW <= 32, "QW in {8,16,24,32}");
   static_assert(STAGE % 1024 == 0, "stages must stay 1024-B aligned for the swizzle atoms");
-  static_assert(TMEM_COLS <= 512, "accumulators must fit TMEM");
+  static_assert(2 * QW + ((QW * 3 + 15) / 16) * 16 <= SET_COLS && 5 * QW <= SET_COLS, "set must fit");
 };
+constexpr int MAX_K_PER_ITEM = 1 << 15;
+
+// one K=64 stage: 2 k-steps x 4 digit planes of A against the operand tile
+template <int QW, bool MN_MAJOR>
+__device__ __forceinline__ void issue_stage(uint32_t sa, uint32_t sb, uint32_t tset, uint32_t idesc0) {
+  using C = Cfg<QW>;
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+    const uint64_t db = sdesc(sb + kk * 32, 16, 512);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      uint64_t da;
+      if (!MN_MAJOR) da = sdesc(sa + a * (BM * KT) + kk * 32, 16, 512);
+      else da = sdesc(sa + a * (64 * KT) + kk * (32 * KT), A_STAGE / 2, 512);
+      const uint32_t idesc = idesc0 | ((uint32_t)(C::n_of(a) >> 3) << 17);
+      mma_i8(tset + a * QW, da, db, idesc, 1u);
+    }
+  }
+}
+
+// zero both accumulator sets of this warp's TMEM lane quarter (prologue)
+__device__ __forceinline__ void tmem_zero_all(uint32_t tmem, int quarter) {
+  const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < 512; c += 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(base + c), "r"(0));
+  asm volatile("tcgen05.wait::st.sync.aligned;");
+}
+
+// Epilogue of one tile for the calling thread's row: read the five
+// significance blocks, re-zero them, combine exactly in int64 and write
+// out[q] = value * scale * op_scale[q].  With TRACK the thread keeps running
+// per-column maxima of |out| in registers (bit patterns of non-negative
+// doubles order like unsigned integers, NaN above everything); they are
+// folded across the warp and the CTA once, at the end of the kernel.
+template <int QW, bool TRACK>
+__device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, const double* __restrict__ op_scale,
+                                             double* o, unsigned long long (&cm)[QW]) {
+#pragma unroll
+  for (int q0 = 0; q0 < QW; q0 += 8) {
+    uint32_t r[5][8];
+#pragma unroll
+    for (int sb = 0; sb < 5; ++sb)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]),
+                     "=r"(r[sb][5]), "=r"(r[sb][6]), "=r"(r[sb][7])
+                   : "r"(tset_lane + sb * QW + q0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int sb = 0; sb < 5; ++sb)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tset_lane + sb * QW + q0),
+                   "r"(0));
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      // value = 2^16 (S0 2^32 + S1 2^24 + S2 2^16 + S3 2^8 + S4), |S1 2^24 + ...| < 2^57
+      const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                           ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+      const double val = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * 65536.0;
+      v[t] = val * scale * op_scale[q0 + t];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + q0 + t) = make_double2(v[t], v[t + 1]);
+    if (TRACK) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const unsigned long long m = (unsigned long long)__double_as_longlong(fabs(v[t]));
+        cm[q0 + t] = m > cm[q0 + t] ? m : cm[q0 + t];
+      }
+    }
+  }
+}
+
+// fold the per-lane column maxima over the warp into this warp's smem slice
+template <int QW>
+__device__ __forceinline__ void warp_fold_max(unsigned long long (&cm)[QW], unsigned long long* slice) {
+#pragma unroll
+  for (int q = 0; q < QW; ++q) {
+    unsigned long long m = cm[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, off);
+      m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0) slice[q] = m;
+  }
+}
 
 // Persistent contraction.  Work item w (< n_items) = (mb = w % n_mblocks,
 // split s = w / n_mblocks): output rows [mb*128, +128), K range
@@ -126,10 +216,11 @@ struct Cfg {
 // out[s][row][0:QW] = sum_k Phi(.)[row][k] * op[k][q] (already scaled).
 //   MODE_FWD : rows are i, K is j; row scale r_i (A = digit planes, K-major)
 //   MODE_BWD : rows are j, K is i; row scale c_j (A = the same planes, MN-major)
-//   MODE_BAND: banded Toeplitz operator (convolution dictionaries): every
-//     output tile sees the same 128 x k_per_split band matrix, so A's TMA
-//     coordinate is relative to the tile: K range [mb*128 + band_offset,
-//     + k_per_split); operand rows outside [0, K) arrive as TMA zero fill.
+//   MODE_BAND: banded Toeplitz operator streamed from L2 (long filters; see
+//     band_kernel for the smem-resident version): every output tile sees the
+//     same 128 x k_per_split band, so A's TMA coordinate is relative to the
+//     tile: K range [mb*128 + band_offset, + k_per_split); operand rows outside
+//     [0, K) arrive as TMA zero fill.
 // Rows >= rows_real are written as zeros; out_colmax (may be null) collects
 // the column maxima of |out| for the next quantisation (single-split modes).
 enum { MODE_FWD = 0, MODE_BWD = 1, MODE_BAND = 2 };
@@ -147,9 +238,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * C::STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(tmem_holder + 2);  // [4 warps][QW]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -157,12 +249,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
   }
+  (void)0;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(512));
@@ -172,6 +267,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_holder;
+  if (warp >= 2) tmem_zero_all(tmem, warp & 3);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -211,100 +310,210 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((BWD ? 1u : 0u) << 15) |
                               ((uint32_t)(BM >> 4) << 24);
       int stage = 0;
-      uint32_t phase = 0, tphase = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
         const int mb = w % n_mblocks, s = w / n_mblocks;
         const int k0 = MODE == MODE_BAND ? mb * BM + band_offset : s * k_per_split;
         const int k1 = MODE == MODE_BAND ? k0 + k_per_split : min(k0 + k_per_split, k_total);
-        mbar_wait(tempty, tphase ^ 1);  // epilogue has drained the accumulators
-        tphase ^= 1;
+        const int buf = it & 1;
+        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);  // this set has been drained and re-zeroed
         asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t tset = tmem + buf * C::SET_COLS;
         for (int k = k0; k < k1; k += KT) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t sa = smem_u32(sm + stage * C::STAGE);
-          const uint32_t sb = sa + A_STAGE;
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const uint64_t db = sdesc(sb + kk * 32, 16, 512);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              uint64_t da;
-              if (!BWD) da = sdesc(sa + a * (BM * KT) + kk * 32, 16, 512);
-              else da = sdesc(sa + a * (64 * KT) + kk * (32 * KT), A_STAGE / 2, 512);
-              const uint32_t idesc = idesc0 | ((uint32_t)(C::n_of(a) >> 3) << 17);
-              mma_i8(tmem + C::col_of(a), da, db, idesc, (k > k0 || kk > 0) ? 1u : 0u);
-            }
-          }
+          issue_stage<QW, BWD>(sa, sa + A_STAGE, tset, idesc0);
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(tfull);  // accumulators complete
+        mma_commit(&tfull[buf]);  // accumulators complete
       }
     }
   } else {
     // ---------------- epilogue: warps 2..5 -> TMEM lane quarters (warp % 4) ----------------
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
-    uint32_t tphase = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    unsigned long long cm[QW];
+#pragma unroll
+    for (int q = 0; q < QW; ++q) cm[q] = 0ull;
+    int it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const int mb = w % n_mblocks, s = w / n_mblocks;
-      mbar_wait(tfull, tphase);
-      tphase ^= 1;
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      double acc[QW];
-#pragma unroll
-      for (int q = 0; q < QW; ++q) acc[q] = 0.0;
-      const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-#pragma unroll
-        for (int b = 0; b < C::nb_of(a); ++b) {
-          // digit weights 256^(3-a) * 256^(3-b) relative to 2^48
-          const double wgt = (double)(1ull << (8 * (6 - a - b)));
-#pragma unroll
-          for (int q0 = 0; q0 < QW; q0 += 8) {
-            uint32_t r[8];
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                           "=r"(r[7])
-                         : "r"(base + C::col_of(a) + b * QW + q0));
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc[q0 + t] = fma((double)(int32_t)r[t], wgt, acc[q0 + t]);
-          }
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(tempty);
       const int64_t row = (int64_t)mb * BM + row_in_tile;
-      const double rs = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
-      double* o = out + ((int64_t)s * out_rows + row) * QW;
-#pragma unroll
-      for (int q = 0; q < QW; q += 2) {
-        const double v0 = acc[q] * rs * op_scale[q], v1 = acc[q + 1] * rs * op_scale[q + 1];
-        *reinterpret_cast<double2*>(o + q) = make_double2(v0, v1);
-        if (out_colmax) {  // warp max over its 32 rows, one atomic per warp and column
-          double m0 = fabs(v0), m1 = fabs(v1);
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            const double o0 = __shfl_xor_sync(0xffffffffu, m0, off), o1 = __shfl_xor_sync(0xffffffffu, m1, off);
-            m0 = (o0 > m0 || o0 != o0) ? o0 : m0;
-            m1 = (o1 > m1 || o1 != o1) ? o1 : m1;
-          }
-          if (lane == 0) {
-            atomicMax(&out_colmax[q], (unsigned long long)__double_as_longlong(m0));
-            atomicMax(&out_colmax[q + 1], (unsigned long long)__double_as_longlong(m1));
+      const double scale = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
+      if (out_colmax)
+        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
+                               out + ((int64_t)s * out_rows + row) * QW, cm);
+      else
+        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
+                                out + ((int64_t)s * out_rows + row) * QW, cm);
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&tempty[buf]);
+    }
+    if (out_colmax) warp_fold_max<QW>(cm, cmax + (warp - 2) * QW);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (out_colmax && threadIdx.x < QW) {
+    unsigned long long m = cmax[threadIdx.x];
+    for (int w = 1; w < 4; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
+    atomicMax(&out_colmax[threadIdx.x], m);
+  }
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// Band-resident Toeplitz contraction (convolution dictionaries).  The whole
+// 128 x nk band (4 digit planes, nk = 128 + lpad bytes per row) is loaded into
+// shared memory ONCE per CTA; the TMA ring then carries only the operand
+// windows (4 QW x 64 B per stage), so the L2 -> SM traffic per output tile is
+// the window alone.  Same significance-aligned, double-buffered accumulation
+// and epilogue as contract_kernel.
+constexpr int BSTAGES = 4;
+template <int QW>
+struct BandCfg {
+  static constexpr int B_STAGE = 4 * QW * KT;
+  static size_t smem(int nk) { return (size_t)nk * 4 * BM + (size_t)BSTAGES * B_STAGE + 1024 + 1280; }
+};
+
+template <int QW>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    band_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                int n_mblocks, int nk, int band_offset, const double* __restrict__ row_scale,
+                const double* __restrict__ op_scale, double* __restrict__ out, int64_t rows_real,
+                unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st) {
+  using C = Cfg<QW>;
+  using BC = BandCfg<QW>;
+  if (st && st->done) return;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nst = nk / KT;                          // band stages
+  unsigned char* band = sm;                         // [nst][4 planes][128][64]
+  unsigned char* ring = sm + (size_t)nst * A_STAGE; // [BSTAGES][4 QW][64]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + BSTAGES * BC::B_STAGE);
+  uint64_t* empty = full + BSTAGES;
+  uint64_t* band_full = empty + BSTAGES;
+  uint64_t* tfull = band_full + 1;  // [2]
+  uint64_t* tempty = tfull + 2;     // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(tmem_holder + 2);  // [4 warps][QW]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < BSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(band_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  (void)0;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_holder;
+  if (warp >= 2) tmem_zero_all(tmem, warp & 3);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // band once, then the operand windows of every tile
+      mbar_expect_tx(band_full, (uint32_t)(nst * A_STAGE));
+      for (int s = 0; s < nst; ++s) tma_load_3d(band + (size_t)s * A_STAGE, &map_a, band_full, s * KT, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x) {
+        const int k0 = mb * BM + band_offset;
+        for (int s = 0; s < nst; ++s) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], BC::B_STAGE);
+          tma_load_3d(ring + stage * BC::B_STAGE, &map_b, &full[stage], k0 + s * KT, 0, 0);
+          if (++stage == BSTAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
     }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BM >> 4) << 24);
+      mbar_wait(band_full, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t tset = tmem + buf * C::SET_COLS;
+        for (int s = 0; s < nst; ++s) {
+          mbar_wait(&full[stage], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          issue_stage<QW, false>(smem_u32(band + (size_t)s * A_STAGE), smem_u32(ring + stage * BC::B_STAGE), tset,
+                                 idesc0);
+          mma_commit(&empty[stage]);
+          if (++stage == BSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    unsigned long long cm[QW];
+#pragma unroll
+    for (int q = 0; q < QW; ++q) cm[q] = 0ull;
+    int it = 0;
+    for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int64_t row = (int64_t)mb * BM + row_in_tile;
+      const double scale = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
+      if (out_colmax)
+        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
+                               out + row * QW, cm);
+      else
+        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
+                                out + row * QW, cm);
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&tempty[buf]);
+    }
+    if (out_colmax) warp_fold_max<QW>(cm, cmax + (warp - 2) * QW);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (out_colmax && threadIdx.x < QW) {
+    unsigned long long m = cmax[threadIdx.x];
+    for (int w = 1; w < 4; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
+    atomicMax(&out_colmax[threadIdx.x], m);
+  }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
