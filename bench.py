@@ -38,7 +38,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "CoFEM EM iters/sec at D=65536,N=16384,K=20 (fp32)"
-METRICS = {"conv-large": "CoFEM EM iters/sec, convolution dictionary N=D=2^22, 256 taps, K=30"}
+METRICS = {"conv-large": "CoFEM EM iters/sec, convolution dictionary N=D=2^22, 256 taps, K=30",
+           "dct-large": "CoFEM EM iters/sec, 2-D partial DCT 1024x1024 (D=2^20, 25% kept), K=20"}
 UNIT = "EM iter/s"
 
 
@@ -192,7 +193,7 @@ def run_ours(args):
     from paper_2105_10439_b200 import simulate as S
 
     world, rank, local = dist_env()
-    if args.config in S.CONV_CONFIGS:
+    if args.config in S.CONV_CONFIGS or args.config in S.DCT_CONFIGS:
         return run_ours_conv(args)
     c = S.CONFIGS[args.config]
     dist = None
@@ -331,19 +332,19 @@ def run_ours(args):
 
 
 def run_ours_conv(args):
-    """BASELINE config 3: banded int8 tensor-core convolution, single GPU."""
+    """BASELINE configs 3 (banded int8 convolution) and 4 (2-D partial DCT), single GPU."""
     import torch
 
-    from paper_2105_10439_b200 import _lib, run_cofem
+    from paper_2105_10439_b200 import run_cofem
     from paper_2105_10439_b200 import simulate as S
 
     world, rank, local = dist_env()
     if world > 1:
-        raise SystemExit("conv configs run on one GPU this round (time-sharded halo exchange not built)")
-    c = S.CONV_CONFIGS[args.config]
-    prob, z = S.conv_problem(c)
-    h = prob.op.gpu_taps()
-    ctx = _lib.Context.convolution(c.D, h, _lib.OZAKI, 0)
+        raise SystemExit("structured dictionaries run on one GPU this round (no sharded halo exchange yet)")
+    is_conv = args.config in S.CONV_CONFIGS
+    c = S.CONV_CONFIGS[args.config] if is_conv else S.DCT_CONFIGS[args.config]
+    prob, z = S.conv_problem(c) if is_conv else S.dct2_problem(c)
+    ctx = prob.op.context("ozaki")
     dseed = 0xC0FE
     ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
     if args.warmup:
@@ -356,7 +357,10 @@ def run_ours_conv(args):
     value = args.steps / (total_ms / 1e3)
     pcg_steps = tim["pcg_steps"]
     qw = 32 if c.K + 1 > 24 else 24
-    alg_bytes = 4.0 * qw * c.D + 8.0 * qw * c.D  # operand digit planes in, fp64 result out
+    if is_conv:
+        alg_bytes = 4.0 * qw * c.D + 8.0 * qw * c.D  # operand digit planes in, fp64 result out
+    else:  # one DCT stage: fp64 stage buffer in (quantiser) + planes + fp64 stage buffer out
+        alg_bytes = 4.0 * qw * c.D + 8.0 * qw * c.D
     fwd_avg = tim["fwd_ms"] / max(tim["fwd_launches"], 1)
     bwd_avg = tim["bwd_ms"] / max(tim["bwd_launches"], 1)
     dom, avg_ms = ("bwd (Phi^T U band)", bwd_avg) if tim["bwd_ms"] >= tim["fwd_ms"] else ("fwd (Phi P band)", fwd_avg)
@@ -366,9 +370,12 @@ def run_ours_conv(args):
         "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "i8 x i8 -> exact i32 (ozaki) / f64",
-        "data": "synthetic (Bernoulli(0.01) x Exp(1) spikes, exp(-t/20) filter, sigma=0.05)",
-        "config": {"workload": f"{args.config}: causal convolution N=D={c.D}, {c.ntaps} taps, K={c.K}, "
-                               f"PCG cap {c.U} tol {c.tol}", "D": c.D, "K": c.K, "taps": c.ntaps},
+        "data": ("synthetic (Bernoulli(0.01) x Exp(1) spikes, exp(-t/20) filter, sigma=0.05)" if is_conv else
+                 "synthetic (3% N(0,1) pixels, variable-density 25% DCT mask, sigma=0.01)"),
+        "config": {"workload": (f"{args.config}: causal convolution N=D={c.D}, {c.ntaps} taps, K={c.K}, "
+                                f"PCG cap {c.U} tol {c.tol}" if is_conv else
+                                f"{args.config}: 2-D partial DCT n={c.n} (D={c.D}, N={prob.op.n_rows}), K={c.K}, "
+                                f"PCG cap {c.U} tol {c.tol}"), "D": c.D, "K": c.K},
         "pcg_steps_per_sec": pcg_steps / (total_ms / 1e3), "pcg_steps_per_em_iteration": pcg_steps / args.steps,
         "gpu_launches": int(tim["kernel_launches"]), "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -376,7 +383,7 @@ def run_ours_conv(args):
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
                      "contraction_share_of_step": (tim["fwd_ms"] + tim["bwd_ms"]) / tim["total_ms"]},
     }
-    ctx.close()
+    prob.op.release()
     if not args.no_e2e:
         cfg = c.cofem_config("ozaki", iterations=args.steps)
         t0 = time.perf_counter()
@@ -387,16 +394,16 @@ def run_ours_conv(args):
                        "d2h_bytes_per_step": 24.0 * c.D / args.steps, "seconds": el,
                        "pcg_steps": int(sum(d["cg_steps"] for d in diag))}
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_sample_conv(c, prob, args.cpu_seconds, pcg_steps / args.steps)
+        line["cpu_baseline"] = cpu_sample_conv(c, prob, args.cpu_seconds, pcg_steps / args.steps, is_conv)
     print(json.dumps(line), flush=True)
 
 
-def cpu_sample_conv(c, prob, seconds, steps_per_em):
-    """The reference algorithm (oracle: FFT convolution like operators.py:209-219,
-    float64, numpy/scipy threads) on the full-size convolution system."""
+def cpu_sample_conv(c, prob, seconds, steps_per_em, is_conv=True):
+    """The reference algorithm (oracle: FFT convolution like operators.py:209-219
+    or scipy.fft dctn, float64, numpy/scipy threads) on the full-size system."""
     from oracle import cofem_oracle as O
 
-    op = O.conv_op(c.D, c.taps())
+    op = O.conv_op(c.D, c.taps()) if is_conv else O.dct2_op(c.n, prob.op.mask)
     probes = O.draw_rademacher(c.D, c.K, O.substream(c.seed, 3))
     rhs = np.concatenate([probes, op.adjoint(np.asarray(prob.y)[:, None])], axis=1)
     alpha = np.ones(c.D)
@@ -408,8 +415,8 @@ def cpu_sample_conv(c, prob, seconds, steps_per_em):
         steps += 1
     per = (time.perf_counter() - t0) / steps
     return {"value": 1.0 / (per * steps_per_em), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{steps} PCG steps of the full D={c.D}, Q={c.K + 1} convolution system with the bit-exact "
-                      f"numpy oracle (scipy.fft rfft/irfft like the reference); {per * 1e3:.0f} ms/PCG step x "
+            "sample": f"{steps} PCG steps of the full D={c.D}, Q={c.K + 1} {'convolution' if is_conv else 'DCT'} "
+                      f"system with the numpy oracle (scipy.fft like the reference); {per * 1e3:.0f} ms/PCG step x "
                       f"{steps_per_em:.1f} PCG steps per EM iteration"}
 
 

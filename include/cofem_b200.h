@@ -106,6 +106,13 @@ int cofem_destroy(cofem_ctx* ctx);
 int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const double* taps, int64_t ntaps,
                              int precision);
 
+/* 2-D partial DCT dictionary (BASELINE config 4; the 2-D analogue of
+ * operators.SubsampledDctOperator, operators.py:132-179): z is an n x n image
+ * (row-major, D = n^2), Phi z = the coefficients `mask` (flat k n + l) of its
+ * orthonormal 2-D DCT-II.  Applied as four int8 tensor-core stages against
+ * the n x n DCT matrix; requires COFEM_OZAKI and n a multiple of 128. */
+int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision);
+
 /* Upload Phi (N x D_local float32, row stride `ld` elements) from host
  * memory (or adopt a device pointer when `on_device` != 0; the caller keeps
  * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */

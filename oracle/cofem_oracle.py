@@ -101,6 +101,34 @@ def dct_op(dim, mask):
               lambda: idct(np.eye(dim), axis=0, norm="ortho")[mask, :], "dct")
 
 
+def dct2_op(n, mask):
+    """BASELINE config 4 (the 2-D analogue of operators.py:132-179): rows `mask`
+    of the orthonormal 2-D DCT-II of n x n images flattened row-major."""
+    from scipy.fft import dctn, idctn
+
+    mask = np.sort(np.asarray(mask, dtype=np.int64))
+    D = n * n
+
+    def fwd(V):
+        Y = dctn(V.reshape(n, n, V.shape[1]), axes=(0, 1), norm="ortho")
+        return Y.reshape(D, V.shape[1])[mask]
+
+    def adj(U):
+        full = np.zeros((D, U.shape[1]))
+        full[mask] = U
+        return idctn(full.reshape(n, n, U.shape[1]), axes=(0, 1), norm="ortho").reshape(D, U.shape[1])
+
+    def norms():
+        k = np.arange(n)[:, None]
+        i = np.arange(n)[None, :]
+        c = np.cos(np.pi * (2 * i + 1) * k / (2.0 * n)) * np.where(k == 0, np.sqrt(1.0 / n), np.sqrt(2.0 / n))
+        g = np.zeros(D)
+        g[mask] = 1.0
+        return ((c * c).T @ g.reshape(n, n) @ (c * c)).ravel()
+
+    return Op(mask.size, D, fwd, adj, norms, lambda: fwd(np.eye(D)), "dct2")
+
+
 def conv_op(dim, taps):
     """operators.py:182-225 -- causal lower-triangular Toeplitz convolution.
 

@@ -37,6 +37,7 @@ EXPORTED = (
     "cofem_create",
     "cofem_destroy",
     "cofem_create_convolution",
+    "cofem_create_dct2",
     "cofem_set_dictionary",
     "cofem_set_shard",
     "cofem_generate_gaussian_dictionary",
@@ -125,6 +126,7 @@ def load():
         "cofem_create": (c_int, [POINTER(vp), c_int, c_int64, c_int64, c_int]),
         "cofem_destroy": (c_int, [vp]),
         "cofem_create_convolution": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_double), c_int64, c_int]),
+        "cofem_create_dct2": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_int64), c_int64, c_int]),
         "cofem_set_dictionary": (c_int, [vp, vp, c_int64, c_int]),
         "cofem_set_shard": (c_int, [vp, c_int64, c_int64]),
         "cofem_generate_gaussian_dictionary": (c_int, [vp, c_uint64, c_double]),
@@ -186,6 +188,15 @@ class Context:
         self.n_rows = int(n_rows)
         self.n_cols = int(n_cols)
         self.precision = precision
+
+    @classmethod
+    def dct2(cls, n, mask, precision=OZAKI, device=0):
+        """Partial 2-D DCT dictionary of n x n images (rows `mask` of the coefficient grid)."""
+        mask = np.ascontiguousarray(mask, dtype=np.int64)
+        handle = c_void_p()
+        check(load().cofem_create_dct2(ctypes.byref(handle), int(device), int(n), mask.ctypes.data_as(POINTER(c_int64)),
+                                       mask.size, int(precision)))
+        return cls(mask.size, n * n, precision, device, _handle=handle)
 
     @classmethod
     def convolution(cls, dim, taps, precision=OZAKI, device=0):

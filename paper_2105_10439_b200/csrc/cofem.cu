@@ -21,6 +21,7 @@
 
 #include "kernels.cuh"
 #include "nccl.h"
+#include "dct.cuh"
 #include "ozaki.cuh"
 #include "pcg.cuh"
 
@@ -181,6 +182,17 @@ struct cofem_ctx {
   double* hrows = nullptr;                           // Dp copies of the band's power-of-two scale
   CUtensorMap map_band_fwd{}, map_band_adj{};
 
+  // 2-D partial DCT (kind 2): n x n images, D = n^2, N = mask size
+  int dct_n = 0;
+  int64_t* dct_mask = nullptr;      // N flat coefficient indices k n + l
+  uint8_t* dct_grid = nullptr;      // n x n 0/1 mask grid
+  double *bufA = nullptr, *bufB = nullptr;  // n x n ldq stage buffers
+  int8_t* wq = nullptr;             // operand digit planes [4][n ldq][n]
+  double* wscale = nullptr;         // n ldq column scales
+  unsigned long long* wcolmax = nullptr;
+  CUtensorMap map_w{};
+  int map_w_ldq = 0;
+
   // multi-GPU
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -324,6 +336,22 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMemset(c->R, 0, dbytes));
   CK(cudaMemset(c->P, 0, dbytes));
   CK(cudaMemset(c->Psi, 0, dbytes));
+  if (c->kind == 2) {
+    const int64_t n = c->dct_n, nc = n * ldq;
+    for (double** b : {&c->bufA, &c->bufB}) {
+      if (*b) cudaFree(*b);
+      CK(cudaMalloc(b, (size_t)n * nc * sizeof(double)));
+      CK(cudaMemset(*b, 0, (size_t)n * nc * sizeof(double)));
+    }
+    if (c->wq) cudaFree(c->wq);
+    if (c->wscale) cudaFree(c->wscale);
+    if (c->wcolmax) cudaFree(c->wcolmax);
+    CK(cudaMalloc(&c->wq, (size_t)4 * nc * n));
+    CK(cudaMalloc(&c->wscale, nc * sizeof(double)));
+    CK(cudaMalloc(&c->wcolmax, nc * sizeof(unsigned long long)));
+    CKR(encode_u8_3d(&c->map_w, c->wq, n, nc, 4, oz::KT, 32, 4));
+    c->map_w_ldq = ldq;
+  }
   c->ldq = ldq;
   return 0;
 }
@@ -437,7 +465,7 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
   }
   oz::contract_kernel<QW, BWD ? oz::MODE_BWD : oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
       map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
-      n_rows_out, nullptr, st);
+      n_rows_out, nullptr, st, sp.nsplit, QW);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -574,6 +602,80 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   return 0;
 }
 
+// ---- 2-D partial DCT: four ozaki stages against the n x n DCT matrix --------
+// one stage: quantise the stacked operand columns (h, q) of src (element
+// (t, h ldq + q) at src[t st + h sh + q]) and contract with C (bwd: C^T)
+int dct_stage(cofem_ctx* c, const double* src, int64_t st, int64_t sh, const double* pre, bool bwd,
+              const double* row_scale, double* out, const Status* stt) {
+  CKR(oz_init_kernels<32>());
+  const int n = c->dct_n, ldq = c->ldq, nc = n * ldq;
+  dct::k_cq_quantize<<<nc / dct::TC, 256, 0, c->stream>>>(n, nc, ldq, st, sh, src, pre, c->wscale, c->wq, stt);
+  const int nmb = n / oz::BM, items = nmb * (nc / 32);
+  const int grid = std::min(items, c->sm_count);
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  if (!bwd)
+    oz::contract_kernel<32, oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<32>::SMEM, c->stream>>>(
+        c->map_phi_fwd, c->map_w, nmb, items, n, n, 0, row_scale, c->wscale, out, n, n, nullptr, stt, 1, nc);
+  else
+    oz::contract_kernel<32, oz::MODE_BWD><<<grid, oz::NTHREADS, oz::Cfg<32>::SMEM, c->stream>>>(
+        c->map_phi_bwd, c->map_w, nmb, items, n, n, 0, row_scale, c->wscale, out, n, n, nullptr, stt, 1, nc);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({bwd ? 1 : 0, c->evnext - 2});
+  }
+  c->launches += 2;
+  if (bwd) c->bwd_launches++;
+  else c->fwd_launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// bufB <- Y^T = (C X C^T)^T for every column image of P (pixel-major D x ldq)
+int dct_forward_dev(cofem_ctx* c, const double* P, const Status* stt) {
+  const int64_t n = c->dct_n, ldq = c->ldq;
+  CKR(dct_stage(c, P, n * ldq, ldq, c->colscale, false, c->rowscale, c->bufA, stt));       // W = C X
+  return dct_stage(c, c->bufA, ldq, n * ldq, c->colscale, false, c->rowscale, c->bufB, stt);  // Y^T = C W^T
+}
+
+// bufB (U^T, masked coefficients) <- Z^T = (C^T U C)^T
+int dct_adjoint_dev(cofem_ctx* c, const Status* stt) {
+  const int64_t n = c->dct_n, ldq = c->ldq;
+  CKR(dct_stage(c, c->bufB, ldq, n * ldq, c->rowscale, true, c->colscale, c->bufA, stt));  // T = C^T U
+  return dct_stage(c, c->bufA, ldq, n * ldq, c->rowscale, true, c->colscale, c->bufB, stt);  // Z^T = C^T T^T
+}
+
+int dct_finish(cofem_ctx* c, double* out, const Status* stt) {
+  const int ldq = c->ldq;
+  dct::k_finish<<<8 * c->sm_count, 256, dct::FJ * dct::FI * ldq * sizeof(double), c->stream>>>(c->dct_n, ldq, c->bufB,
+                                                                                             out, stt);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Psi = beta Phi^T Phi P + alpha .* P for all ldq columns at once, pi on the fly
+int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
+  CKR(dct_forward_dev(c, (const double*)c->P, stt));
+  const int64_t total = (int64_t)c->dct_n * c->dct_n * c->ldq;
+  dct::k_apply_mask<<<(int)std::min<int64_t>((total + 255) / 256, 16 * c->sm_count), 256, 0, c->stream>>>(
+      c->dct_n, c->ldq, c->bufB, c->dct_grid, stt);
+  c->launches++;
+  CKR(dct_adjoint_dev(c, stt));
+  CKR(dct_finish(c, (double*)c->ppart, stt));
+  Scalars sc = c->sc();
+  const int bs = elem_block(c->ldq);
+  k_combine<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->ppart, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
+      stt);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // ---- the two contractions ----------------------------------------------
 // fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
 template <typename T, int QP>
@@ -678,6 +780,9 @@ inline int chunk_width(int ldq, int qoff) { return std::min(QCHUNK, ldq - qoff);
 // Psi = beta Phi^T Phi P + alpha .* P for all ldq columns, pi on the fly
 template <typename T>
 int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (c->kind == 2) return dct_system_apply(c, beta, st);
+  }
   Scalars sc = c->sc();
   for (int qoff = 0; qoff < c->ldq; qoff += QCHUNK) {
     const int qpc = chunk_width(c->ldq, qoff);
@@ -738,11 +843,11 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   // ozaki: k_direction also emits the column maxima of diag(c) P for the next
   // Phi P quantisation (k_update re-zeroes them every step)
   const bool oz = c->prec == COFEM_OZAKI;
-  if (oz) {
+  if (oz && c->kind != 2) {
     if (c->kind == 0) CKR(ensure_oz(c));
     CK(cudaMemsetAsync(c->colmax, 0, ldq * sizeof(unsigned long long), c->stream));
   }
-  unsigned long long* pmax = oz ? c->colmax : nullptr;
+  unsigned long long* pmax = (oz && c->kind != 2) ? c->colmax : nullptr;
   k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
       c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
       ngroups, groups, sc, c->colscale, pmax, c->st);
@@ -822,11 +927,29 @@ int check_ctx(cofem_ctx* c, bool need_phi = true) {
 int ldq_for(int64_t q) { return (int)round_up(std::max<int64_t>(q, 1), 8); }
 
 // ---- apply / adjoint / system apply ---------------------------------------
+// DCT: tmpD (D x ldq) <- Phi^T V for V (N x ldq) already in c->V
+int dct_adjoint_from_V(cofem_ctx* c) {
+  const int64_t n = c->dct_n, ldq = c->ldq;
+  CK(cudaMemsetAsync(c->bufB, 0, (size_t)n * n * ldq * sizeof(double), c->stream));
+  dct::k_scatter<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, (int)n, (int)ldq, c->dct_mask, (const double*)c->V,
+                                                         c->bufB);
+  c->launches++;
+  CKR(dct_adjoint_dev(c, nullptr));
+  return dct_finish(c, (double*)c->tmpD, nullptr);
+}
+
 template <typename T>
 int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
   const int ldq = ldq_for(q);
   CKR(ensure_ws(c, ldq));
   CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
+  if (c->kind == 2) {
+    CKR(dct_forward_dev(c, (const double*)c->P, nullptr));
+    dct::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, c->dct_n, ldq, c->dct_mask, c->bufB, (double*)c->V);
+    c->launches++;
+    CK(cudaGetLastError());
+    return download_block<T>(c, c->V, c->N, q, ldq, 0, out);
+  }
   std::vector<double> chunk;
   for (int qoff = 0; qoff < ldq; qoff += QCHUNK) {
     const int qpc = chunk_width(ldq, qoff);
@@ -846,6 +969,11 @@ template <typename T>
 int adjoint_impl(cofem_ctx* c, const double* U, int64_t q, double* out) {
   const int ldq = ldq_for(q);
   CKR(ensure_ws(c, ldq));
+  if (c->kind == 2) {
+    CKR(upload_block<T>(c, U, c->N, q, c->Np, ldq, c->V));
+    CKR(dct_adjoint_from_V(c));
+    return download_block<T>(c, c->tmpD, c->D, q, ldq, 0, out);
+  }
   std::vector<double> chunk;
   for (int qoff = 0; qoff < ldq; qoff += QCHUNK) {
     const int qpc = chunk_width(ldq, qoff);
@@ -891,6 +1019,19 @@ template <typename T>
 int compute_aty(cofem_ctx* c, const double* y_host) {
   // V[:, 0] = y, other columns 0 -> Phi^T V via the bwd contraction (8-wide)
   CKR(ensure_ws(c, std::max(c->ldq, 8)));
+  if (c->kind == 2) {
+    std::vector<double> vb((size_t)c->Np * c->ldq, 0.0);
+    for (int64_t i = 0; i < c->N; ++i) vb[i * c->ldq] = y_host[i];
+    CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CKR(dct_adjoint_from_V(c));
+    std::vector<double> out((size_t)c->Dp * c->ldq);
+    CK(cudaMemcpyAsync(out.data(), c->tmpD, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<double> aty(c->Dp, 0.0);
+    for (int64_t j = 0; j < c->D; ++j) aty[j] = out[j * c->ldq];
+    CK(cudaMemcpy(c->aty, aty.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+    return 0;
+  }
   std::vector<T> vb((size_t)c->Np * 8, T(0));
   for (int64_t i = 0; i < c->N; ++i) vb[i * 8] = (T)y_host[i];
   CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
@@ -930,6 +1071,7 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   std::vector<double> a(c->Dp, 1.0);
   CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
   if (em->theta_policy == COFEM_THETA_JACOBI) {
+    if (c->kind == 2) return fail(COFEM_EINVAL, "jacobi on a DCT dictionary: pass its column norms as custom theta");
     if (c->kind == 0) {
       k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
       c->launches++;
@@ -1179,6 +1321,97 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   return 0;
 }
 
+int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision) {
+  if (!out || !mask) return fail(COFEM_EINVAL, "null argument");
+  *out = nullptr;
+  if (n < 128 || n % 128 != 0 || n > 8192) return fail(COFEM_EINVAL, "image side must be a multiple of 128 in [128, 8192]");
+  if (nmask < 1 || nmask > n * n) return fail(COFEM_EINVAL, "need 1 <= mask size <= n^2");
+  if (precision != COFEM_OZAKI) return fail(COFEM_EINVAL, "2-D DCT dictionaries run in OZAKI precision");
+  std::vector<uint8_t> grid((size_t)n * n, 0);
+  for (int64_t m = 0; m < nmask; ++m) {
+    if (mask[m] < 0 || mask[m] >= n * n) return fail(COFEM_EINVAL, "mask indices must lie in [0, n^2)");
+    if (grid[mask[m]]) return fail(COFEM_EINVAL, "mask indices must be distinct");
+    grid[mask[m]] = 1;
+  }
+  cofem_ctx* c = new cofem_ctx();
+  c->kind = 2;
+  c->device = device;
+  c->prec = precision;
+  c->dct_n = (int)n;
+  c->N = nmask;
+  c->D = n * n;
+  c->Np = round_up(nmask, PAD);
+  c->Dp = round_up(c->D, PAD);
+  c->global_cols = c->D;
+  auto bail = [&](int rc) {
+    cofem_destroy(c);
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(COFEM_ECUDA, "stream create failed"));
+  double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty};
+  for (double** p : dvecs) {
+    if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
+    cudaMemset(*p, 0, c->Dp * sizeof(double));
+  }
+  if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
+  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "pinned status"));
+  for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  if (cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "colmax"));
+  // the n x n orthonormal DCT-II matrix C[k][i] = c_k cos(pi (2 i + 1) k / (2 n)) as digit planes
+  std::vector<double> C((size_t)n * n), rs(n), cs(n);
+  for (int64_t k = 0; k < n; ++k) {
+    const double ck = k == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n);
+    for (int64_t i = 0; i < n; ++i) C[k * n + i] = ck * std::cos(M_PI * (2.0 * i + 1.0) * k / (2.0 * n));
+  }
+  for (int64_t k = 0; k < n; ++k) {
+    double m = 0.0;
+    for (int64_t i = 0; i < n; ++i) m = std::max(m, std::fabs(C[k * n + i]));
+    rs[k] = host_pow2_ceil(m);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double m = 0.0;
+    for (int64_t k = 0; k < n; ++k) m = std::max(m, std::fabs(C[k * n + i]) / rs[k]);
+    cs[i] = host_pow2_ceil(m);
+  }
+  std::vector<int8_t> planes((size_t)4 * n * n);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = 0; i < n; ++i) {
+      int8_t d[4];
+      host_digits4(C[k * n + i] / (rs[k] * cs[i]) * 1073741824.0, d);
+      for (int a = 0; a < 4; ++a) planes[((size_t)a * n + k) * n + i] = d[a];
+    }
+  if (cudaMalloc(&c->phiq, planes.size()) != cudaSuccess || cudaMalloc(&c->rowscale, n * sizeof(double)) ||
+      cudaMalloc(&c->colscale, n * sizeof(double)) || cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) ||
+      cudaMalloc(&c->dct_grid, grid.size()))
+    return bail(fail(COFEM_ENOMEM, "DCT planes"));
+  cudaMemcpy(c->phiq, planes.data(), planes.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->rowscale, rs.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->colscale, cs.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  std::vector<int64_t> sorted(mask, mask + nmask);
+  std::sort(sorted.begin(), sorted.end());
+  cudaMemcpy(c->dct_mask, sorted.data(), nmask * sizeof(int64_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->dct_grid, grid.data(), grid.size(), cudaMemcpyHostToDevice);
+  int rc = encode_u8_3d(&c->map_phi_fwd, c->phiq, n, n, 4, oz::KT, oz::BM, 4);
+  if (!rc) rc = encode_u8_3d(&c->map_phi_bwd, c->phiq, n, n, 4, 64, oz::KT, 4);
+  if (rc) return bail(rc);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+  c->have_phi = true;
+  c->oz_ready = true;
+  *out = c;
+  return 0;
+}
+
 int cofem_destroy(cofem_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
@@ -1186,7 +1419,8 @@ int cofem_destroy(cofem_ctx* c) {
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
-                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows};
+                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
+                  c->dct_mask, c->dct_grid, c->bufA, c->bufB, c->wq, c->wscale, c->wcolmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -1255,7 +1489,7 @@ int cofem_nccl_get_unique_id(void* out128) {
 
 int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
   CKR(check_ctx(c, false));
-  if (c->kind != 0 && nranks > 1) return fail(COFEM_EINVAL, "time-sharded convolution is not implemented yet");
+  if (c->kind != 0 && nranks > 1) return fail(COFEM_EINVAL, "sharding is implemented for dense dictionaries only");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
   CKR(nccl_load());
   ncclUniqueId id;
@@ -1294,6 +1528,7 @@ int cofem_column_sq_norms(cofem_ctx* c, double* out) {
     CK(cudaMemcpy(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost));
     return 0;
   }
+  if (c->kind == 2) return fail(COFEM_EINVAL, "DCT column norms are computed by the host (pass a custom theta)");
   k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
   c->launches++;
   CK(cudaGetLastError());

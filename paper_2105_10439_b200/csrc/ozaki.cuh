@@ -223,6 +223,9 @@ __device__ __forceinline__ void warp_fold_max(unsigned long long (&cm)[QW], unsi
 //     [0, K) arrive as TMA zero fill.
 // Rows >= rows_real are written as zeros; out_colmax (may be null) collects
 // the column maxima of |out| for the next quantisation (single-split modes).
+// Wide operands (n_items > n_mblocks * n_split): item w also selects column
+// chunk nc = w / (n_mblocks * n_split) of an operand with out_ld columns
+// (B TMA row coordinate nc * QW, op_scale / out offset nc * QW).
 enum { MODE_FWD = 0, MODE_BWD = 1, MODE_BAND = 2 };
 template <int QW, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
@@ -230,7 +233,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     int n_mblocks, int n_items, int k_per_split, int k_total, int band_offset,
                     const double* __restrict__ row_scale, const double* __restrict__ op_scale,
                     double* __restrict__ out, int64_t out_rows, int64_t rows_real,
-                    unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st) {
+                    unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st, int n_split = 1,
+                    int out_ld = QW) {
   constexpr bool BWD = MODE == MODE_BWD;
   using C = Cfg<QW>;
   if (st && st->done) return;
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-        const int mb = w % n_mblocks, s = w / n_mblocks;
+        const int mb = w % n_mblocks, s = (w / n_mblocks) % n_split, nc = w / (n_mblocks * n_split);
         const int k0 = MODE == MODE_BAND ? mb * BM + band_offset : s * k_per_split;
         const int k1 = MODE == MODE_BAND ? k0 + k_per_split : min(k0 + k_per_split, k_total);
         for (int k = k0; k < k1; k += KT) {
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_3d(sa, &map_a, &full[stage], mb * BM, k, 0);
             tma_load_3d(sa + A_STAGE / 2, &map_a, &full[stage], mb * BM + 64, k, 0);
           }
-          tma_load_3d(sb, &map_b, &full[stage], k, 0, 0);
+          tma_load_3d(sb, &map_b, &full[stage], k, nc * QW, 0);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-        const int mb = w % n_mblocks, s = w / n_mblocks;
+        const int mb = w % n_mblocks, s = (w / n_mblocks) % n_split;
         const int k0 = MODE == MODE_BAND ? mb * BM + band_offset : s * k_per_split;
         const int k1 = MODE == MODE_BAND ? k0 + k_per_split : min(k0 + k_per_split, k_total);
         const int buf = it & 1;
@@ -343,18 +347,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int q = 0; q < QW; ++q) cm[q] = 0ull;
     int it = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
-      const int mb = w % n_mblocks, s = w / n_mblocks;
+      const int mb = w % n_mblocks, s = (w / n_mblocks) % n_split, nc = w / (n_mblocks * n_split);
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int64_t row = (int64_t)mb * BM + row_in_tile;
       const double scale = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
+      double* orow = out + ((int64_t)s * out_rows + row) * out_ld + nc * QW;
       if (out_colmax)
-        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
-                               out + ((int64_t)s * out_rows + row) * QW, cm);
+        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale,
+                               op_scale + nc * QW, orow, cm);
       else
-        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
-                                out + ((int64_t)s * out_rows + row) * QW, cm);
+        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale,
+                                op_scale + nc * QW, orow, cm);
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[buf]);

@@ -200,6 +200,91 @@ class ConvolutionOperator(LinearOperator):
         return c[np.minimum(self.filter.size, self.n_cols - np.arange(self.n_cols))]
 
 
+class PartialDct2Operator(LinearOperator):
+    """Row subset of the orthonormal 2-D DCT-II of n x n images (BASELINE config 4;
+    the 2-D analogue of the reference's SubsampledDctOperator, operators.py:132-179).
+
+    z is an n x n image flattened row-major (D = n^2); Phi z = the coefficients
+    at the flat indices ``mask`` (k n + l, sorted, distinct) of
+    ``scipy.fft.dctn(z, norm="ortho")``.  Rows are orthonormal (Phi Phi^T = I).
+    On the GPU one apply is four int8 tensor-core stages against the n x n DCT
+    matrix (precision "ozaki"; n a multiple of 128).
+    """
+
+    kind = "partial-dct2"
+
+    def __init__(self, n, mask, device=0):
+        mask = np.asarray(mask, dtype=np.int64)
+        if mask.ndim != 1 or mask.size < 1:
+            raise ValueError("mask must be a nonempty 1-D index array")
+        if np.unique(mask).size != mask.size:
+            raise ValueError("mask indices must be distinct")
+        if mask.min() < 0 or mask.max() >= n * n:
+            raise ValueError(f"mask indices must lie in [0, {n * n})")
+        super().__init__(mask.size, n * n)
+        mask = np.sort(mask)
+        mask.flags.writeable = False
+        self.n = int(n)
+        self.mask = mask
+        self.device = device
+        self._ctx = {}
+
+    def context(self, precision="ozaki"):
+        if precision != "ozaki":
+            raise NotImplementedError("2-D DCT dictionaries run in the 'ozaki' precision mode")
+        ctx = self._ctx.get(precision)
+        if ctx is None:
+            ctx = _lib.Context.dct2(self.n, self.mask, _lib.OZAKI, self.device)
+            self._ctx[precision] = ctx
+        return ctx
+
+    def release(self):
+        for ctx in self._ctx.values():
+            ctx.close()
+        self._ctx.clear()
+
+    def _apply(self, V):
+        return self.context().apply(V)
+
+    def _apply_adjoint(self, U):
+        return self.context().apply_adjoint(U)
+
+    def dct_matrix(self):
+        n = self.n
+        k = np.arange(n)[:, None]
+        i = np.arange(n)[None, :]
+        c = np.cos(np.pi * (2 * i + 1) * k / (2.0 * n))
+        c *= np.where(k == 0, np.sqrt(1.0 / n), np.sqrt(2.0 / n))
+        return c
+
+    def column_sq_norms(self):
+        """||Phi e_ij||^2 = sum_{(k,l) in mask} C_ki^2 C_lj^2 = ((C.C)^T M (C.C))_ij."""
+        c2 = self.dct_matrix() ** 2
+        grid = np.zeros(self.n * self.n)
+        grid[self.mask] = 1.0
+        return (c2.T @ grid.reshape(self.n, self.n) @ c2).ravel()
+
+
+def variable_density_mask(n, keep_frac, rng, r0=None):
+    """MRI-style mask: keep probability ~ 1/(1 + r/r0)^2 (r = radius from the DC
+    coefficient, r0 = 64 at n = 1024), normalised so the expected kept fraction
+    is keep_frac; one Bernoulli draw per coefficient."""
+    r0 = 64.0 * n / 1024.0 if r0 is None else r0
+    k = np.arange(n)
+    r = np.sqrt(k[:, None] ** 2 + k[None, :] ** 2)
+    w = 1.0 / (1.0 + r / r0) ** 2
+    target = keep_frac * n * n
+    lo, hi = 0.0, 1.0 / w.min()
+    for _ in range(100):  # bisection for c: sum min(1, c w) = target
+        mid = 0.5 * (lo + hi)
+        if np.minimum(1.0, mid * w).sum() < target:
+            lo = mid
+        else:
+            hi = mid
+    p = np.minimum(1.0, hi * w)
+    return np.flatnonzero(rng.random(n * n) < p.ravel())
+
+
 def build_exp_convolution(dim, decay):
     """Lower-triangular convolution with filter (1-rho)^m, m = 0..D-1 (operators.py:243-245)."""
     return ConvolutionOperator(dim, decay)
@@ -241,6 +326,6 @@ class SystemMatrix:
         """A @ V on the GPU without materialising A."""
         V, single = _as_columns(V, self.dim, "system apply")
         if precision is None:
-            precision = "ozaki" if isinstance(self.op, ConvolutionOperator) else "fp64"
+            precision = "ozaki" if isinstance(self.op, (ConvolutionOperator, PartialDct2Operator)) else "fp64"
         out = self.op.context(precision).system_apply(self.beta, self.alpha, V)
         return out[:, 0] if single else out

@@ -116,6 +116,56 @@ def conv_problem(cfg: ConvConfig):
     return SblProblem(y, ConvolutionOperator.from_taps(cfg.D, h), cfg.beta), z
 
 
+@dataclass(frozen=True)
+class Dct2Config:
+    """BASELINE config 4: MRI-style undersampled 2-D DCT (synthetic)."""
+
+    name: str
+    n: int           # image side, D = n^2
+    keep: float      # fraction of DCT coefficients kept (variable density)
+    frac: float      # fraction of nonzero pixels, N(0,1) values
+    sigma: float
+    K: int
+    T: int
+    U: int
+    tol: float
+    seed: int = 0
+
+    @property
+    def D(self):
+        return self.n * self.n
+
+    @property
+    def beta(self):
+        return 1.0 / self.sigma**2
+
+    def cofem_config(self, precision="ozaki", **over):
+        cg = CgConfig(max_steps=self.U, tolerance=self.tol, precision=precision)
+        kw = dict(iterations=self.T, probes=self.K, cg=cg, seed=self.seed)
+        kw.update(over)
+        return CofemConfig(**kw)
+
+
+DCT_CONFIGS = {
+    "dct-large": Dct2Config("dct-large", 1024, 0.25, 0.03, 0.01, 20, 20, 200, 1e-5),
+    "dct-small": Dct2Config("dct-small", 128, 0.25, 0.03, 0.01, 20, 3, 200, 1e-5),
+}
+
+
+def dct2_problem(cfg: Dct2Config):
+    """(SblProblem, z_true): mask from substream(seed, 0), pixels from
+    substream(seed, 1), noise from substream(seed, 2); y in float64."""
+    from scipy.fft import dctn
+
+    from .operators import PartialDct2Operator, variable_density_mask
+
+    mask = variable_density_mask(cfg.n, cfg.keep, substream(cfg.seed, 0))
+    z = sparse_signal(cfg.D, int(round(cfg.frac * cfg.D)), cfg.seed)
+    y = dctn(z.reshape(cfg.n, cfg.n), norm="ortho").ravel()[mask]
+    y = y + cfg.sigma * substream(cfg.seed, 2).standard_normal(mask.size)
+    return SblProblem(y, PartialDct2Operator(cfg.n, mask), cfg.beta), z
+
+
 def gaussian_dictionary(N, D, seed):
     """N x D float32, entries N(0, 1/N), from substream(seed, 0)."""
     rng = substream(seed, 0)

@@ -354,3 +354,35 @@ def test_run_cofem_convolution_parity():
     np.testing.assert_array_equal(st.alpha < PRUNE, g["alpha"] < PRUNE)
     nref, nour = S.nmse(g["mu"], g["z"]), S.nmse(est.mu, g["z"])
     assert abs(nour - nref) <= 0.01 * nref
+
+
+# ------------------------------------------------------- 2-D partial DCT ----
+@pytest.mark.parametrize("n,q", [(128, 21), (256, 5)])
+def test_dct2_apply_matches_oracle(n, q):
+    from paper_2105_10439_b200 import PartialDct2Operator, variable_density_mask, substream
+
+    rng = np.random.default_rng(n + q)
+    mask = variable_density_mask(n, 0.25, substream(1, 0))
+    op = PartialDct2Operator(n, mask)
+    oop = O.dct2_op(n, mask)
+    V = rng.standard_normal((n * n, q))
+    U = rng.standard_normal((mask.size, q))
+    assert rel(op.apply(V), oop.apply(V)) <= 5e-9
+    assert rel(op.apply_adjoint(U), oop.adjoint(U)) <= 5e-9
+    alpha = rng.random(n * n) + 0.5
+    want = 3.0 * oop.adjoint(oop.apply(V)) + alpha[:, None] * V
+    assert rel(SystemMatrix(op, 3.0, alpha).apply(V), want) <= 5e-9
+
+
+def test_run_cofem_dct2_parity_with_oracle():
+    """BASELINE config 4 at n = 128 (D = 16384), 3 EM iterations: against the
+    float64 oracle on identical inputs and probes."""
+    c = S.DCT_CONFIGS["dct-small"]
+    prob, z = S.dct2_problem(c)
+    cfg = c.cofem_config()
+    st, est, diag = run_cofem(prob, cfg)
+    ocfg = O.CofemConfig(iterations=c.T, probes=c.K, seed=c.seed, cg=O.CgConfig(max_steps=c.U, tolerance=c.tol))
+    alpha, mu, s, odiag = O.run_cofem(O.dct2_op(c.n, prob.op.mask), np.asarray(prob.y), c.beta, ocfg)
+    emu, ea = rel(est.mu, mu), rel(st.alpha, alpha)
+    assert emu <= 1e-4 and ea <= 1e-4, (emu, ea, [d["cg_steps"] for d in diag], [d["cg_steps"] for d in odiag])
+    np.testing.assert_array_equal(st.alpha < PRUNE, alpha < PRUNE)

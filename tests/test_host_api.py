@@ -121,3 +121,27 @@ def test_simulate_generators_are_deterministic():
     assert 0.8 / c.N <= phi1.astype(np.float64).var() <= 1.2 / c.N
     assert p1.beta == pytest.approx(1e4)
     assert S.nrmse(z1, z1) == 0.0
+
+
+def test_dct2_oracle_and_mask_generator():
+    from scipy.fft import dctn
+
+    from paper_2105_10439_b200 import PartialDct2Operator, variable_density_mask
+
+    rng = np.random.default_rng(4)
+    n = 16
+    mask = variable_density_mask(n, 0.25, substream(0, 0))
+    again = variable_density_mask(n, 0.25, substream(0, 0))
+    np.testing.assert_array_equal(mask, again)
+    assert 0.1 < mask.size / n**2 < 0.4 and 0 in mask  # DC always kept
+    op = O.dct2_op(n, mask)
+    V = rng.standard_normal((n * n, 3))
+    U = rng.standard_normal((mask.size, 3))
+    np.testing.assert_allclose(op.apply(V)[:, 1], dctn(V[:, 1].reshape(n, n), norm="ortho").ravel()[mask])
+    assert abs(np.sum(U * op.apply(V)) - np.sum(op.adjoint(U) * V)) < 1e-10
+    np.testing.assert_allclose(op.apply(op.adjoint(U)), U, atol=1e-12)  # orthonormal rows
+    m = op.materialize()
+    np.testing.assert_allclose(op.col_sq_norms(), (m * m).sum(axis=0), atol=1e-12)
+    np.testing.assert_allclose(PartialDct2Operator(n, mask).column_sq_norms(), op.col_sq_norms(), atol=1e-12)
+    with pytest.raises(ValueError, match="distinct"):
+        PartialDct2Operator(4, np.array([1, 1]))
