@@ -118,6 +118,11 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
  * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */
 int cofem_set_dictionary(cofem_ctx* ctx, const float* phi, int64_t ld, int on_device);
 
+/* Upload a float64 Phi from host memory (row stride `ld`).  The fp32/fp64
+ * modes keep its float32 rounding; in COFEM_OZAKI mode the fixed-point digit
+ * planes are built from the exact float64 values (no float32 rounding). */
+int cofem_set_dictionary_f64(cofem_ctx* ctx, const double* phi, int64_t ld);
+
 /* Declare this context's place in a column-sharded dictionary: it holds
  * global columns [col_offset, col_offset + n_cols) of `global_cols`.  Used by
  * the device generators so every shard draws the same global Phi / probes. */

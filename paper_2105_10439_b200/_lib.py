@@ -39,6 +39,7 @@ EXPORTED = (
     "cofem_create_convolution",
     "cofem_create_dct2",
     "cofem_set_dictionary",
+    "cofem_set_dictionary_f64",
     "cofem_set_shard",
     "cofem_generate_gaussian_dictionary",
     "cofem_get_dictionary",
@@ -128,6 +129,7 @@ def load():
         "cofem_create_convolution": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_double), c_int64, c_int]),
         "cofem_create_dct2": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_int64), c_int64, c_int]),
         "cofem_set_dictionary": (c_int, [vp, vp, c_int64, c_int]),
+        "cofem_set_dictionary_f64": (c_int, [vp, POINTER(c_double), c_int64]),
         "cofem_set_shard": (c_int, [vp, c_int64, c_int64]),
         "cofem_generate_gaussian_dictionary": (c_int, [vp, c_uint64, c_double]),
         "cofem_get_dictionary": (c_int, [vp, POINTER(c_float)]),
@@ -225,6 +227,12 @@ class Context:
             pass
 
     # -- dictionary
+    def set_dictionary_f64(self, phi):
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        if phi.shape != (self.n_rows, self.n_cols):
+            raise ValueError(f"dictionary shape {phi.shape} != {(self.n_rows, self.n_cols)}")
+        check(load().cofem_set_dictionary_f64(self.handle, _dp(phi), phi.shape[1]))
+
     def set_dictionary(self, phi):
         phi = np.ascontiguousarray(phi, dtype=np.float32)
         if phi.shape != (self.n_rows, self.n_cols):

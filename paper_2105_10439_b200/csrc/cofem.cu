@@ -377,8 +377,10 @@ ncclDataType_t nccl_t() {
 }
 
 // ---- Ozaki int8 tensor-core contractions -----------------------------------
-int ensure_oz(cofem_ctx* c) {
-  if (c->oz_ready) return 0;
+// digit planes + power-of-two scales of Phi; src = the dense float32 copy, or
+// a float64 original (cofem_set_dictionary_f64) when given
+int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
+  if (c->oz_ready && !src64) return 0;
   if (!c->phiq) {
     CK(cudaMalloc(&c->phiq, (size_t)4 * c->Np * c->Dp));
     CK(cudaMalloc(&c->rowscale, c->Np * sizeof(double)));
@@ -391,11 +393,19 @@ int ensure_oz(cofem_ctx* c) {
     CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
     CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
   }
-  oz::k_phi_rowscale<<<(unsigned)c->Np, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->rowscale);
-  oz::k_phi_colscale<<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->Dp, c->rowscale,
-                                                                              c->colscale);
-  oz::k_phi_planes<<<16 * c->sm_count, 256, 0, c->stream>>>(c->phi, c->Dp, c->Np, c->Dp, c->rowscale, c->colscale,
-                                                            c->phiq);
+  if (src64) {
+    oz::k_phi_rowscale<double><<<(unsigned)c->Np, 256, 0, c->stream>>>(src64, c->Dp, c->N, c->D, c->rowscale);
+    oz::k_phi_colscale<double><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(src64, c->Dp, c->N, c->Dp,
+                                                                                        c->rowscale, c->colscale);
+    oz::k_phi_planes<double><<<16 * c->sm_count, 256, 0, c->stream>>>(src64, c->Dp, c->Np, c->Dp, c->rowscale,
+                                                                      c->colscale, c->phiq);
+  } else {
+    oz::k_phi_rowscale<float><<<(unsigned)c->Np, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->rowscale);
+    oz::k_phi_colscale<float><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->Dp,
+                                                                                       c->rowscale, c->colscale);
+    oz::k_phi_planes<float><<<16 * c->sm_count, 256, 0, c->stream>>>(c->phi, c->Dp, c->Np, c->Dp, c->rowscale,
+                                                                     c->colscale, c->phiq);
+  }
   c->launches += 3;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
@@ -1445,6 +1455,37 @@ int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_devi
   c->have_phi = true;
   c->oz_ready = false;
   return 0;
+}
+
+namespace {
+__global__ void k_round_f32(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = (float)src[e];
+}
+}  // namespace
+
+int cofem_set_dictionary_f64(cofem_ctx* c, const double* phi, int64_t ld) {
+  CKR(check_ctx(c, false));
+  if (c->kind != 0) return fail(COFEM_EINVAL, "not a dense dictionary context");
+  if (!phi || ld < c->D) return fail(COFEM_EINVAL, "dictionary pointer / leading dimension");
+  double* tmp = nullptr;
+  const size_t bytes = (size_t)c->Np * c->Dp * sizeof(double);
+  CK(cudaMalloc(&tmp, bytes));
+  CK(cudaMemsetAsync(tmp, 0, bytes, c->stream));
+  int rc = 0;
+  cudaError_t e = cudaMemcpy2DAsync(tmp, c->Dp * sizeof(double), phi, ld * sizeof(double), c->D * sizeof(double),
+                                    c->N, cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) rc = fail(COFEM_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
+  if (!rc) {
+    k_round_f32<<<16 * c->sm_count, 256, 0, c->stream>>>(tmp, c->phi, (int64_t)c->Np * c->Dp);
+    c->launches++;
+    c->oz_ready = false;
+    if (c->prec == COFEM_OZAKI) rc = ensure_oz(c, tmp);  // planes from the exact float64 values
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaFree(tmp);
+  if (!rc) c->have_phi = true;
+  return rc;
 }
 
 int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {

@@ -628,7 +628,8 @@ __global__ void __launch_bounds__(256)
 
 // ---- dictionary conversion (once per dictionary) ---------------------------
 // row scales r_i = 2^ceil(log2 max_j |Phi_ij|)
-__global__ void k_phi_rowscale(const float* __restrict__ phi, int64_t ld, int64_t n_real, int64_t d_real,
+template <typename PT>
+__global__ void k_phi_rowscale(const PT* __restrict__ phi, int64_t ld, int64_t n_real, int64_t d_real,
                                double* __restrict__ rs) {
   const int64_t i = blockIdx.x;
   double m = 0.0;
@@ -644,7 +645,8 @@ __global__ void k_phi_rowscale(const float* __restrict__ phi, int64_t ld, int64_
 }
 
 // column scales c_j = 2^ceil(log2 max_i |Phi_ij| / r_i)
-__global__ void k_phi_colscale(const float* __restrict__ phi, int64_t ld, int64_t n_real, int64_t d_pad,
+template <typename PT>
+__global__ void k_phi_colscale(const PT* __restrict__ phi, int64_t ld, int64_t n_real, int64_t d_pad,
                                const double* __restrict__ rs, double* __restrict__ cs) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d_pad) return;
@@ -654,7 +656,8 @@ __global__ void k_phi_colscale(const float* __restrict__ phi, int64_t ld, int64_
 }
 
 // digit planes [4][Np][Dp] of round(Phi / (r c) * 2^30)
-__global__ void k_phi_planes(const float* __restrict__ phi, int64_t ld, int64_t np, int64_t dp,
+template <typename PT>
+__global__ void k_phi_planes(const PT* __restrict__ phi, int64_t ld, int64_t np, int64_t dp,
                              const double* __restrict__ rs, const double* __restrict__ cs, int8_t* __restrict__ planes) {
   const int64_t n = np * dp;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {

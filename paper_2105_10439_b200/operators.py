@@ -101,7 +101,10 @@ class DenseOperator(LinearOperator):
         ctx = self._ctx.get(code)
         if ctx is None:
             ctx = _lib.Context(self.n_rows, self.n_cols, code, self.device)
-            ctx.set_dictionary(self.matrix)
+            if self.matrix.dtype == np.float64:
+                ctx.set_dictionary_f64(self.matrix)  # ozaki planes from the exact float64 entries
+            else:
+                ctx.set_dictionary(self.matrix)
             self._ctx[code] = ctx
         return ctx
 
@@ -122,6 +125,52 @@ class DenseOperator(LinearOperator):
 
     def column_sq_norms(self):
         return self.context("fp64").column_sq_norms()
+
+
+class SubsampledDctOperator(DenseOperator):
+    """Phi = M Omega^{-1}: inverse orthonormal DCT-II rows selected by a mask
+    (operators.py:132-179).  Materialised once (float64, N x D) and run as a
+    dense dictionary on the GPU -- the int8 digit planes are built from the
+    float64 entries -- so D is limited to dense-friendly sizes (<= 32768)."""
+
+    kind = "undersampled-dct"
+
+    def __init__(self, dim, mask, device=0):
+        from scipy.fft import idct
+
+        mask = np.asarray(mask, dtype=np.int64)
+        if mask.ndim != 1 or mask.size < 1:
+            raise ValueError("mask must be a nonempty 1-D index array")
+        if np.unique(mask).size != mask.size:
+            raise ValueError("mask indices must be distinct")
+        if mask.min() < 0 or mask.max() >= dim:
+            raise ValueError(f"mask indices must lie in [0, {dim})")
+        if dim > 32768:
+            raise ValueError("SubsampledDctOperator is materialised; use PartialDct2Operator for large D")
+        mask = np.sort(mask)
+        super().__init__(idct(np.eye(dim), axis=0, norm="ortho")[mask, :], device=device)
+        mask.flags.writeable = False
+        self.mask = mask
+
+    def column_sq_norms(self):
+        """Analytic column norms, operators.py:165-179."""
+        dim = self.n_cols
+        pts = (2.0 * self.mask + 1.0) * (np.pi / (2.0 * dim))
+        scale = np.full(dim, 2.0 / dim)
+        scale[0] = 1.0 / dim
+        out = np.empty(dim)
+        for start in range(0, dim, 512):
+            stop = min(start + 512, dim)
+            c = np.cos(np.outer(np.arange(start, stop), pts))
+            out[start:stop] = scale[start:stop] * np.einsum("ji,ji->j", c, c)
+        return out
+
+
+def build_undersampled_dct(dim, n_rows, rng):
+    """Orthonormal DCT-II rows subsampled uniformly without replacement (operators.py:235-240)."""
+    if not 1 <= n_rows <= dim:
+        raise ValueError(f"need 1 <= N <= D, got N={n_rows}, D={dim}")
+    return SubsampledDctOperator(dim, rng.choice(dim, size=n_rows, replace=False))
 
 
 class ConvolutionOperator(LinearOperator):

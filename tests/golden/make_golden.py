@@ -174,6 +174,36 @@ def make_conv():
     np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **out)
 
 
+def make_reference_workloads():
+    """Two workloads the reference's own tests use: the undersampled-DCT
+    recovery of test_cofem.py:257-265 and a float64 dense instance from its
+    conftest generator (tests/conftest.py:10-24)."""
+    from sbl.operators import build_undersampled_dct
+    from sbl.problem import substream
+    from sbl.simulate import gen_observation, gen_signal
+
+    op = build_undersampled_dct(1024, 341, substream(0, 0))
+    z = gen_signal(1024, 122, "normal", substream(0, 1))
+    y, beta = gen_observation(op, z, 0.01, substream(0, 2))
+    cfg = sbl.CofemConfig(iterations=30, probes=20, seed=0)
+    state, est, diag = ref_cofem.run_cofem(SblProblem(y, op, beta), cfg)
+    out = {"dct_mask": op.mask, "dct_y": y, "dct_z": z, "dct_beta": np.array(beta), "dct_mu": est.mu,
+           "dct_alpha": state.alpha, "dct_steps": np.array([r["cg_steps"] for r in diag])}
+    print(f"dct1d steps {[r['cg_steps'] for r in diag]}")
+    rng = np.random.default_rng(12345)
+    n_rows, dim, n_spikes, beta = 64, 256, 15, 1e4
+    phi = rng.normal(0.0, 1.0 / np.sqrt(n_rows), size=(n_rows, dim))
+    zz = np.zeros(dim)
+    zz[rng.choice(dim, size=n_spikes, replace=False)] = rng.uniform(-2.0, 2.0, size=n_spikes)
+    yy = phi @ zz + (1.0 / np.sqrt(beta)) * rng.standard_normal(n_rows)
+    cfg = sbl.CofemConfig(iterations=30, probes=20, seed=0)
+    state, est, diag = ref_cofem.run_cofem(SblProblem(yy, DenseOperator(phi), beta), cfg)
+    out.update(d64_phi=phi, d64_y=yy, d64_z=zz, d64_mu=est.mu, d64_alpha=state.alpha,
+               d64_steps=np.array([r["cg_steps"] for r in diag]))
+    print(f"dense64 steps {[r['cg_steps'] for r in diag]}")
+    np.savez_compressed(os.path.join(HERE, "reference_workloads.npz"), **out)
+
+
 def make_known_answers():
     """Known-answer values the reference's own tests pin (test_cofem.py:187-190,
     test_cg.py:450-466, test_operators.py:392-394), recomputed from the reference."""
@@ -189,11 +219,13 @@ def make_known_answers():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid", "conv"}
+    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid", "conv", "workloads"}
     if "known" in which:
         make_known_answers()
     if "conv" in which:
         make_conv()
+    if "workloads" in which:
+        make_reference_workloads()
     if "pcg" in which:
         make_pcg()
     if "variants" in which:

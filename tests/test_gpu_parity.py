@@ -386,3 +386,67 @@ def test_run_cofem_dct2_parity_with_oracle():
     emu, ea = rel(est.mu, mu), rel(st.alpha, alpha)
     assert emu <= 1e-4 and ea <= 1e-4, (emu, ea, [d["cg_steps"] for d in diag], [d["cg_steps"] for d in odiag])
     np.testing.assert_array_equal(st.alpha < PRUNE, alpha < PRUNE)
+
+
+# --------------------------------------------- the reference's own workloads --
+@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+def test_reference_dct1d_recovery_parity(precision):
+    """test_cofem.py:257-265 workload (SubsampledDctOperator D=1024, N=341, 30 EM
+    iterations): parity with the reference and its NRMSE < 2% bar."""
+    from paper_2105_10439_b200 import SubsampledDctOperator
+
+    g = golden("reference_workloads.npz")
+    prob = SblProblem(g["dct_y"], SubsampledDctOperator(1024, g["dct_mask"]), float(g["dct_beta"]))
+    cfg = CofemConfig(iterations=30, probes=20, seed=0, cg=CgConfig(precision=precision))
+    st, est, diag = run_cofem(prob, cfg)
+    emu, ea = rel(est.mu, g["dct_mu"]), rel(st.alpha, g["dct_alpha"])
+    # the reference's default CG tolerance (1e-4) leaves each E-step converged
+    # only to 1e-4: a 1e-9 operator difference can flip a step count at the
+    # threshold and move the iterate ~1e-4, hence alpha <= 1e-3 here (the
+    # BASELINE configs run at tol 1e-5 and are held to 1e-4)
+    assert emu <= 1e-4 and ea <= 1e-3, (emu, ea)
+    steps = np.array([d["cg_steps"] for d in diag])
+    assert np.all(np.abs(steps - g["dct_steps"]) <= 1)
+    assert S.nrmse(est.mu, g["dct_z"]) < 2.0
+    np.testing.assert_array_equal(st.alpha < PRUNE, g["dct_alpha"] < PRUNE)
+
+
+@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+def test_reference_dense_float64_parity(precision):
+    """A float64 (not float32-exact) dictionary from the reference's conftest
+    generator: the ozaki planes are built from the float64 entries."""
+    g = golden("reference_workloads.npz")
+    prob = SblProblem(g["d64_y"], DenseOperator(g["d64_phi"]), 1e4)
+    cfg = CofemConfig(iterations=30, probes=20, seed=0, cg=CgConfig(precision=precision))
+    st, est, diag = run_cofem(prob, cfg)
+    emu, ea = rel(est.mu, g["d64_mu"]), rel(st.alpha, g["d64_alpha"])
+    assert emu <= 1e-4, (emu, ea)
+    if precision == "ozaki":
+        assert ea <= 1e-3, (emu, ea)
+    np.testing.assert_array_equal(st.alpha < PRUNE, g["d64_alpha"] < PRUNE)
+
+
+def test_filtered_mode_matches_nnls_oracle():
+    """cofem.py:248-271 on the nonneg variant (reference test_cofem.py:398-418
+    setup): nonnegative output whose restricted ridge objective matches an
+    active-set NNLS on the same columns."""
+    from scipy.optimize import nnls
+
+    from paper_2105_10439_b200 import build_exp_convolution, filtered_mode, substream
+
+    dim, n_spikes = 256, 6
+    op = build_exp_convolution(dim, 0.04)
+    rng = substream(8, 1)
+    z = np.zeros(dim)
+    z[rng.choice(dim, n_spikes, replace=False)] = rng.exponential(1.0 / 1.5, n_spikes)
+    y = op.materialize() @ z + 0.01 * substream(8, 2).standard_normal(dim)
+    prob = SblProblem(y, op, 1e4)
+    st, est, _ = run_cofem(prob, CofemConfig(iterations=30, seed=8, variant="nonneg"))
+    res = filtered_mode(prob, st, est, 0.05)
+    assert not res.empty and np.all(res.z >= 0.0)
+    cols = op.materialize()[:, res.support]
+    ridge = st.alpha[res.support] / prob.beta
+    oracle, _ = nnls(np.vstack([cols, np.diag(np.sqrt(ridge))]), np.concatenate([y, np.zeros(res.support.size)]))
+    assert np.max(np.abs(res.z[res.support] - oracle)) <= 1e-5
+    empty = filtered_mode(prob, st, type(est)(np.zeros(dim), np.ones(dim)), 0.05)
+    assert empty.empty and empty.support.size == 0

@@ -142,3 +142,17 @@ def test_convolution_operator_host_side_matches_reference():
         ConvolutionOperator(8, 1.0)
     with pytest.raises(ValueError):
         ConvolutionOperator.from_taps(2, [1.0, 2.0, 3.0])
+
+
+def test_oracle_reference_workloads():
+    """The reference's undersampled-DCT recovery (test_cofem.py:257-265) and a
+    float64 dense instance (its conftest generator), bit for bit."""
+    g = golden("reference_workloads.npz")
+    cfg = O.CofemConfig(iterations=30, probes=20, seed=0)
+    alpha, mu, s, diag = O.run_cofem(O.dct_op(1024, g["dct_mask"]), g["dct_y"], float(g["dct_beta"]), cfg)
+    np.testing.assert_array_equal(mu, g["dct_mu"])
+    np.testing.assert_array_equal(alpha, g["dct_alpha"])
+    assert [d["cg_steps"] for d in diag] == list(g["dct_steps"])
+    alpha, mu, s, diag = O.run_cofem(O.dense_op(g["d64_phi"]), g["d64_y"], 1e4, cfg)
+    np.testing.assert_array_equal(mu, g["d64_mu"])
+    np.testing.assert_array_equal(alpha, g["d64_alpha"])
