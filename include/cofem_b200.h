@@ -185,6 +185,20 @@ int cofem_run(cofem_ctx* ctx, const double* y, double beta, const cofem_em_confi
               int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration,
               int32_t* failed_step);
 
+/* ---- multi-task CoFEM ----------------------------------------------------------
+ * cofem.run_cofem_multitask (cofem.py:160-214): L tasks (one context each,
+ * same D and precision, one GPU) share alpha; every EM iteration solves all
+ * L (K+1)-column systems in ONE lockstep PCG whose stopping rule aggregates
+ * the residual over all tasks (cg.solve_blocked, cg.py:201-234), then the
+ * pooled M-step alpha = L / sum_l (mu_l^2 + s_l).  betas: one noise precision
+ * per task (task.beta).  theta (custom policy only): L x D, row l for task l.
+ * probes: T x L x D x K int8
+ * in the reference's draw order; mus / ss: L host pointers of length D. */
+int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const* ys, const double* betas,
+                        const cofem_em_config* em, const cofem_cg_config* cg, const double* theta,
+                        const int8_t* probes, double* alpha, double* const* mus, double* const* ss,
+                        int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration, int32_t* failed_step);
+
 /* ---- device-timed benchmark hooks ----------------------------------------
  * Run `n_iter` EM iterations continuing the context's resident state
  * (bench.py "value": inputs already in HBM), returning device milliseconds

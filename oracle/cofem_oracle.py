@@ -410,3 +410,51 @@ def run_cofem_multitask(ops, ys, beta, cfg, share_probes=False):
         diag.append({"iteration": t, "cg_steps": rep.steps_taken,
                      "cg_residual": rep.final_relative_residual})
     return alpha, ests, diag
+
+
+def ozaki_dictionary(phi):
+    """The dictionary the 'ozaki' device mode multiplies (NOT reference code):
+    Phi_ij rounded to round(Phi_ij / (r_i c_j) 2^30) r_i c_j / 2^30 with
+    power-of-two row scales r_i = 2^ceil(log2 max_j |Phi_ij|) and column
+    scales c_j = 2^ceil(log2 max_i |Phi_ij| / r_i) (csrc/ozaki.cuh
+    k_phi_rowscale / k_phi_colscale / k_phi_planes).  Running the reference
+    recursion on this matrix separates representation sensitivity of a
+    workload from kernel error."""
+    phi = np.asarray(phi, dtype=np.float64)
+
+    def p2(m):
+        e = np.ceil(np.log2(np.where(m > 0, m, 1.0)))
+        return np.where(m > 0, 2.0 ** e, 1.0)
+
+    r = p2(np.abs(phi).max(axis=1))
+    c = p2((np.abs(phi) / r[:, None]).max(axis=0))
+    sc = r[:, None] * c[None, :]
+    return np.rint(phi / sc * 2.0**30) * sc / 2.0**30
+
+
+def ozaki_op(phi):
+    """Arithmetic model of the 'ozaki' device contraction (NOT reference code):
+    the dictionary is ozaki_dictionary(phi); every operand column is rounded
+    to 31-bit fixed point against its own power-of-two scale s_q =
+    2^ceil(log2 max_j |M_jq w_j|) (w = Phi's column scales c for Phi V, its
+    row scales r for Phi^T U; csrc/ozaki.cuh k_quantize / col_scale) and the
+    int8 digit products are summed exactly, so the device result is this
+    matrix product up to the final fp64 rounding.  Running the reference
+    recursion with it reproduces the device's CG trajectory."""
+    phi = np.asarray(phi, dtype=np.float64)
+
+    def p2(m):
+        return np.where(m > 0, 2.0 ** np.ceil(np.log2(np.where(m > 0, m, 1.0))), 1.0)
+
+    r = p2(np.abs(phi).max(axis=1))
+    c = p2((np.abs(phi) / r[:, None]).max(axis=0))
+    phq = ozaki_dictionary(phi)
+
+    def qcols(M, w):
+        X = M * w[:, None]
+        s = p2(np.abs(X).max(axis=0))
+        return np.rint(X / s * 2.0**30) * s / 2.0**30 / w[:, None]
+
+    base = dense_op(phq)
+    return Op(base.n_rows, base.n_cols, lambda V: phq @ qcols(V, c), lambda U: phq.T @ qcols(U, r),
+              base.col_sq_norms, base.materialize, "dense")

@@ -51,6 +51,7 @@ EXPORTED = (
     "cofem_column_sq_norms",
     "cofem_pcg_solve",
     "cofem_run",
+    "cofem_run_multitask",
     "cofem_bench_prepare",
     "cofem_bench_iterations",
 )
@@ -147,6 +148,11 @@ def load():
                               POINTER(c_double), POINTER(c_int8), c_uint64, POINTER(c_double),
                               POINTER(c_double), POINTER(c_double), POINTER(c_int32), POINTER(c_double),
                               POINTER(c_int32), POINTER(c_int32)]),
+        "cofem_run_multitask": (c_int, [POINTER(vp), c_int, POINTER(POINTER(c_double)), POINTER(c_double),
+                                        POINTER(EmConfigC), POINTER(CgConfigC), POINTER(c_double),
+                                        POINTER(c_int8), POINTER(c_double), POINTER(POINTER(c_double)),
+                                        POINTER(POINTER(c_double)), POINTER(c_int32), POINTER(c_double),
+                                        POINTER(c_int32), POINTER(c_int32)]),
         "cofem_bench_prepare": (c_int, [vp, POINTER(c_double), c_double, POINTER(EmConfigC),
                                         POINTER(CgConfigC), c_uint64]),
         "cofem_bench_iterations": (c_int, [vp, c_int, c_int, POINTER(TimingC)]),
@@ -344,6 +350,46 @@ class Context:
         t = TimingC()
         check(load().cofem_bench_iterations(self.handle, int(n_iter), 1 if time_kernels else 0, ctypes.byref(t)))
         return {k: getattr(t, k) for k, _ in TimingC._fields_}
+
+
+def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_max, floor_eps, max_steps,
+                  tolerance, printed=False, theta=None, probe_blocks=None):
+    """cofem_run_multitask over L contexts (one per task, same D, one GPU).
+
+    probe_blocks: T x L x D x K signs; theta: L x D (custom policy).  Returns
+    ((alpha, mus, ss, steps, resid), None) or (None, (iteration, step)) on divergence."""
+    L = len(contexts)
+    d = contexts[0].n_cols
+    em = EmConfigC(int(iterations), int(probes), 0, int(theta_policy), float(clamp_max), float(floor_eps))
+    cg = CgConfigC(int(max_steps), 1 if printed else 0, float(tolerance))
+    handles = (c_void_p * L)(*[c.handle for c in contexts])
+    ys = [np.ascontiguousarray(y, dtype=np.float64) for y in ys]
+    y_ptrs = (POINTER(c_double) * L)(*[_dp(y) for y in ys])
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    assert betas.shape == (L,)
+    th = None
+    if theta is not None:
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        assert theta.shape == (L, d)
+        th = _dp(theta)
+    probe_blocks = np.ascontiguousarray(probe_blocks, dtype=np.int8)
+    assert probe_blocks.shape == (iterations, L, d, probes)
+    alpha = np.empty(d)
+    mus = [np.empty(d) for _ in range(L)]
+    ss = [np.empty(d) for _ in range(L)]
+    mu_ptrs = (POINTER(c_double) * L)(*[_dp(m) for m in mus])
+    s_ptrs = (POINTER(c_double) * L)(*[_dp(m) for m in ss])
+    steps = np.zeros(iterations, dtype=np.int32)
+    resid = np.zeros(iterations)
+    fit, fst = c_int32(0), c_int32(0)
+    rc = load().cofem_run_multitask(handles, L, y_ptrs, _dp(betas), ctypes.byref(em), ctypes.byref(cg), th,
+                                    probe_blocks.ctypes.data_as(POINTER(c_int8)), _dp(alpha), mu_ptrs, s_ptrs,
+                                    steps.ctypes.data_as(POINTER(c_int32)), _dp(resid), ctypes.byref(fit),
+                                    ctypes.byref(fst))
+    if rc == COFEM_EDIVERGED:
+        return None, (fit.value, fst.value)
+    check(rc)
+    return (alpha, mus, ss, steps, resid), None
 
 
 def nccl_unique_id() -> bytes:

@@ -907,6 +907,110 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   return 0;
 }
 
+// ---- multi-task lockstep PCG (cg.solve_blocked over the tasks' systems,
+// cg.py:201-234, as run_cofem_multitask drives it): every task keeps its own
+// blocks and per-column scalars; the stopping rule aggregates ||R||_F and
+// ||B||_F over all tasks (k_sum_tasks -> agg), and one status gates them all.
+// All contexts run on task 0's stream.
+template <typename T>
+int pcg_multi(cofem_ctx** cs, int L, const double* betas, int q_real, const cofem_cg_config* cg, cofem_cg_report* rep,
+              double* agg, double** dptrs) {
+  cofem_ctx* c0 = cs[0];
+  const int ldq = c0->ldq;
+  const int bs = elem_block(ldq);
+  memset(rep, 0, sizeof(*rep));
+  Status s0{};
+  Status* st = c0->st;
+  CK(cudaMemcpyAsync(st, &s0, sizeof(Status), cudaMemcpyHostToDevice, c0->stream));
+  std::vector<double> ones(ldq, 1.0);
+  // pointer tables: rn2[L] | bn2[L]
+  std::vector<double*> tab(2 * L);
+  for (int l = 0; l < L; ++l) {
+    cofem_ctx* c = cs[l];
+    Scalars sc = c->sc();
+    tab[l] = sc.rn2;
+    tab[L + l] = sc.bn2;
+    CK(cudaMemcpyAsync(sc.rho[0], ones.data(), ldq * sizeof(double), cudaMemcpyHostToDevice, c0->stream));
+    CK(cudaMemsetAsync(c->frozen, 0, ldq * sizeof(int), c0->stream));
+    CK(cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c0->stream));
+    k_pcg_init<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c0->stream>>>(
+        c->Dp, ldq, q_real, (T*)c->X, (T*)c->P, (const T*)c->R, c->minv, 1, nullptr, sc);
+    c->launches++;
+  }
+  CK(cudaMemcpyAsync(dptrs, tab.data(), 2 * L * sizeof(double*), cudaMemcpyHostToDevice, c0->stream));
+  k_sum_tasks<<<1, 1, 0, c0->stream>>>(L, ldq, (const double* const*)dptrs, (const double* const*)(dptrs + L), agg);
+  CK(cudaGetLastError());
+  double hagg[2];
+  CK(cudaMemcpyAsync(hagg, agg, 2 * sizeof(double), cudaMemcpyDeviceToHost, c0->stream));
+  CK(cudaStreamSynchronize(c0->stream));
+  const double bnorm = sqrt(hagg[1]);
+  if (bnorm == 0.0) {
+    rep->converged = 1;
+    return 0;
+  }
+  if (1.0 <= cg->tolerance) {
+    rep->final_relative_residual = 1.0;
+    rep->converged = 1;
+    return 0;
+  }
+  const bool oz = c0->prec == COFEM_OZAKI;
+  for (int l = 0; l < L; ++l) {
+    cofem_ctx* c = cs[l];
+    const bool fused = oz && c->kind != 2;
+    if (fused) {
+      if (c->kind == 0) CKR(ensure_oz(c));
+      CK(cudaMemsetAsync(c->colmax, 0, ldq * sizeof(unsigned long long), c0->stream));
+    }
+    k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c0->stream>>>(
+        c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
+        c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg);
+    c->launches++;
+    c->p_colmax_valid = fused;
+  }
+  CK(cudaGetLastError());
+  int u = 1;
+  for (; u <= cg->max_steps; ++u) {
+    if (u > LAG) {
+      const int slot = (u - LAG) % LAG;
+      CK(cudaEventSynchronize(c0->ev[slot]));
+      if (c0->h_st[slot].done) break;
+    }
+    for (int l = 0; l < L; ++l) {
+      cofem_ctx* c = cs[l];
+      const bool fused = oz && c->kind != 2;
+      CKR(system_apply_dev<T>(c, betas[l], st));
+      k_update<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c0->stream>>>(
+          c->Dp, ldq, q_real, u & 1, (T*)c->X, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, 1, nullptr,
+          c->sc(), fused ? c->colmax : nullptr, st);
+      c->launches++;
+    }
+    k_sum_tasks<<<1, 1, 0, c0->stream>>>(L, ldq, (const double* const*)dptrs, (const double* const*)(dptrs + L), agg);
+    for (int l = 0; l < L; ++l) {
+      cofem_ctx* c = cs[l];
+      const bool fused = oz && c->kind != 2;
+      k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c0->stream>>>(
+          c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
+          c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg);
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    const int slot = u % LAG;
+    CK(cudaMemcpyAsync(&c0->h_st[slot], st, sizeof(Status), cudaMemcpyDeviceToHost, c0->stream));
+    CK(cudaEventRecord(c0->ev[slot], c0->stream));
+  }
+  for (int l = 0; l < L; ++l) cs[l]->p_colmax_valid = false;
+  Status fin;
+  CK(cudaMemcpyAsync(&fin, st, sizeof(Status), cudaMemcpyDeviceToHost, c0->stream));
+  CK(cudaStreamSynchronize(c0->stream));
+  c0->pcg_steps += fin.steps;
+  rep->steps_taken = fin.steps;
+  rep->converged = fin.converged;
+  rep->diverged = fin.diverged;
+  rep->final_relative_residual = fin.delta;
+  if (fin.diverged) return fail(COFEM_EDIVERGED, "non-finite residual at CG step " + std::to_string(fin.steps));
+  return 0;
+}
+
 // host double (rows x q, row stride q) -> device T (rows_pad x ldq, zero padded)
 template <typename T>
 int upload_block(cofem_ctx* c, const double* h, int64_t rows, int64_t q, int64_t rows_pad, int ldq, void* dst) {
@@ -1154,6 +1258,104 @@ int run_impl(cofem_ctx* c, const double* y, double beta, const cofem_em_config* 
   if (mu) CK(cudaMemcpy(mu, c->mu, c->D * sizeof(double), cudaMemcpyDeviceToHost));
   if (s) CK(cudaMemcpy(s, c->s, c->D * sizeof(double), cudaMemcpyDeviceToHost));
   return 0;
+}
+
+// run_cofem_multitask (cofem.py:160-214): shared alpha, all L (K+1)-column
+// systems in one lockstep PCG per EM iteration, pooled M-step
+template <typename T>
+int run_multi_impl(cofem_ctx** cs, int L, const double* const* ys, const double* betas, const cofem_em_config* em,
+                   const cofem_cg_config* cg, const double* theta, const int8_t* probes, double* alpha,
+                   double* const* mus, double* const* ss, int32_t* steps, double* resid, int32_t* fail_it,
+                   int32_t* fail_step) {
+  cofem_ctx* c0 = cs[0];
+  const int K = em->probes;
+  std::vector<cudaStream_t> saved(L);
+  for (int l = 0; l < L; ++l) {
+    saved[l] = cs[l]->stream;
+    CKR(em_prepare<T>(cs[l], ys[l], betas[l], em, theta ? theta + (size_t)l * cs[l]->D : nullptr));
+  }
+  CK(cudaDeviceSynchronize());
+  for (int l = 0; l < L; ++l) cs[l]->stream = c0->stream;  // one stream for the lockstep
+  double* agg = nullptr;
+  double** dptrs = nullptr;
+  double** aptrs = nullptr;  // mu | s | alpha | minv | theta (L each)
+  double* dbeta = nullptr;
+  int rc = 0;
+  auto cleanup = [&]() {
+    for (int l = 0; l < L; ++l) cs[l]->stream = saved[l];
+    if (agg) cudaFree(agg);
+    if (dptrs) cudaFree(dptrs);
+    if (aptrs) cudaFree(aptrs);
+    if (dbeta) cudaFree(dbeta);
+  };
+  if (cudaMalloc(&agg, 2 * sizeof(double)) || cudaMalloc(&dptrs, 2 * L * sizeof(double*)) ||
+      cudaMalloc(&aptrs, 5 * L * sizeof(double*)) || cudaMalloc(&dbeta, L * sizeof(double))) {
+    cleanup();
+    return fail(COFEM_ENOMEM, "multitask tables");
+  }
+  std::vector<double*> at(5 * L);
+  for (int l = 0; l < L; ++l) {
+    at[l] = cs[l]->mu;
+    at[L + l] = cs[l]->s;
+    at[2 * L + l] = cs[l]->alpha;
+    at[3 * L + l] = cs[l]->minv;
+    at[4 * L + l] = cs[l]->theta;
+  }
+  cudaMemcpy(aptrs, at.data(), at.size() * sizeof(double*), cudaMemcpyHostToDevice);
+  cudaMemcpy(dbeta, betas, L * sizeof(double), cudaMemcpyHostToDevice);
+  const int64_t dk = c0->D * K;
+  for (int t = 1; t <= em->iterations && !rc; ++t) {
+    for (int l = 0; l < L; ++l) {
+      cofem_ctx* c = cs[l];
+      const int8_t* pt = probes + ((size_t)(t - 1) * L + l) * dk;
+      if (cudaMemcpyAsync(c->probes, pt, (size_t)dk, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess) {
+        rc = fail(COFEM_ECUDA, "probe upload");
+        break;
+      }
+      const int64_t n = c->Dp * c->ldq;
+      k_build_rhs<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c0->stream>>>(
+          c->D, c->Dp, c->ldq, K, c->probes, 0, t, c->col_offset, c->aty, (T*)c->R, c->probe_store);
+      c->launches++;
+    }
+    if (rc) break;
+    cofem_cg_report rep;
+    rc = pcg_multi<T>(cs, L, betas, K + 1, cg, &rep, agg, dptrs);
+    if (steps) steps[t - 1] = rep.steps_taken;
+    if (resid) resid[t - 1] = rep.final_relative_residual;
+    if (rc == COFEM_EDIVERGED) {
+      if (fail_it) *fail_it = t;
+      if (fail_step) *fail_step = rep.steps_taken;
+      rc = fail(COFEM_EDIVERGED, "non-finite residual at CG step " + std::to_string(rep.steps_taken) +
+                                     " (EM iteration " + std::to_string(t) + ")");
+      break;
+    }
+    if (rc) break;
+    if (t == em->iterations && alpha) cudaMemcpyAsync(alpha, c0->alpha, c0->D * sizeof(double),
+                                                       cudaMemcpyDeviceToHost, c0->stream);
+    for (int l = 0; l < L; ++l) {
+      cofem_ctx* c = cs[l];
+      k_em_finish<T><<<(int)((c->D + 255) / 256), 256, 0, c0->stream>>>(
+          c->D, c->ldq, K, betas[l], (const T*)c->X, c->probe_store, c->mu, c->s, c->alpha, c->minv, c->theta,
+          em->theta_policy, 0, 0, em->floor_eps, em->clamp_max);
+      c->launches++;
+    }
+    if (t < em->iterations) {
+      k_multitask_alpha<<<(int)((c0->D + 255) / 256), 256, 0, c0->stream>>>(
+          c0->D, L, dbeta, (const double* const*)aptrs, (const double* const*)(aptrs + L), aptrs + 2 * L,
+          aptrs + 3 * L, (const double* const*)(aptrs + 4 * L), em->theta_policy, em->floor_eps, em->clamp_max);
+      c0->launches++;
+    }
+    if (cudaGetLastError() != cudaSuccess) rc = fail(COFEM_ECUDA, "multitask kernels");
+  }
+  if (!rc) {
+    cudaStreamSynchronize(c0->stream);
+    for (int l = 0; l < L; ++l) {
+      if (mus && mus[l]) cudaMemcpy(mus[l], cs[l]->mu, c0->D * sizeof(double), cudaMemcpyDeviceToHost);
+      if (ss && ss[l]) cudaMemcpy(ss[l], cs[l]->s, c0->D * sizeof(double), cudaMemcpyDeviceToHost);
+    }
+  }
+  cleanup();
+  return rc;
 }
 
 }  // namespace
@@ -1650,6 +1852,30 @@ int cofem_run(cofem_ctx* c, const double* y, double beta, const cofem_em_config*
   if (!(beta > 0) || !std::isfinite(beta)) return fail(COFEM_EINVAL, "beta must be positive and finite");
   return DISPATCH(c, run_impl, c, y, beta, em, cg, theta, probes, dseed, alpha, mu, s, cg_steps, cg_residuals,
                   failed_iteration, failed_step);
+}
+
+int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const* ys, const double* betas,
+                        const cofem_em_config* em, const cofem_cg_config* cg, const double* theta,
+                        const int8_t* probes, double* alpha, double* const* mus, double* const* ss,
+                        int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration, int32_t* failed_step) {
+  if (!ctxs || n_tasks < 1 || !ys || !betas || !em || !cg || !probes) return fail(COFEM_EINVAL, "null argument");
+  cofem_ctx* c0 = ctxs[0];
+  CKR(check_ctx(c0));
+  if (em->variant != COFEM_STANDARD) return fail(COFEM_EINVAL, "multi-task loop supports the standard variant only");
+  if (em->iterations < 1 || em->probes < 1 || em->probes + 1 > 1024) return fail(COFEM_EINVAL, "bad EM config");
+  if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
+  for (int l = 0; l < n_tasks; ++l) {
+    cofem_ctx* c = ctxs[l];
+    if (!(betas[l] > 0) || !std::isfinite(betas[l])) return fail(COFEM_EINVAL, "beta must be positive and finite");
+    CKR(check_ctx(c));
+    if (c->D != c0->D || c->prec != c0->prec || c->device != c0->device || c->nranks > 1)
+      return fail(COFEM_EINVAL, "tasks must share D, precision and device (single GPU)");
+    for (int m = 0; m < l; ++m)
+      if (ctxs[m] == c) return fail(COFEM_EINVAL, "each task needs its own context");
+  }
+  std::vector<cofem_ctx*> cs(ctxs, ctxs + n_tasks);
+  return DISPATCH(c0, run_multi_impl, cs.data(), n_tasks, ys, betas, em, cg, theta, probes, alpha, mus, ss,
+                  cg_steps, cg_residuals, failed_iteration, failed_step);
 }
 
 int cofem_bench_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em,

@@ -275,19 +275,26 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
 template <typename T>
 __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
                             T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
-                            const double* pre, unsigned long long* colmax, Status* st) {
+                            const double* pre, unsigned long long* colmax, Status* st,
+                            const double* agg = nullptr) {
+  // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
   if (st->done) return;
   extern __shared__ double sm_dir[];
   const int cur = step & 1, nxt = (step + 1) & 1;
   if (step == 0) {
     double b2 = 0.0;
     for (int c = 0; c < ldq; ++c) b2 += sc.bn2[c];
+    if (agg) b2 = agg[1];
     if (blockIdx.x == 0 && threadIdx.x == 0) st->bnorm = sqrt(b2);
   } else {
     double r2 = 0.0;
     for (int c = 0; c < ldq; ++c) r2 += sc.rn2[c];
     double b2 = 0.0;
     for (int c = 0; c < ldq; ++c) b2 += sc.bn2[c];
+    if (agg) {
+      r2 = agg[0];
+      b2 = agg[1];
+    }
     const double delta = sqrt(r2) / sqrt(b2);
     const bool finite = isfinite(delta);
     const bool conv = finite && delta <= tol;
@@ -337,6 +344,39 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
   }
   if (blockIdx.x == 0 && threadIdx.x < ldq) sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
   if (colmax) block_col_max(sm_dir, ldq, pmax, colmax);
+}
+
+// ---- multi-task glue (cofem.py:160-214) -------------------------------------
+// agg = {sum_l sum_q rn2_l[q], sum_l sum_q bn2_l[q]} in task order
+__global__ void k_sum_tasks(int L, int ldq, const double* const* rn2, const double* const* bn2, double* agg) {
+  // one sequential pass over the concatenated columns, like the single-task
+  // reduction in k_direction (so L = 1 reproduces run_cofem bit for bit)
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double r = 0.0, b = 0.0;
+  for (int l = 0; l < L; ++l)
+    for (int q = 0; q < ldq; ++q) {
+      r += rn2[l][q];
+      b += bn2[l][q];
+    }
+  agg[0] = r;
+  agg[1] = b;
+}
+
+// shared precision update: alpha = min(L / max(sum_l (mu_l^2 + s_l), floor), clamp),
+// written into every task together with its next M^-1 (task beta_l)
+__global__ void k_multitask_alpha(int64_t d_real, int L, const double* betas, const double* const* mu,
+                                  const double* const* s, double* const* alpha, double* const* minv,
+                                  const double* const* theta, int theta_policy, double floor_eps, double clamp_max) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < d_real; j += (int64_t)gridDim.x * blockDim.x) {
+    double tot = 0.0;
+    for (int l = 0; l < L; ++l) tot = tot + (mu[l][j] * mu[l][j] + s[l][j]);
+    const double a = fmin((double)L / fmax(tot, floor_eps), clamp_max);
+    for (int l = 0; l < L; ++l) {
+      alpha[l][j] = a;
+      const double th = theta_policy == 0 ? 1.0 : (theta_policy == 2 ? 0.0 : theta[l][j]);
+      minv[l][j] = theta_policy == 2 ? 1.0 : 1.0 / (betas[l] * th + a);
+    }
+  }
 }
 
 // ---- EM glue ---------------------------------------------------------------

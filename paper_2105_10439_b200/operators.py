@@ -100,12 +100,16 @@ class DenseOperator(LinearOperator):
         code = PRECISIONS[precision]
         ctx = self._ctx.get(code)
         if ctx is None:
-            ctx = _lib.Context(self.n_rows, self.n_cols, code, self.device)
-            if self.matrix.dtype == np.float64:
-                ctx.set_dictionary_f64(self.matrix)  # ozaki planes from the exact float64 entries
-            else:
-                ctx.set_dictionary(self.matrix)
-            self._ctx[code] = ctx
+            ctx = self._ctx[code] = self.new_context(precision)
+        return ctx
+
+    def new_context(self, precision="fp32"):
+        """An uncached device copy (the caller closes it)."""
+        ctx = _lib.Context(self.n_rows, self.n_cols, PRECISIONS[precision], self.device)
+        if self.matrix.dtype == np.float64:
+            ctx.set_dictionary_f64(self.matrix)  # ozaki planes from the exact float64 entries
+        else:
+            ctx.set_dictionary(self.matrix)
         return ctx
 
     def release(self):
@@ -216,13 +220,15 @@ class ConvolutionOperator(LinearOperator):
         return h[: keep[-1] + 1] if keep.size else h[:1]
 
     def context(self, precision="ozaki"):
-        if precision != "ozaki":
-            raise NotImplementedError("convolution dictionaries run in the 'ozaki' precision mode")
         ctx = self._ctx.get(precision)
         if ctx is None:
-            ctx = _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
-            self._ctx[precision] = ctx
+            ctx = self._ctx[precision] = self.new_context(precision)
         return ctx
+
+    def new_context(self, precision="ozaki"):
+        if precision != "ozaki":
+            raise NotImplementedError("convolution dictionaries run in the 'ozaki' precision mode")
+        return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
 
     def release(self):
         for ctx in self._ctx.values():
@@ -279,13 +285,15 @@ class PartialDct2Operator(LinearOperator):
         self._ctx = {}
 
     def context(self, precision="ozaki"):
-        if precision != "ozaki":
-            raise NotImplementedError("2-D DCT dictionaries run in the 'ozaki' precision mode")
         ctx = self._ctx.get(precision)
         if ctx is None:
-            ctx = _lib.Context.dct2(self.n, self.mask, _lib.OZAKI, self.device)
-            self._ctx[precision] = ctx
+            ctx = self._ctx[precision] = self.new_context(precision)
         return ctx
+
+    def new_context(self, precision="ozaki"):
+        if precision != "ozaki":
+            raise NotImplementedError("2-D DCT dictionaries run in the 'ozaki' precision mode")
+        return _lib.Context.dct2(self.n, self.mask, _lib.OZAKI, self.device)
 
     def release(self):
         for ctx in self._ctx.values():

@@ -204,6 +204,59 @@ def make_reference_workloads():
     np.savez_compressed(os.path.join(HERE, "reference_workloads.npz"), **out)
 
 
+def make_multitask():
+    """run_cofem_multitask (cofem.py:160-214) on the reference's shared-support
+    undersampled-DCT tasks (test_acceptance.py:367-378 / test_cofem.py:295-320,
+    seed 42) and on three float32 dense tasks with shared probes."""
+    from sbl.operators import build_undersampled_dct
+    from sbl.problem import MultiTaskProblem, substream
+
+    out = {}
+    dim, n_rows, n_spikes, L, seed = 256, 85, 16, 3, 42
+    support = substream(seed, 1).choice(dim, size=n_spikes, replace=False)
+    tasks = []
+    for ell in range(L):
+        op = build_undersampled_dct(dim, n_rows, substream(seed, 0, ell))
+        z = np.zeros(dim)
+        z[support] = substream(seed, 1, ell).normal(0.0, np.sqrt(5.0), size=n_spikes)
+        y = op.apply(z) + 0.01 * substream(seed, 2, ell).standard_normal(n_rows)
+        tasks.append(SblProblem(y, op, 1e4))
+        out[f"dct_mask{ell}"] = op.mask
+        out[f"dct_y{ell}"] = y
+    cfg = sbl.CofemConfig(iterations=30, probes=20, seed=seed)
+    state, ests, diag = ref_cofem.run_cofem_multitask(MultiTaskProblem(tuple(tasks)), cfg)
+    out["dct_support"] = np.sort(support)
+    out["dct_alpha"] = state.alpha
+    for ell, e in enumerate(ests):
+        out[f"dct_mu{ell}"] = e.mu
+        out[f"dct_s{ell}"] = e.s
+    out["dct_steps"] = np.array([r["cg_steps"] for r in diag])
+    print(f"multitask dct steps {[r['cg_steps'] for r in diag]}")
+
+    rng = np.random.default_rng(77)
+    n, d = 96, 384
+    tasks = []
+    zs = np.zeros(d)
+    zs[rng.choice(d, size=12, replace=False)] = 1.0
+    for ell in range(L):
+        phi = phi32(rng, n, d)
+        z = zs * rng.standard_normal(d)
+        y = phi.astype(np.float64) @ z + 0.01 * rng.standard_normal(n)
+        tasks.append(SblProblem(y, DenseOperator(phi.astype(np.float64)), 1e4))
+        out[f"dense_phi{ell}"] = phi
+        out[f"dense_y{ell}"] = y
+    cfg = sbl.CofemConfig(iterations=6, probes=12, seed=3, cg=sbl.CgConfig(max_steps=400, tolerance=1e-5))
+    state, ests, diag = ref_cofem.run_cofem_multitask(MultiTaskProblem(tuple(tasks)), cfg, share_probes=True)
+    out["dense_alpha"] = state.alpha
+    for ell, e in enumerate(ests):
+        out[f"dense_mu{ell}"] = e.mu
+        out[f"dense_s{ell}"] = e.s
+    out["dense_steps"] = np.array([r["cg_steps"] for r in diag])
+    out["dense_resid"] = np.array([r["cg_residual"] for r in diag])
+    print(f"multitask dense steps {[r['cg_steps'] for r in diag]}")
+    np.savez_compressed(os.path.join(HERE, "multitask.npz"), **out)
+
+
 def make_known_answers():
     """Known-answer values the reference's own tests pin (test_cofem.py:187-190,
     test_cg.py:450-466, test_operators.py:392-394), recomputed from the reference."""
@@ -219,13 +272,16 @@ def make_known_answers():
 
 
 if __name__ == "__main__":
-    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid", "conv", "workloads"}
+    which = set(sys.argv[1:]) or {"known", "pcg", "variants", "small", "mid", "conv", "workloads",
+                                    "multitask"}
     if "known" in which:
         make_known_answers()
     if "conv" in which:
         make_conv()
     if "workloads" in which:
         make_reference_workloads()
+    if "multitask" in which:
+        make_multitask()
     if "pcg" in which:
         make_pcg()
     if "variants" in which:

@@ -405,10 +405,22 @@ def test_reference_dct1d_recovery_parity(precision):
     # threshold and move the iterate ~1e-4, hence alpha <= 1e-3 here (the
     # BASELINE configs run at tol 1e-5 and are held to 1e-4)
     assert emu <= 1e-4 and ea <= 1e-3, (emu, ea)
-    steps = np.array([d["cg_steps"] for d in diag])
-    assert np.all(np.abs(steps - g["dct_steps"]) <= 1)
+    assert_dct_steps_close([d["cg_steps"] for d in diag], g["dct_steps"])
     assert S.nrmse(est.mu, g["dct_z"]) < 2.0
     np.testing.assert_array_equal(st.alpha < PRUNE, g["dct_alpha"] < PRUNE)
+
+
+def assert_dct_steps_close(steps, ref):
+    """Step counts on the undersampled-DCT workloads.  Phi has orthonormal
+    rows, and CG's step count there depends on Phi Phi^T = I to ~1e-11: the
+    reference's own recursion takes [2, 14, 18, ...] instead of [2, 12, 16,
+    ...] once Phi is rounded to the ozaki representation (2^-30 of the row
+    scale; tests/test_host_api.py::test_dct_step_sensitivity_is_a_reference_property),
+    so per-iteration counts are not a kernel-error signal here.  Held: the
+    first E-step (same alpha = 1 system) to +-1 and the run's total to 15%."""
+    steps, ref = np.asarray(steps), np.asarray(ref)
+    assert abs(int(steps[0]) - int(ref[0])) <= 1, (steps, ref)
+    assert abs(steps.sum() - ref.sum()) <= 0.15 * ref.sum(), (steps, ref)
 
 
 @pytest.mark.parametrize("precision", ["ozaki", "fp64"])
@@ -450,3 +462,113 @@ def test_filtered_mode_matches_nnls_oracle():
     assert np.max(np.abs(res.z[res.support] - oracle)) <= 1e-5
     empty = filtered_mode(prob, st, type(est)(np.zeros(dim), np.ones(dim)), 0.05)
     assert empty.empty and empty.support.size == 0
+
+
+# ---- multi-task (cofem.py:160-214) -------------------------------------------
+
+def _multitask_golden_tasks(g, kind):
+    from paper_2105_10439_b200 import SubsampledDctOperator
+
+    if kind == "dct":
+        return [SblProblem(g[f"dct_y{l}"], SubsampledDctOperator(256, g[f"dct_mask{l}"]), 1e4) for l in range(3)]
+    return [SblProblem(g[f"dense_y{l}"], DenseOperator(g[f"dense_phi{l}"]), 1e4) for l in range(3)]
+
+
+@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+def test_multitask_single_task_degenerates(precision):
+    """test_cofem.py:272-279: a one-task multi-task run IS the single-task loop
+    (same device kernels, same reduction order) -- bit for bit."""
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    g = golden("multitask.npz")
+    prob = _multitask_golden_tasks(g, "dense")[0]
+    cfg = CofemConfig(iterations=6, probes=10, seed=5, cg=CgConfig(precision=precision))
+    st1, est1, d1 = run_cofem(prob, cfg)
+    stm, ests, dm = run_cofem_multitask(MultiTaskProblem((prob,)), cfg)
+    np.testing.assert_array_equal(stm.alpha, st1.alpha)
+    np.testing.assert_array_equal(ests[0].mu, est1.mu)
+    np.testing.assert_array_equal(ests[0].s, est1.s)
+    assert [d["cg_steps"] for d in dm] == [d["cg_steps"] for d in d1]
+
+
+def test_multitask_identical_tasks_match_single():
+    """test_cofem.py:282-292: two copies of one task with shared probes follow
+    the single-task alpha trajectory (the same dictionary object gets a second
+    device context)."""
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    g = golden("multitask.npz")
+    prob = _multitask_golden_tasks(g, "dense")[1]
+    cfg = CofemConfig(iterations=6, probes=10, seed=9)
+    st1, _, _ = run_cofem(prob, cfg)
+    stm, ests, _ = run_cofem_multitask(MultiTaskProblem((prob, prob)), cfg, share_probes=True)
+    np.testing.assert_array_equal(ests[0].mu, ests[1].mu)
+    # the aggregate residual sums 2x the columns: only the last rounding bit
+    # of ||R|| differs, so the trajectories agree to solver precision
+    assert rel(stm.alpha, st1.alpha) <= 1e-9
+
+
+@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+def test_multitask_dense_parity(precision):
+    """Three float32 dense tasks, shared probes, against the reference."""
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    g = golden("multitask.npz")
+    cfg = CofemConfig(iterations=6, probes=12, seed=3, cg=CgConfig(max_steps=400, tolerance=1e-5,
+                                                                   precision=precision))
+    st, ests, diag = run_cofem_multitask(MultiTaskProblem(tuple(_multitask_golden_tasks(g, "dense"))), cfg,
+                                         share_probes=True)
+    assert rel(st.alpha, g["dense_alpha"]) <= 1e-4
+    for l, e in enumerate(ests):
+        assert rel(e.mu, g[f"dense_mu{l}"]) <= 1e-4, l
+    steps = np.array([d["cg_steps"] for d in diag])
+    if precision == "ozaki":
+        # ~100-step solves at large kappa: the 2^-31 operand rounding alone
+        # moves the reference's step counts (29, 87, ..., 117 -> 29, 90, ...,
+        # 137).  The reference recursion run on the arithmetic model of the
+        # contraction (oracle.ozaki_op) must give the device's counts.
+        ops = [O.ozaki_op(g[f"dense_phi{l}"]) for l in range(3)]
+        ocfg = O.CofemConfig(iterations=6, probes=12, seed=3, cg=O.CgConfig(max_steps=400, tolerance=1e-5))
+        _, oests, odiag = O.run_cofem_multitask(ops, [g[f"dense_y{l}"] for l in range(3)], 1e4, ocfg,
+                                                share_probes=True)
+        model = np.array([d["cg_steps"] for d in odiag])
+        assert np.all(np.abs(steps - model) <= 1), (steps, model)
+        for l, e in enumerate(ests):
+            assert rel(e.mu, oests[l][0]) <= 1e-6, l
+    else:
+        assert np.all(np.abs(steps - g["dense_steps"]) <= np.maximum(1, 0.1 * g["dense_steps"])), steps
+    np.testing.assert_array_equal(st.alpha < PRUNE, g["dense_alpha"] < PRUNE)
+
+
+def test_multitask_shared_support_dct_parity_and_pooling():
+    """test_cofem.py:295-320 (three undersampled-DCT tasks, one support): parity
+    with the reference run and pooled F1 >= mean lone-task F1."""
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    g = golden("multitask.npz")
+    tasks = _multitask_golden_tasks(g, "dct")
+    cfg = CofemConfig(iterations=30, probes=20, seed=42)
+    st, ests, diag = run_cofem_multitask(MultiTaskProblem(tuple(tasks)), cfg)
+    # reference default tolerance 1e-4 (see test_reference_dct1d_recovery_parity)
+    ea = rel(st.alpha, g["dct_alpha"])
+    for l, e in enumerate(ests):
+        assert rel(e.mu, g[f"dct_mu{l}"]) <= 1e-4, l
+    assert ea <= 1e-3, ea
+    assert_dct_steps_close([d["cg_steps"] for d in diag], g["dct_steps"])
+    support = g["dct_support"]
+
+    def f1(found):
+        tp = np.intersect1d(found, support).size
+        return 0.0 if tp == 0 else 2 * tp / (found.size + support.size)
+
+    lone = [f1(np.flatnonzero(run_cofem(t, cfg)[0].alpha < 1e6)) for t in tasks]
+    assert f1(np.flatnonzero(st.alpha < 1e6)) + 1e-12 >= np.mean(lone)
+
+
+def test_multitask_rejects_nonneg_and_mismatch():
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    g = golden("multitask.npz")
+    prob = _multitask_golden_tasks(g, "dense")[0]
+    with pytest.raises(ValueError, match="standard"):
+        run_cofem_multitask(MultiTaskProblem((prob,)), CofemConfig(variant="nonneg"))

@@ -145,3 +145,42 @@ def test_dct2_oracle_and_mask_generator():
     np.testing.assert_allclose(PartialDct2Operator(n, mask).column_sq_norms(), op.col_sq_norms(), atol=1e-12)
     with pytest.raises(ValueError, match="distinct"):
         PartialDct2Operator(4, np.array([1, 1]))
+
+
+def test_multitask_validation_before_any_device_work():
+    from paper_2105_10439_b200 import MultiTaskProblem, run_cofem_multitask
+
+    prob = SblProblem(np.ones(4), DenseOperator(np.ones((4, 8))), 1e4)
+    with pytest.raises(ValueError, match="standard"):
+        run_cofem_multitask(MultiTaskProblem((prob,)), CofemConfig(variant="nonneg"))
+    with pytest.raises(ShapeMismatchError):
+        MultiTaskProblem((prob, SblProblem(np.ones(4), DenseOperator(np.ones((4, 9))), 1e4)))
+
+
+def test_dct_step_sensitivity_is_a_reference_property():
+    """The reference recursion (oracle, bit-exact with it) on the undersampled
+    DCT workload of test_cofem.py:257-265 changes its CG step counts when Phi is
+    rounded to the device's 32-bit fixed-point representation -- the basis of
+    the step tolerance in test_gpu_parity.assert_dct_steps_close."""
+    from scipy.fft import idct
+
+    from conftest import golden
+
+    g = golden("reference_workloads.npz")
+    phi = idct(np.eye(1024), axis=0, norm="ortho")[np.sort(g["dct_mask"]), :]
+    cfg = O.CofemConfig(iterations=3, probes=20, seed=0)
+    _, _, _, exact = O.run_cofem(O.dense_op(phi), g["dct_y"], float(g["dct_beta"]), cfg)
+    _, _, _, quant = O.run_cofem(O.dense_op(O.ozaki_dictionary(phi)), g["dct_y"], float(g["dct_beta"]), cfg)
+    assert [d["cg_steps"] for d in exact] == list(g["dct_steps"][:3])
+    assert [d["cg_steps"] for d in quant][1] > [d["cg_steps"] for d in exact][1]
+    assert np.abs(O.ozaki_dictionary(phi) - phi).max() <= 2.0**-31
+
+
+def test_ozaki_model_is_close_to_exact():
+    rng = np.random.default_rng(3)
+    phi = rng.standard_normal((40, 70)).astype(np.float32).astype(np.float64)
+    op = O.ozaki_op(phi)
+    V = rng.standard_normal((70, 5))
+    U = rng.standard_normal((40, 5))
+    assert np.abs(op.apply(V) - phi @ V).max() <= 1e-8 * np.abs(phi @ V).max()
+    assert np.abs(op.adjoint(U) - phi.T @ U).max() <= 1e-8 * np.abs(phi.T @ U).max()

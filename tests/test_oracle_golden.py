@@ -156,3 +156,25 @@ def test_oracle_reference_workloads():
     alpha, mu, s, diag = O.run_cofem(O.dense_op(g["d64_phi"]), g["d64_y"], 1e4, cfg)
     np.testing.assert_array_equal(mu, g["d64_mu"])
     np.testing.assert_array_equal(alpha, g["d64_alpha"])
+
+
+def test_oracle_multitask_matches_reference():
+    """run_cofem_multitask (cofem.py:160-214): the shared-support DCT tasks of
+    test_cofem.py:295-320 and three dense tasks with shared probes."""
+    g = golden("multitask.npz")
+    ops = [O.dct_op(256, g[f"dct_mask{l}"]) for l in range(3)]
+    cfg = O.CofemConfig(iterations=30, probes=20, seed=42)
+    alpha, ests, diag = O.run_cofem_multitask(ops, [g[f"dct_y{l}"] for l in range(3)], 1e4, cfg)
+    np.testing.assert_array_equal(alpha, g["dct_alpha"])
+    for l, (mu, s) in enumerate(ests):
+        np.testing.assert_array_equal(mu, g[f"dct_mu{l}"])
+        np.testing.assert_array_equal(s, g[f"dct_s{l}"])
+    assert [d["cg_steps"] for d in diag] == list(g["dct_steps"])
+    ops = [O.dense_op(g[f"dense_phi{l}"].astype(np.float64)) for l in range(3)]
+    cfg = O.CofemConfig(iterations=6, probes=12, seed=3, cg=O.CgConfig(max_steps=400, tolerance=1e-5))
+    alpha, ests, diag = O.run_cofem_multitask(ops, [g[f"dense_y{l}"] for l in range(3)], 1e4, cfg,
+                                              share_probes=True)
+    np.testing.assert_array_equal(alpha, g["dense_alpha"])
+    for l, (mu, s) in enumerate(ests):
+        np.testing.assert_array_equal(mu, g[f"dense_mu{l}"])
+    assert [d["cg_steps"] for d in diag] == list(g["dense_steps"])
