@@ -14,7 +14,7 @@ from ctypes import POINTER, c_double, c_float, c_int, c_int8, c_int32, c_int64, 
 import numpy as np
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libcofem_b200.so")
+LIB_PATH = os.environ.get("COFEM_LIB") or os.path.join(LIB_DIR, "libcofem_b200.so")  # override: profiling variants
 
 COFEM_OK = 0
 COFEM_EINVAL = -1

@@ -110,6 +110,23 @@ int encode_u8_3d(CUtensorMap* m, void* ptr, uint64_t d0, uint64_t d1, uint64_t d
   return 0;
 }
 
+// K-blocked operand planes [k_pad / 64][4][ncols][64] (oz::kb_offset), box {64, box_cols, 4, 1}
+int encode_u8_kblocked(CUtensorMap* m, void* ptr, uint64_t k_pad, uint64_t ncols, uint32_t box_cols) {
+  if (!g_encode) {
+    int rc = encode_u8_3d(m, ptr, 64, 8, 1, 64, 8, 1);  // resolves the driver entry point
+    if (rc) return rc;
+  }
+  cuuint64_t dims[4] = {64, ncols, 4, k_pad / 64};
+  cuuint64_t strides[3] = {64, 64 * ncols, 256 * ncols};
+  cuuint32_t box[4] = {64, box_cols, 4, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COFEM_ECUDA, "cuTensorMapEncodeTiled (4d) failed: " + std::to_string((int)r));
+  return 0;
+}
+
 // ---- contraction configurations -------------------------------------------
 // fp32: 4 rows (fwd) / 4 columns (bwd) x QP accumulators per thread
 // fp64: 2 x QP double accumulators per thread
@@ -166,7 +183,7 @@ struct cofem_ctx {
   bool oz_ready = false;
   int8_t* phiq = nullptr;        // [4][Np][Dp] signed digit planes
   double *rowscale = nullptr, *colscale = nullptr;  // Np, Dp powers of two
-  int8_t *pq = nullptr, *vq = nullptr;              // operand planes [4][QW][Dp] / [4][QW][Np]
+  int8_t *pq = nullptr, *vq = nullptr;              // operand planes, K-blocked [Dp/64][4][QW][64] / [Np/64][...]
   double* opscale = nullptr;                        // QCHUNK column scales
   unsigned long long* colmax = nullptr;             // P column maxima (up to 1024 columns)
   unsigned long long* vcolmax = nullptr;            // V column maxima (QCHUNK)
@@ -349,7 +366,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
     CK(cudaMalloc(&c->wq, (size_t)4 * nc * n));
     CK(cudaMalloc(&c->wscale, nc * sizeof(double)));
     CK(cudaMalloc(&c->wcolmax, nc * sizeof(unsigned long long)));
-    CKR(encode_u8_3d(&c->map_w, c->wq, n, nc, 4, oz::KT, 32, 4));
+    CKR(encode_u8_kblocked(&c->map_w, c->wq, n, nc, 32));
     c->map_w_ldq = ldq;
   }
   c->ldq = ldq;
@@ -495,7 +512,7 @@ int oz_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, con
   CKR(ensure_oz(c));
   const int slot = QW / 8;
   if (!c->map_p_ok[slot]) {
-    CKR(encode_u8_3d(&c->map_p[slot], c->pq, c->Dp, QW, 4, oz::KT, QW, 4));
+    CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
     c->map_p_ok[slot] = true;
   }
   // P's column maxima come fused out of k_direction inside a PCG solve; the
@@ -518,7 +535,7 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   CKR(ensure_oz(c));
   const int slot = QW / 8;
   if (!c->map_v_ok[slot]) {
-    CKR(encode_u8_3d(&c->map_v[slot], c->vq, c->Np, QW, 4, oz::KT, QW, 4));
+    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
     c->map_v_ok[slot] = true;
   }
   CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->rowscale, c->vq, c->vcolmax, c->v_colmax_valid,
@@ -558,7 +575,7 @@ int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, c
   CKR(oz_init_kernels<QW>());
   const int slot = QW / 8;
   if (!c->map_p_ok[slot]) {
-    CKR(encode_u8_3d(&c->map_p[slot], c->pq, c->Dp, QW, 4, oz::KT, QW, 4));
+    CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
     c->map_p_ok[slot] = true;
   }
   CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
@@ -587,7 +604,7 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   CKR(oz_init_kernels<QW>());
   const int slot = QW / 8;
   if (!c->map_v_ok[slot]) {
-    CKR(encode_u8_3d(&c->map_v[slot], c->vq, c->Np, QW, 4, oz::KT, QW, 4));
+    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
     c->map_v_ok[slot] = true;
   }
   CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,

@@ -11,7 +11,7 @@
 // Layouts (ldq = padded column count, Q images side by side):
 //   PCG block  P[(i n + j) ldq + q]                 (pixel-major, as every block)
 //   stage buffers B[r][(h ldq + q)], r, h < n        (n x n ldq row-major)
-//   operand planes [4][n ldq][n]: column c = h ldq + q, K index t
+//   operand planes K-blocked [n / 64][4][n ldq][64] (oz::kb_offset): column c = h ldq + q, K index t
 // Operand element (t, c = h ldq + lo) lives at src[t st + h sh + lo].
 #pragma once
 #include "ozaki.cuh"
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256)
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
-          *reinterpret_cast<uint32_t*>(planes + ((int64_t)a * NC + c0 + cc) * K + t0 + quad * 4) = word[a];
+          *reinterpret_cast<uint32_t*>(planes + oz::kb_offset(NC, a, c0 + cc, t0 + quad * 4)) = word[a];
       }
     }
   }

@@ -18,7 +18,8 @@
 // Phi^T V (BWD): A = digit plane, MN-major (m = j, k = i), TMA boxes {64 j, 64 i, 4} x 2
 // B (both): operand digit planes [4][QW][K], K-major, TMA box {64 k, QW, 4}
 // SWIZZLE_64B everywhere; 5-stage TMA -> smem ring; persistent CTAs
-// (warp 0 TMA producer, warp 1 MMA issuer, warps 2..5 TMEM epilogue).
+// (warp 0 TMA producer, warp 1 MMA issuer, warps 2..9 TMEM epilogue: warp w
+// reads lane quarter w % 4, and the 8-column groups of parity (w - 2) / 4).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -29,10 +30,17 @@
 namespace cofem {
 namespace oz {
 
+#ifndef OZ_VARIANT
+// band_kernel timing builds (scratch/build_variants.sh; results in DESIGN.md):
+// 1 = no MMAs, 2 = epilogue without math / stores, 3 = no epilogue,
+// 4 = no epilogue and no operand loads (pure MMA), 5 = no operand loads
+#define OZ_VARIANT 0
+#endif
 constexpr int KT = 64;           // K bytes per stage (one SWIZZLE_64B row)
 constexpr int BM = 128;          // output rows per tile (UMMA M)
 constexpr int STAGES = 5;
-constexpr int NTHREADS = 192;    // 6 warps
+constexpr int EPI_WARPS = 8;     // two epilogue warps per TMEM lane quarter (column halves)
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int A_STAGE = 4 * BM * KT;  // 32 KB: four digit planes
 constexpr double SCALE30 = 1073741824.0;  // 2^30
 
@@ -61,6 +69,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+// operand planes live K-blocked in HBM: [k / 64][4 planes][ncols][64 k], so
+// the {64 k, QW cols, 4 planes} box of one stage is 4 contiguous runs of 64 QW
+// bytes (not 4 QW rows of 64 B a whole column apart); c3 = k / 64
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// byte offset of digit plane a, column col, K index k in the K-blocked layout
+__host__ __device__ __forceinline__ int64_t kb_offset(int64_t ncols, int a, int64_t col, int64_t k) {
+  return ((((k >> 6) * 4 + a) * ncols + col) << 6) + (k & 63);
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -156,11 +179,15 @@ __device__ __forceinline__ void tmem_zero_all(uint32_t tmem, int quarter) {
 // per-column maxima of |out| in registers (bit patterns of non-negative
 // doubles order like unsigned integers, NaN above everything); they are
 // folded across the warp and the CTA once, at the end of the kernel.
-template <int QW, bool TRACK>
+template <int QW, bool TRACK, int HALF>
 __device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, const double* __restrict__ op_scale,
                                              double* o, unsigned long long (&cm)[QW]) {
 #pragma unroll
-  for (int q0 = 0; q0 < QW; q0 += 8) {
+  for (int q0 = HALF * 8; q0 < QW; q0 += 16) {
+    // scale * op_scale: both powers of two, so the products below are exact
+    double f[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) f[t] = scale * __ldg(op_scale + q0 + t);
     uint32_t r[5][8];
 #pragma unroll
     for (int sb = 0; sb < 5; ++sb)
@@ -180,18 +207,32 @@ __device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, c
       // value = 2^16 (S0 2^32 + S1 2^24 + S2 2^16 + S3 2^8 + S4), |S1 2^24 + ...| < 2^57
       const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
                            ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
-      const double val = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * 65536.0;
-      v[t] = val * scale * op_scale[q0 + t];
+      v[t] = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * f[t];
     }
 #pragma unroll
     for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + q0 + t) = make_double2(v[t], v[t + 1]);
     if (TRACK) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const unsigned long long m = (unsigned long long)__double_as_longlong(fabs(v[t]));
+        // |v| as a bit pattern: clear the sign bit on the integer side (no FP64 op)
+        const unsigned long long m = (unsigned long long)__double_as_longlong(v[t]) & 0x7fffffffffffffffull;
         cm[q0 + t] = m > cm[q0 + t] ? m : cm[q0 + t];
       }
     }
+  }
+}
+
+// the calling epilogue warp's share of one tile row (column groups of parity half)
+template <int QW>
+__device__ __forceinline__ void epilogue_part(int half, bool track, uint32_t tset_lane, double scale,
+                                              const double* __restrict__ op_scale, double* o,
+                                              unsigned long long (&cm)[QW]) {
+  if (half == 0) {
+    if (track) epilogue_row<QW, true, 0>(tset_lane, scale, op_scale, o, cm);
+    else epilogue_row<QW, false, 0>(tset_lane, scale, op_scale, o, cm);
+  } else {
+    if (track) epilogue_row<QW, true, 1>(tset_lane, scale, op_scale, o, cm);
+    else epilogue_row<QW, false, 1>(tset_lane, scale, op_scale, o, cm);
   }
 }
 
@@ -245,7 +286,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(tmem_holder + 2);  // [4 warps][QW]
+  // [EPI_WARPS][QW] column maxima, folded after the last tile: aliases the
+  // stage ring, which every MMA has finished reading by then
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(sm);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -255,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&map_a);
@@ -271,7 +314,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_holder;
-  if (warp >= 2) tmem_zero_all(tmem, warp & 3);
+  if (warp >= 2 && warp < 6) tmem_zero_all(tmem, warp & 3);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -298,7 +341,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_3d(sa, &map_a, &full[stage], mb * BM, k, 0);
             tma_load_3d(sa + A_STAGE / 2, &map_a, &full[stage], mb * BM + 64, k, 0);
           }
-          tma_load_3d(sb, &map_b, &full[stage], k, nc * QW, 0);
+          tma_load_4d(sb, &map_b, &full[stage], 0, nc * QW, 0, k >> 6);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -339,8 +382,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
-    // ---------------- epilogue: warps 2..5 -> TMEM lane quarters (warp % 4) ----------------
-    const int quarter = warp & 3;
+    // ---------------- epilogue: warps 2..9 -> TMEM lane quarter warp % 4, column half ----------------
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
     unsigned long long cm[QW];
 #pragma unroll
@@ -349,17 +392,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
       const int mb = w % n_mblocks, s = (w / n_mblocks) % n_split, nc = w / (n_mblocks * n_split);
       const int buf = it & 1;
+      const int64_t row = (int64_t)mb * BM + row_in_tile;
+      // the row scale load is issued before the wait so its latency hides behind the MMAs
+      const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int64_t row = (int64_t)mb * BM + row_in_tile;
-      const double scale = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
       double* orow = out + ((int64_t)s * out_rows + row) * out_ld + nc * QW;
-      if (out_colmax)
-        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale,
-                               op_scale + nc * QW, orow, cm);
-      else
-        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale,
-                                op_scale + nc * QW, orow, cm);
+      epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16),
+                        scale, op_scale + nc * QW, orow, cm);
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[buf]);
@@ -370,7 +410,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (out_colmax && threadIdx.x < QW) {
     unsigned long long m = cmax[threadIdx.x];
-    for (int w = 1; w < 4; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
+    for (int w = 1; w < EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
     atomicMax(&out_colmax[threadIdx.x], m);
   }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -409,7 +449,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* tfull = band_full + 1;  // [2]
   uint64_t* tempty = tfull + 2;     // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(tmem_holder + 2);  // [4 warps][QW]
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);  // [EPI_WARPS][QW], after the last tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -420,7 +460,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(band_full, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 32 * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&map_a);
@@ -436,7 +476,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_holder;
-  if (warp >= 2) tmem_zero_all(tmem, warp & 3);
+  if (warp >= 2 && warp < 6) tmem_zero_all(tmem, warp & 3);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -452,8 +492,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int k0 = mb * BM + band_offset;
         for (int s = 0; s < nst; ++s) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], BC::B_STAGE);
-          tma_load_3d(ring + stage * BC::B_STAGE, &map_b, &full[stage], k0 + s * KT, 0, 0);
+          if (OZ_VARIANT >= 4) {
+            mbar_arrive(&full[stage]);  // timing variants: no operand loads
+          } else {
+            mbar_expect_tx(&full[stage], BC::B_STAGE);
+            tma_load_4d(ring + stage * BC::B_STAGE, &map_b, &full[stage], 0, 0, 0, (k0 + s * KT) >> 6);
+          }
           if (++stage == BSTAGES) {
             stage = 0;
             phase ^= 1;
@@ -476,8 +520,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int s = 0; s < nst; ++s) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          issue_stage<QW, false>(smem_u32(band + (size_t)s * A_STAGE), smem_u32(ring + stage * BC::B_STAGE), tset,
-                                 idesc0);
+          if (OZ_VARIANT != 1)
+            issue_stage<QW, false>(smem_u32(band + (size_t)s * A_STAGE), smem_u32(ring + stage * BC::B_STAGE), tset,
+                                   idesc0);
           mma_commit(&empty[stage]);
           if (++stage == BSTAGES) {
             stage = 0;
@@ -488,7 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
     unsigned long long cm[QW];
 #pragma unroll
@@ -496,16 +541,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
       const int buf = it & 1;
+      const int64_t row = (int64_t)mb * BM + row_in_tile;
+      const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const int64_t row = (int64_t)mb * BM + row_in_tile;
-      const double scale = row < rows_real ? row_scale[row] * (1.0 / (SCALE30 * SCALE30)) : 0.0;
-      if (out_colmax)
-        epilogue_row<QW, true>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
-                               out + row * QW, cm);
-      else
-        epilogue_row<QW, false>(tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16), scale, op_scale,
-                                out + row * QW, cm);
+      if (OZ_VARIANT == 2) {
+        uint32_t r[5][8];
+        const uint32_t tl = tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16);
+        for (int q0 = half * 8; q0 < QW; q0 += 16) {
+          for (int sb = 0; sb < 5; ++sb)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]),
+                           "=r"(r[sb][5]), "=r"(r[sb][6]), "=r"(r[sb][7])
+                         : "r"(tl + sb * QW + q0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          for (int sb = 0; sb < 5; ++sb)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
+                         "r"(0));
+          if (r[0][0] == 0x12345 && scale == 3.0) out[row] = 1.0;
+        }
+      } else if (OZ_VARIANT != 3 && OZ_VARIANT != 4)
+        epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16),
+                          scale, op_scale, out + row * QW, cm);
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[buf]);
@@ -516,7 +573,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (out_colmax && threadIdx.x < QW) {
     unsigned long long m = cmax[threadIdx.x];
-    for (int w = 1; w < 4; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
+    for (int w = 1; w < EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
     atomicMax(&out_colmax[threadIdx.x], m);
   }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -621,7 +678,7 @@ __global__ void __launch_bounds__(256)
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-        *reinterpret_cast<uint32_t*>(planes + ((int64_t)a * QW + q) * k_pad + k0 + quad * 4) = word[a];
+        *reinterpret_cast<uint32_t*>(planes + kb_offset(QW, a, q, k0 + quad * 4)) = word[a];
     }
   }
 }
