@@ -457,8 +457,8 @@ int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int
                                                                              st);
     c->launches++;
   }
-  const int64_t ntile = k_pad / oz::QTILE;
-  oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>(ntile, 4 * c->sm_count), 256, 0, c->stream>>>(
+  const int64_t nchunk = k_pad / oz::QCHUNK_K;  // one warp each, 8 warps per block
+  oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>((nchunk + 7) / 8, 16 * c->sm_count), 256, 0, c->stream>>>(
       k_real, k_pad, ldm, qoff, M, pre, colmax, c->opscale, planes, reset, st);
   c->launches++;
   CK(cudaGetLastError());

@@ -633,11 +633,14 @@ __device__ __forceinline__ double col_scale(unsigned long long bits) {
   return m == 0.0 ? 1.0 : pow2_ceil(m);
 }
 
-// Block-tiled quantisation: a 128-row x QW tile of M is staged through smem
-// with coalesced loads, then each thread packs 4 rows of one column into one
-// 32-bit word per digit plane (stores coalesced along k).  `reset` (may be
-// null) is zeroed by block 0 for the next fused column max.
-constexpr int QTILE = 128;
+// Operand quantisation, one warp per 16-row K chunk: lane q < QW owns column
+// q, loads its 16 values (each warp load is one contiguous row of the block),
+// splits them into signed base-256 digits and stores 16 K bytes per digit
+// plane (one 16-B store per plane into the K-blocked layout).  No shared
+// memory, 16 independent loads in flight per lane.  The column maxima come
+// fused out of the producing kernel.  `reset` (may be null) is zeroed by
+// block 0 for the next fused column max.
+constexpr int QCHUNK_K = 16;
 template <typename T, int QW>
 __global__ void __launch_bounds__(256)
     k_quantize(int64_t k_real, int64_t k_pad, int ldm, int qoff, const T* __restrict__ M,
@@ -645,41 +648,38 @@ __global__ void __launch_bounds__(256)
                double* __restrict__ scale_out, int8_t* __restrict__ planes, unsigned long long* __restrict__ reset,
                const Status* __restrict__ st) {
   if (st && st->done) return;
-  __shared__ double inv_s[QW];
-  __shared__ double tile[QTILE][QW + 1];
-  if (threadIdx.x < QW) {
-    const double sc = col_scale(colmax[threadIdx.x]);
-    inv_s[threadIdx.x] = SCALE30 / sc;  // NaN for a non-finite column
-    if (blockIdx.x == 0) scale_out[threadIdx.x] = sc;
-  }
+  if (blockIdx.x == 0 && threadIdx.x < QW) scale_out[threadIdx.x] = col_scale(colmax[threadIdx.x]);
   if (blockIdx.x == 0 && reset && threadIdx.x < 32) reset[threadIdx.x] = 0ull;
-  const int64_t ntile = k_pad / QTILE;
-  for (int64_t tb = blockIdx.x; tb < ntile; tb += gridDim.x) {
-    const int64_t k0 = tb * QTILE;
-    __syncthreads();
-    for (int e = threadIdx.x; e < QTILE * QW; e += blockDim.x) {
-      const int r = e / QW, q = e % QW;
+  const int lane = threadIdx.x & 31;
+  if (lane >= QW) return;
+  const double is = SCALE30 / col_scale(colmax[lane]);  // NaN for a non-finite column
+  const int64_t nchunks = k_pad / QCHUNK_K;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
+    const int64_t k0 = ch * QCHUNK_K;
+    double x[QCHUNK_K];
+#pragma unroll
+    for (int r = 0; r < QCHUNK_K; ++r) {
       const int64_t k = k0 + r;
-      tile[r][q] = (k < k_real) ? (double)M[k * ldm + qoff + q] * pre[k] : 0.0;
+      x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * __ldg(pre + k) : 0.0;
     }
-    __syncthreads();
-    for (int w = threadIdx.x; w < (QTILE / 4) * QW; w += blockDim.x) {
-      const int quad = w % (QTILE / 4), q = w / (QTILE / 4);
-      const double is = inv_s[q];
-      uint32_t word[4] = {0u, 0u, 0u, 0u};
-      if (is == is) {
+    uint32_t w[4][QCHUNK_K / 4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          int8_t d[4];
-          digits4(tile[quad * 4 + r][q] * is, d);
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int a = 0; a < 4; ++a) word[a] |= (uint32_t)(uint8_t)d[a] << (8 * r);
-        }
+      for (int j = 0; j < QCHUNK_K / 4; ++j) w[a][j] = 0u;
+    if (is == is) {
+#pragma unroll
+      for (int r = 0; r < QCHUNK_K; ++r) {
+        int8_t d[4];
+        digits4(x[r] * is, d);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) w[a][r / 4] |= (uint32_t)(uint8_t)d[a] << (8 * (r % 4));
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-        *reinterpret_cast<uint32_t*>(planes + kb_offset(QW, a, q, k0 + quad * 4)) = word[a];
     }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      *reinterpret_cast<uint4*>(planes + kb_offset(QW, a, lane, k0)) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
   }
 }
 
