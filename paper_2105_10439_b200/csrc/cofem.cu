@@ -203,12 +203,9 @@ struct cofem_ctx {
   int dct_n = 0;
   int64_t* dct_mask = nullptr;      // N flat coefficient indices k n + l
   uint8_t* dct_grid = nullptr;      // n x n 0/1 mask grid
-  double *bufA = nullptr, *bufB = nullptr;  // n x n ldq stage buffers
-  int8_t* wq = nullptr;             // operand digit planes [4][n ldq][n]
-  double* wscale = nullptr;         // n ldq column scales
-  unsigned long long* wcolmax = nullptr;
-  CUtensorMap map_w{};
-  int map_w_ldq = 0;
+  double *bufA = nullptr, *bufB = nullptr;  // n x n ldq pass buffers
+  double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n}
+  double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
   // multi-GPU
   ncclComm_t comm = nullptr;
@@ -360,14 +357,6 @@ int ensure_ws(cofem_ctx* c, int ldq) {
       CK(cudaMalloc(b, (size_t)n * nc * sizeof(double)));
       CK(cudaMemset(*b, 0, (size_t)n * nc * sizeof(double)));
     }
-    if (c->wq) cudaFree(c->wq);
-    if (c->wscale) cudaFree(c->wscale);
-    if (c->wcolmax) cudaFree(c->wcolmax);
-    CK(cudaMalloc(&c->wq, (size_t)4 * nc * n));
-    CK(cudaMalloc(&c->wscale, nc * sizeof(double)));
-    CK(cudaMalloc(&c->wcolmax, nc * sizeof(unsigned long long)));
-    CKR(encode_u8_kblocked(&c->map_w, c->wq, n, nc, 32));
-    c->map_w_ldq = ldq;
   }
   c->ldq = ldq;
   return 0;
@@ -629,74 +618,80 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   return 0;
 }
 
-// ---- 2-D partial DCT: four ozaki stages against the n x n DCT matrix --------
-// one stage: quantise the stacked operand columns (h, q) of src (element
-// (t, h ldq + q) at src[t st + h sh + q]) and contract with C (bwd: C^T)
-int dct_stage(cofem_ctx* c, const double* src, int64_t st, int64_t sh, const double* pre, bool bwd,
-              const double* row_scale, double* out, const Status* stt) {
-  CKR(oz_init_kernels<32>());
-  const int n = c->dct_n, ldq = c->ldq, nc = n * ldq;
-  dct::k_cq_quantize<<<nc / dct::TC, 256, 0, c->stream>>>(n, nc, ldq, st, sh, src, pre, c->wscale, c->wq, stt);
-  const int nmb = n / oz::BM, items = nmb * (nc / 32);
-  const int grid = std::min(items, c->sm_count);
+// ---- 2-D partial DCT: fused float64 FFT passes (dct.cuh) ------------------
+// pass over an n x n x ldq block; row passes run along j (outer i), column
+// passes along i (outer j / l)
+template <int N1, int N2, int MODE>
+void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+  const int64_t n = c->dct_n, ldq = c->ldq;
+  constexpr int NT = 4 * N2;
+  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dctf::k_dct_pass<N1, N2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int items = (int)(n * (ldq / 8));
+  int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));  // blocks that fit one SM's shared memory
+  if (per_sm > 16) per_sm = 16;
+  const int grid = std::min(items, per_sm * c->sm_count);
+  dctf::k_dct_pass<N1, N2, MODE><<<grid, NT, smem, c->stream>>>(
+      src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / 8), c->dct_wN, c->dct_tw, c->dct_cn,
+      c->dct_grid, stt);
+  c->launches++;
+}
+
+template <int MODE>
+int dct_pass(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+  switch (c->dct_n) {
+    case 64: dct_pass_t<8, 8, MODE>(c, src, dst, rows, stt); break;
+    case 128: dct_pass_t<8, 16, MODE>(c, src, dst, rows, stt); break;
+    case 256: dct_pass_t<16, 16, MODE>(c, src, dst, rows, stt); break;
+    case 512: dct_pass_t<16, 32, MODE>(c, src, dst, rows, stt); break;
+    case 1024: dct_pass_t<32, 32, MODE>(c, src, dst, rows, stt); break;
+    default: return fail(COFEM_EINVAL, "unsupported DCT image side");
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// bufB <- coefficient grid Y[(k n + l) ldq + q] = DCT2 of every column image of P
+int dct_forward_dev(cofem_ctx* c, const double* P, const Status* stt) {
+  CKR((dct_pass<dctf::P_FWD>(c, P, c->bufA, true, stt)));
+  return dct_pass<dctf::P_FWD>(c, c->bufA, c->bufB, false, stt);
+}
+
+// out <- DCT2^T of the coefficient grid in bufB
+int dct_adjoint_dev(cofem_ctx* c, double* out, const Status* stt) {
+  CKR((dct_pass<dctf::P_INV>(c, c->bufB, c->bufA, false, stt)));
+  return dct_pass<dctf::P_INV>(c, c->bufA, out, true, stt);
+}
+
+// Psi = beta Phi^T Phi P + alpha .* P for all ldq columns at once, pi on the
+// fly: row DCT-II, fused column DCT-II / mask / DCT-III, row DCT-III + combine
+int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
+  CKR((dct_pass<dctf::P_FWD>(c, (const double*)c->P, c->bufA, true, stt)));
+  cudaEvent_t e0 = nullptr;
   if (c->time_kernels) {
-    cudaEvent_t e0 = next_event(c);
+    e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  if (!bwd)
-    oz::contract_kernel<32, oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<32>::SMEM, c->stream>>>(
-        c->map_phi_fwd, c->map_w, nmb, items, n, n, 0, row_scale, c->wscale, out, n, n, nullptr, stt, 1, nc);
-  else
-    oz::contract_kernel<32, oz::MODE_BWD><<<grid, oz::NTHREADS, oz::Cfg<32>::SMEM, c->stream>>>(
-        c->map_phi_bwd, c->map_w, nmb, items, n, n, 0, row_scale, c->wscale, out, n, n, nullptr, stt, 1, nc);
+  CKR((dct_pass<dctf::P_FMI>(c, c->bufA, c->bufB, false, stt)));
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
-    c->timed.push_back({bwd ? 1 : 0, c->evnext - 2});
+    c->timed.push_back({0, c->evnext - 2});
+    c->fwd_launches++;
   }
-  c->launches += 2;
-  if (bwd) c->bwd_launches++;
-  else c->fwd_launches++;
-  CK(cudaGetLastError());
-  return 0;
-}
-
-// bufB <- Y^T = (C X C^T)^T for every column image of P (pixel-major D x ldq)
-int dct_forward_dev(cofem_ctx* c, const double* P, const Status* stt) {
-  const int64_t n = c->dct_n, ldq = c->ldq;
-  CKR(dct_stage(c, P, n * ldq, ldq, c->colscale, false, c->rowscale, c->bufA, stt));       // W = C X
-  return dct_stage(c, c->bufA, ldq, n * ldq, c->colscale, false, c->rowscale, c->bufB, stt);  // Y^T = C W^T
-}
-
-// bufB (U^T, masked coefficients) <- Z^T = (C^T U C)^T
-int dct_adjoint_dev(cofem_ctx* c, const Status* stt) {
-  const int64_t n = c->dct_n, ldq = c->ldq;
-  CKR(dct_stage(c, c->bufB, ldq, n * ldq, c->rowscale, true, c->colscale, c->bufA, stt));  // T = C^T U
-  return dct_stage(c, c->bufA, ldq, n * ldq, c->rowscale, true, c->colscale, c->bufB, stt);  // Z^T = C^T T^T
-}
-
-int dct_finish(cofem_ctx* c, double* out, const Status* stt) {
-  const int ldq = c->ldq;
-  dct::k_finish<<<8 * c->sm_count, 256, dct::FJ * dct::FI * ldq * sizeof(double), c->stream>>>(c->dct_n, ldq, c->bufB,
-                                                                                             out, stt);
-  c->launches++;
-  CK(cudaGetLastError());
-  return 0;
-}
-
-// Psi = beta Phi^T Phi P + alpha .* P for all ldq columns at once, pi on the fly
-int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
-  CKR(dct_forward_dev(c, (const double*)c->P, stt));
-  const int64_t total = (int64_t)c->dct_n * c->dct_n * c->ldq;
-  dct::k_apply_mask<<<(int)std::min<int64_t>((total + 255) / 256, 16 * c->sm_count), 256, 0, c->stream>>>(
-      c->dct_n, c->ldq, c->bufB, c->dct_grid, stt);
-  c->launches++;
-  CKR(dct_adjoint_dev(c, stt));
-  CKR(dct_finish(c, (double*)c->ppart, stt));
+  (void)e0;
+  // the row DCT-III writes Z; Psi = beta Z + alpha .* P and pi in the streaming
+  // combine (fusing it into the pass stalls the FFT pipeline on the P loads)
+  CKR((dct_pass<dctf::P_INV>(c, c->bufB, c->bufA, true, stt)));
   Scalars sc = c->sc();
   const int bs = elem_block(c->ldq);
   k_combine<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
-      c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->ppart, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
+      c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->bufA, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
       stt);
   c->launches++;
   CK(cudaGetLastError());
@@ -1062,11 +1057,10 @@ int ldq_for(int64_t q) { return (int)round_up(std::max<int64_t>(q, 1), 8); }
 int dct_adjoint_from_V(cofem_ctx* c) {
   const int64_t n = c->dct_n, ldq = c->ldq;
   CK(cudaMemsetAsync(c->bufB, 0, (size_t)n * n * ldq * sizeof(double), c->stream));
-  dct::k_scatter<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, (int)n, (int)ldq, c->dct_mask, (const double*)c->V,
-                                                         c->bufB);
+  dctf::k_scatter<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, (int)ldq, c->dct_mask, (const double*)c->V,
+                                                          c->bufB);
   c->launches++;
-  CKR(dct_adjoint_dev(c, nullptr));
-  return dct_finish(c, (double*)c->tmpD, nullptr);
+  return dct_adjoint_dev(c, (double*)c->tmpD, nullptr);
 }
 
 template <typename T>
@@ -1076,7 +1070,7 @@ int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
   CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
   if (c->kind == 2) {
     CKR(dct_forward_dev(c, (const double*)c->P, nullptr));
-    dct::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, c->dct_n, ldq, c->dct_mask, c->bufB, (double*)c->V);
+    dctf::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, ldq, c->dct_mask, c->bufB, (double*)c->V);
     c->launches++;
     CK(cudaGetLastError());
     return download_block<T>(c, c->V, c->N, q, ldq, 0, out);
@@ -1553,9 +1547,10 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
 int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision) {
   if (!out || !mask) return fail(COFEM_EINVAL, "null argument");
   *out = nullptr;
-  if (n < 128 || n % 128 != 0 || n > 8192) return fail(COFEM_EINVAL, "image side must be a multiple of 128 in [128, 8192]");
+  if (n < 64 || n > 1024 || (n & (n - 1)) != 0) return fail(COFEM_EINVAL, "image side must be a power of two in [64, 1024]");
   if (nmask < 1 || nmask > n * n) return fail(COFEM_EINVAL, "need 1 <= mask size <= n^2");
-  if (precision != COFEM_OZAKI) return fail(COFEM_EINVAL, "2-D DCT dictionaries run in OZAKI precision");
+  if (precision != COFEM_OZAKI && precision != COFEM_FP64)
+    return fail(COFEM_EINVAL, "2-D DCT dictionaries run in FP64 (fused FFT passes; OZAKI is accepted as an alias)");
   std::vector<uint8_t> grid((size_t)n * n, 0);
   for (int64_t m = 0; m < nmask; ++m) {
     if (mask[m] < 0 || mask[m] >= n * n) return fail(COFEM_EINVAL, "mask indices must lie in [0, n^2)");
@@ -1565,7 +1560,7 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   cofem_ctx* c = new cofem_ctx();
   c->kind = 2;
   c->device = device;
-  c->prec = precision;
+  c->prec = COFEM_FP64;  // float64 FFT passes whatever the requested mode
   c->dct_n = (int)n;
   c->N = nmask;
   c->D = n * n;
@@ -1596,43 +1591,28 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   cudaEventCreate(&c->t1);
   if (cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "colmax"));
-  // the n x n orthonormal DCT-II matrix C[k][i] = c_k cos(pi (2 i + 1) k / (2 n)) as digit planes
-  std::vector<double> C((size_t)n * n), rs(n), cs(n);
-  for (int64_t k = 0; k < n; ++k) {
-    const double ck = k == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n);
-    for (int64_t i = 0; i < n; ++i) C[k * n + i] = ck * std::cos(M_PI * (2.0 * i + 1.0) * k / (2.0 * n));
+  // FFT tables: w_n^j = e^{-2 pi i j / n}, Makhoul twiddles e^{-i pi k / 2n},
+  // orthonormal scales c_k; the register DFTs' e^{-2 pi i j / 64} in __constant__
+  std::vector<double2> wN(n), tw(n), w64(64);
+  std::vector<double> cn(n);
+  for (int64_t j = 0; j < n; ++j) {
+    wN[j] = make_double2(std::cos(2.0 * M_PI * j / n), -std::sin(2.0 * M_PI * j / n));
+    tw[j] = make_double2(std::cos(M_PI * j / (2.0 * n)), -std::sin(M_PI * j / (2.0 * n)));
+    cn[j] = j == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n);
   }
-  for (int64_t k = 0; k < n; ++k) {
-    double m = 0.0;
-    for (int64_t i = 0; i < n; ++i) m = std::max(m, std::fabs(C[k * n + i]));
-    rs[k] = host_pow2_ceil(m);
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    double m = 0.0;
-    for (int64_t k = 0; k < n; ++k) m = std::max(m, std::fabs(C[k * n + i]) / rs[k]);
-    cs[i] = host_pow2_ceil(m);
-  }
-  std::vector<int8_t> planes((size_t)4 * n * n);
-  for (int64_t k = 0; k < n; ++k)
-    for (int64_t i = 0; i < n; ++i) {
-      int8_t d[4];
-      host_digits4(C[k * n + i] / (rs[k] * cs[i]) * 1073741824.0, d);
-      for (int a = 0; a < 4; ++a) planes[((size_t)a * n + k) * n + i] = d[a];
-    }
-  if (cudaMalloc(&c->phiq, planes.size()) != cudaSuccess || cudaMalloc(&c->rowscale, n * sizeof(double)) ||
-      cudaMalloc(&c->colscale, n * sizeof(double)) || cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) ||
+  for (int j = 0; j < 64; ++j) w64[j] = make_double2(std::cos(2.0 * M_PI * j / 64), -std::sin(2.0 * M_PI * j / 64));
+  if (cudaMalloc(&c->dct_wN, n * sizeof(double2)) || cudaMalloc(&c->dct_tw, n * sizeof(double2)) ||
+      cudaMalloc(&c->dct_cn, n * sizeof(double)) || cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) ||
       cudaMalloc(&c->dct_grid, grid.size()))
-    return bail(fail(COFEM_ENOMEM, "DCT planes"));
-  cudaMemcpy(c->phiq, planes.data(), planes.size(), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->rowscale, rs.data(), n * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->colscale, cs.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+    return bail(fail(COFEM_ENOMEM, "DCT tables"));
+  cudaMemcpy(c->dct_wN, wN.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->dct_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  cudaMemcpy(c->dct_cn, cn.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpyToSymbol(dctf::c_w64, w64.data(), 64 * sizeof(double2));
   std::vector<int64_t> sorted(mask, mask + nmask);
   std::sort(sorted.begin(), sorted.end());
   cudaMemcpy(c->dct_mask, sorted.data(), nmask * sizeof(int64_t), cudaMemcpyHostToDevice);
   cudaMemcpy(c->dct_grid, grid.data(), grid.size(), cudaMemcpyHostToDevice);
-  int rc = encode_u8_3d(&c->map_phi_fwd, c->phiq, n, n, 4, oz::KT, oz::BM, 4);
-  if (!rc) rc = encode_u8_3d(&c->map_phi_bwd, c->phiq, n, n, 4, 64, oz::KT, 4);
-  if (rc) return bail(rc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
@@ -1649,7 +1629,7 @@ int cofem_destroy(cofem_ctx* c) {
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
                   c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
-                  c->dct_mask, c->dct_grid, c->bufA, c->bufB, c->wq, c->wscale, c->wcolmax};
+                  c->dct_mask, c->dct_grid, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

@@ -1,152 +1,259 @@
-// dct.cuh -- 2-D partial-DCT dictionaries (BASELINE config 4) on the int8
-// tensor-core contraction.
+// dct.cuh -- 2-D partial-DCT dictionaries (BASELINE config 4) as fused
+// float64 FFT passes.
 //
-// Phi = M * DCT2 (orthonormal 2-D DCT-II of an n x n image, then the rows of
-// the coefficient grid selected by the mask M), so Phi^T Phi P = DCT2^T (M .*
-// DCT2 P) and one PCG apply is four dense stages against the fixed n x n DCT
-// matrix C (Y = C X C^T, Z = C^T U C), each an ozaki contraction over the
-// stacked images of all Q columns.  The digit planes of C are read K-major for
-// the C stages and MN-major (C^T) for the adjoint stages -- one copy.
+// Phi = M * DCT2: orthonormal 2-D DCT-II of an n x n image, then the
+// coefficients selected by the mask M.  One PCG apply needs
+//   Psi = beta DCT2^T (M .* DCT2 P) + alpha .* P
+// for the Q = ldq column images of P at once, which is three passes over HBM:
+//   row pass    DCT-II along j                        P    -> T1
+//   column pass DCT-II along i, mask, DCT-III along i  T1   -> T2  (fused)
+//   row pass    DCT-III along j                        T2   -> Z
+// (then the streaming PCG combine Psi = beta Z + alpha .* P, pi = <P, Psi>).
+// Each pass streams one n^2 x ldq float64 block in and one out: HBM-bound,
+// O(log n) arithmetic per element (a dense C X C^T would be O(n)).
 //
-// Layouts (ldq = padded column count, Q images side by side):
-//   PCG block  P[(i n + j) ldq + q]                 (pixel-major, as every block)
-//   stage buffers B[r][(h ldq + q)], r, h < n        (n x n ldq row-major)
-//   operand planes K-blocked [n / 64][4][n ldq][64] (oz::kb_offset): column c = h ldq + q, K index t
-// Operand element (t, c = h ldq + lo) lives at src[t st + h sh + lo].
+// Every 1-D transform is Makhoul's: DCT-II of real x is Re(e^{-i pi k / 2n}
+// FFT_n(v)[k]) of the even/odd reordering v, and DCT-III inverts it with an
+// inverse FFT of e^{i pi k / 2n}(X[k] - i X[n-k]).  Two real vectors ride in
+// one complex FFT (real / imaginary part), and the length-n FFT is a
+// four-step N1 x N2 decomposition: register DFTs of size N2 and N1, one
+// twiddle multiply and two padded shared-memory transposes.
+//
+// Block layout (ldq = padded column count, Q images interleaved):
+//   P[(i n + j) ldq + q]       pixel-major, as every PCG block
+//   T1[(i n + l) ldq + q]      after the row pass (l = j frequency)
+//   Y[(k n + l) ldq + q]       coefficient grid after the column pass
+// A pass item is (outer index o, q-group of 8 columns): 4 complex FFTs.
 #pragma once
-#include "ozaki.cuh"
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "pcg.cuh"
 
 namespace cofem {
-namespace dct {
+namespace dctf {
 
-// digit planes of the columns.  One block owns a strip of 64 columns: pass 1
-// folds the column maxima (4 K-rows x 64 columns per sweep, coalesced along
-// the columns), pass 2 re-reads the strip (L2-hot) in 32 x 64 smem tiles and
-// stores one 32-bit word (4 K rows) per digit plane, coalesced along K.
-constexpr int TT = 32, TC = 64;
-__global__ void __launch_bounds__(256)
-    k_cq_quantize(int K, int NC, int ldq, int64_t st, int64_t sh, const double* __restrict__ src,
-                  const double* __restrict__ pre, double* __restrict__ scale_out, int8_t* __restrict__ planes,
-                  const Status* __restrict__ stt) {
-  if (stt && stt->done) return;
-  __shared__ double tile[TT][TC + 1];
-  __shared__ double inv_s[TC];
-  __shared__ unsigned long long red[4][TC];
-  const int ntc = NC / TC;
-  for (int strip = blockIdx.x; strip < ntc; strip += gridDim.x) {
-    const int c0 = strip * TC;
-    {
-      const int cc = threadIdx.x % TC, tt = threadIdx.x / TC;  // 4 x 64
-      const int c = c0 + cc;
-      const int64_t base = (int64_t)(c / ldq) * sh + (c % ldq);
-      double m = 0.0;
-      for (int t = tt; t < K; t += 4) {
-        const double v = fabs(src[base + (int64_t)t * st] * pre[t]);
-        m = (v > m || v != v) ? v : m;
-      }
-      __syncthreads();
-      red[tt][cc] = (unsigned long long)__double_as_longlong(m);
-      __syncthreads();
-      if (threadIdx.x < TC) {
-        unsigned long long mm = red[0][threadIdx.x];
-        for (int r = 1; r < 4; ++r) mm = red[r][threadIdx.x] > mm ? red[r][threadIdx.x] : mm;
-        const double sc = oz::col_scale(mm);
-        inv_s[threadIdx.x] = oz::SCALE30 / sc;
-        scale_out[c0 + threadIdx.x] = sc;
-      }
-    }
-    for (int t0 = 0; t0 < K; t0 += TT) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < TT * TC; e += blockDim.x) {
-        const int r = e / TC, cc = e % TC;
-        const int c = c0 + cc, t = t0 + r;
-        tile[r][cc] = src[(int64_t)t * st + (int64_t)(c / ldq) * sh + (c % ldq)] * pre[t];
-      }
-      __syncthreads();
-      for (int w = threadIdx.x; w < TC * (TT / 4); w += blockDim.x) {
-        const int quad = w % (TT / 4), cc = w / (TT / 4);
-        const double is = inv_s[cc];
-        uint32_t word[4] = {0u, 0u, 0u, 0u};
-        if (is == is) {
+__constant__ double2 c_w64[64];  // e^{-2 pi i j / 64}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+// bit reversal of the low `bits` bits; iterative so that unrolled loops fold it
+__host__ __device__ __forceinline__ constexpr int brev(int k, int bits) {
+  int r = 0;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            int8_t d[4];
-            oz::digits4(tile[quad * 4 + r][cc] * is, d);
+  for (int b = 0; b < 6; ++b)
+    if (b < bits) r |= ((k >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// In-register DFT of size R (power of two <= 64), decimation in frequency:
+// natural-order input, bit-reversed output (X[k] = x[brev(k)]).  SIGN = -1
+// forward, +1 inverse (unnormalised).
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_reg(double2 (&x)[R]) {
 #pragma unroll
-            for (int a = 0; a < 4; ++a) word[a] |= (uint32_t)(uint8_t)d[a] << (8 * r);
-          }
+  for (int s = R; s >= 2; s >>= 1) {
+#pragma unroll
+    for (int b = 0; b < R; b += s) {
+#pragma unroll
+      for (int j = 0; j < s / 2; ++j) {
+        const double2 a = x[b + j], c = x[b + j + s / 2];
+        x[b + j] = cadd(a, c);
+        const double2 d = csub(a, c);
+        if (j == 0) {
+          x[b + j + s / 2] = d;
+        } else {
+          const double2 w = c_w64[j * (64 / s)];
+          x[b + j + s / 2] = cmul(d, SIGN < 0 ? w : conj2(w));
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-          *reinterpret_cast<uint32_t*>(planes + oz::kb_offset(NC, a, c0 + cc, t0 + quad * 4)) = word[a];
       }
     }
   }
 }
 
-// U = M .* Y on the coefficient grid; the stage buffer holds Y^T as
-// [l][(k ldq + q)], the mask is the n x n 0/1 grid [k][l]
-__global__ void k_apply_mask(int n, int ldq, double* __restrict__ buf, const uint8_t* __restrict__ grid,
-                             const Status* __restrict__ stt) {
+// Length-N (= N1 N2) FFT of one region z (natural order in, natural order
+// out) by the TPF = N2 threads lt of its group.  Input x[n1 + N1 n2]; step 1
+// DFTs over n2 (thread n1), twiddle w_N^{n1 k2}, step 3 DFTs over n1
+// (thread k2) -> X[k2 + N2 k1].  The intermediate uses the padded stride
+// N2 + 1 (conflict-free transposes).  Contains __syncthreads: every thread of
+// the block must call it.
+template <int N1, int N2, int SIGN>
+__device__ __forceinline__ void fft4step(double2* z, int lt, const double2* __restrict__ wN) {
+  constexpr int B2 = ilog2(N2), B1 = ilog2(N1);
+  {
+    double2 r[N2];
+    if (lt < N1) {
+#pragma unroll
+      for (int n2 = 0; n2 < N2; ++n2) r[n2] = z[lt + N1 * n2];
+      dft_reg<N2, SIGN>(r);
+    }
+    __syncthreads();
+    if (lt < N1) {
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) {
+        double2 v = r[brev(k2, B2)];
+        if (k2 != 0) {
+          const double2 w = __ldg(wN + lt * k2);
+          v = cmul(v, SIGN < 0 ? w : conj2(w));
+        }
+        z[lt * (N2 + 1) + k2] = v;
+      }
+    }
+    __syncthreads();
+  }
+  double2 s[N1];
+#pragma unroll
+  for (int n1 = 0; n1 < N1; ++n1) s[n1] = z[n1 * (N2 + 1) + lt];
+  dft_reg<N1, SIGN>(s);
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < N1; ++k1) z[lt + N2 * k1] = s[brev(k1, B1)];
+  __syncthreads();
+}
+
+enum { P_FWD = 0, P_INV = 1, P_FMI = 2 };  // DCT-II; DCT-III; DCT-II -> mask -> DCT-III
+
+// Orthonormal DCT-II coefficients at k and n-k of the two real vectors
+// packed in the spectrum Z (Z[k], Z[n-k] given): x = (vector a, vector b).
+__device__ __forceinline__ void fwd_post(double2 zk, double2 znk, double2 twk, double2 twnk, double ck, double cnk,
+                                         double2& xk, double2& xnk) {
+  // V_a = (Z[k] + conj Z[n-k]) / 2, V_b = (Z[k] - conj Z[n-k]) / 2i; V[n-k] = conj V[k]
+  const double2 va = make_double2(0.5 * (zk.x + znk.x), 0.5 * (zk.y - znk.y));
+  const double2 vb = make_double2(0.5 * (zk.y + znk.y), -0.5 * (zk.x - znk.x));
+  xk = make_double2(ck * (twk.x * va.x - twk.y * va.y), ck * (twk.x * vb.x - twk.y * vb.y));
+  xnk = make_double2(cnk * (twnk.x * va.x + twnk.y * va.y), cnk * (twnk.x * vb.x + twnk.y * vb.y));
+}
+
+// Inverse-FFT input at k of one real coefficient vector X:
+// spec(X)[k] = e^{i pi k / 2n} (X[k] / c_k - i X[n-k] / c_{n-k}) / n, X[n] = 0
+__device__ __forceinline__ double2 inv_pre1(double xk, double xnk, double2 twk, double ick, double icnk, double inv_n,
+                                            bool k0) {
+  const double re = xk * ick, im = k0 ? 0.0 : -xnk * icnk;
+  return make_double2((twk.x * re + twk.y * im) * inv_n, (twk.x * im - twk.y * re) * inv_n);
+}
+// W = spec(a) + i spec(b) at k and n - k from the coefficient pairs x = (a, b)
+__device__ __forceinline__ void inv_pre(double2 xk, double2 xnk, double2 twk, double2 twnk, double ick, double icnk,
+                                        double inv_n, bool k0, double2& wk, double2& wnk) {
+  const double2 sa = inv_pre1(xk.x, xnk.x, twk, ick, icnk, inv_n, k0);
+  const double2 sb = inv_pre1(xk.y, xnk.y, twk, ick, icnk, inv_n, k0);
+  wk = make_double2(sa.x - sb.y, sa.y + sb.x);
+  const double2 ta = inv_pre1(xnk.x, xk.x, twnk, icnk, ick, inv_n, false);
+  const double2 tb = inv_pre1(xnk.y, xk.y, twnk, icnk, ick, inv_n, false);
+  wnk = make_double2(ta.x - tb.y, ta.y + tb.x);
+}
+
+// One pass over an (nouter x n x ldq) float64 block: item (o, g) transforms
+// the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
+//   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(grid .* DCT-II)
+//   with grid[k n + o] (coefficient index k along m, outer index o)
+template <int N1, int N2, int MODE>
+__global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
+    k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
+               int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tw,
+               const double* __restrict__ cn, const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
+  constexpr int N = N1 * N2, FPI = 4, TPF = N2, NT = FPI * TPF;
+  constexpr int ZS = N1 * (N2 + 1);  // complex entries per FFT region (padded transpose)
   if (stt && stt->done) return;
-  const int64_t total = (int64_t)n * n * ldq;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = e / ((int64_t)n * ldq);
-    const int k = (int)((e / ldq) % n);
-    if (!grid[(int64_t)k * n + l]) buf[e] = 0.0;
+  extern __shared__ double2 zsm[];  // [FPI][ZS]
+  const int t = threadIdx.x;
+  const int f_own = t / TPF, lt = t % TPF;
+  const double inv_n = 1.0 / N;
+  for (int item = blockIdx.x; item < nouter * ngroups; item += gridDim.x) {
+    const int o = item / ngroups, g = item % ngroups;
+    const int64_t base = (int64_t)o * stride_o + g * 8;
+    __syncthreads();  // the previous item is done with shared memory
+    // ---- load: 4 consecutive threads copy one contiguous 64-B row of the item;
+    // cp.async keeps every copy of the thread in flight without registers
+#pragma unroll 8
+    for (int e = t; e < FPI * N; e += NT) {
+      const int f = e % FPI, m = e / FPI;
+      const int dst_i = MODE == P_INV ? m : ((m & 1) ? N - 1 - (m >> 1) : (m >> 1));  // Makhoul reorder
+      cp_async16(zsm + f * ZS + dst_i, src + base + m * stride_m + 2 * f);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (MODE == P_INV) {
+      // W at the pairs (k, n - k), in place (pairs are disjoint across threads)
+      for (int e = t; e < FPI * (N / 2 + 1); e += NT) {
+        const int f = e % FPI, k = e / FPI;
+        double2* z = zsm + f * ZS;
+        const int nk = (N - k) & (N - 1);
+        double2 wk, wnk;
+        inv_pre(z[k], z[nk], __ldg(tw + k), __ldg(tw + nk), 1.0 / __ldg(cn + k), 1.0 / __ldg(cn + nk), inv_n,
+                k == 0, wk, wnk);
+        z[k] = wk;
+        if (k != 0 && k != N / 2) z[nk] = wnk;
+      }
+      __syncthreads();
+    }
+    fft4step<N1, N2, (MODE == P_INV) ? 1 : -1>(zsm + f_own * ZS, lt, wN);
+    if (MODE == P_FWD) {
+      for (int e = t; e < FPI * N; e += NT) {
+        const int f = e % FPI, k = e / FPI;
+        const double2* z = zsm + f * ZS;
+        const int nk = (N - k) & (N - 1);
+        double2 xk, xnk;
+        fwd_post(z[k], z[nk], __ldg(tw + k), __ldg(tw + nk), __ldg(cn + k), __ldg(cn + nk), xk, xnk);
+        __stcs(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), xk);
+      }
+      continue;
+    }
+    if (MODE == P_FMI) {
+      // coefficients at (k, n - k) -> mask -> inverse-FFT input, in place per pair
+      for (int e = t; e < FPI * (N / 2 + 1); e += NT) {
+        const int f = e % FPI, k = e / FPI;
+        double2* z = zsm + f * ZS;
+        const int nk = (N - k) & (N - 1);
+        const double2 twk = __ldg(tw + k), twnk = __ldg(tw + nk);
+        const double ck = __ldg(cn + k), cnk = __ldg(cn + nk);
+        double2 xk, xnk;
+        fwd_post(z[k], z[nk], twk, twnk, ck, cnk, xk, xnk);
+        if (!__ldg(grid + (int64_t)k * N + o)) xk = make_double2(0.0, 0.0);
+        if (!__ldg(grid + (int64_t)nk * N + o)) xnk = make_double2(0.0, 0.0);
+        double2 wk, wnk;
+        inv_pre(xk, xnk, twk, twnk, 1.0 / ck, 1.0 / cnk, inv_n, k == 0, wk, wnk);
+        z[k] = wk;
+        if (k != 0 && k != N / 2) z[nk] = wnk;
+      }
+      __syncthreads();
+      fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, wN);
+    }
+    // ---- DCT-III output: x[m] = v[p(m)] (real part: vector 2f, imaginary: 2f + 1)
+#pragma unroll 4
+    for (int e = t; e < FPI * N; e += NT) {
+      const int f = e % FPI, m = e / FPI;
+      const double2 v = zsm[f * ZS + ((m & 1) ? N - 1 - (m >> 1) : (m >> 1))];
+      __stcs(reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f), v);
+    }
   }
 }
 
-// final transpose: out[(i n + j) ldq + q] = buf[j][(i ldq + q)], tiles of
-// 8 j x 16 i x ldq staged through smem (contiguous along (i, q) on load and
-// along (j, q) on store)
-constexpr int FJ = 8, FI = 16;
-__global__ void k_finish(int n, int ldq, const double* __restrict__ buf, double* __restrict__ out,
-                         const Status* __restrict__ stt) {
-  if (stt && stt->done) return;
-  extern __shared__ double ftile[];  // [FJ][FI * ldq]
-  const int nti = n / FI, ntj = n / FJ;
-  const int row = FI * ldq;
-  for (int tb = blockIdx.x; tb < nti * ntj; tb += gridDim.x) {
-    const int ib = tb % nti, jb = tb / nti;
-    __syncthreads();
-    for (int e = threadIdx.x; e < FJ * row; e += blockDim.x) {
-      const int jj = e / row, r = e % row;  // r = ii * ldq + q
-      ftile[jj * row + r] = buf[((int64_t)(jb * FJ + jj) * n + ib * FI) * ldq + r];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < FJ * row; e += blockDim.x) {
-      const int ii = e / (FJ * ldq), r = e % (FJ * ldq);  // r = jj * ldq + q
-      const int jj = r / ldq, q = r % ldq;
-      out[((int64_t)(ib * FI + ii) * n + jb * FJ) * ldq + r] = ftile[jj * row + ii * ldq + q];
-    }
-  }
-}
-
-// measurement gather / scatter for the explicit apply / adjoint utilities
-__global__ void k_gather(int64_t nm, int n, int ldq, const int64_t* __restrict__ mask, const double* __restrict__ buf,
+// measurement gather / scatter on the coefficient grid Y[(k n + l) ldq + q]
+__global__ void k_gather(int64_t nm, int ldq, const int64_t* __restrict__ mask, const double* __restrict__ grid_buf,
                          double* __restrict__ v) {
   const int64_t total = nm * ldq;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = e / ldq;
-    const int q = (int)(e % ldq);
-    const int64_t kl = mask[m];
-    const int64_t k = kl / n, l = kl % n;
-    v[e] = buf[(l * n + k) * ldq + q];  // buf = Y^T [l][(k ldq + q)]
+    v[e] = grid_buf[mask[m] * ldq + (e % ldq)];
   }
 }
 
-__global__ void k_scatter(int64_t nm, int n, int ldq, const int64_t* __restrict__ mask, const double* __restrict__ v,
-                          double* __restrict__ buf) {
+__global__ void k_scatter(int64_t nm, int ldq, const int64_t* __restrict__ mask, const double* __restrict__ v,
+                          double* __restrict__ grid_buf) {
   const int64_t total = nm * ldq;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = e / ldq;
-    const int q = (int)(e % ldq);
-    const int64_t kl = mask[m];
-    const int64_t k = kl / n, l = kl % n;
-    buf[(l * n + k) * ldq + q] = v[e];
+    grid_buf[mask[m] * ldq + (e % ldq)] = v[e];
   }
 }
 
-}  // namespace dct
+}  // namespace dctf
 }  // namespace cofem

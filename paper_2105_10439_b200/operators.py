@@ -262,8 +262,9 @@ class PartialDct2Operator(LinearOperator):
     z is an n x n image flattened row-major (D = n^2); Phi z = the coefficients
     at the flat indices ``mask`` (k n + l, sorted, distinct) of
     ``scipy.fft.dctn(z, norm="ortho")``.  Rows are orthonormal (Phi Phi^T = I).
-    On the GPU one apply is four int8 tensor-core stages against the n x n DCT
-    matrix (precision "ozaki"; n a multiple of 128).
+    On the GPU Phi^T Phi is three fused float64 FFT passes (row DCT-II, column
+    DCT-II / mask / DCT-III, row DCT-III + PCG combine); n a power of two in
+    [64, 1024].  Precision "ozaki" and "fp64" both select this float64 path.
     """
 
     kind = "partial-dct2"
@@ -285,15 +286,15 @@ class PartialDct2Operator(LinearOperator):
         self._ctx = {}
 
     def context(self, precision="ozaki"):
-        ctx = self._ctx.get(precision)
+        ctx = self._ctx.get("fft")
         if ctx is None:
-            ctx = self._ctx[precision] = self.new_context(precision)
+            ctx = self._ctx["fft"] = self.new_context(precision)
         return ctx
 
     def new_context(self, precision="ozaki"):
-        if precision != "ozaki":
-            raise NotImplementedError("2-D DCT dictionaries run in the 'ozaki' precision mode")
-        return _lib.Context.dct2(self.n, self.mask, _lib.OZAKI, self.device)
+        if precision not in ("ozaki", "fp64"):
+            raise NotImplementedError("2-D DCT dictionaries run the float64 FFT path ('ozaki' or 'fp64')")
+        return _lib.Context.dct2(self.n, self.mask, _lib.FP64, self.device)
 
     def release(self):
         for ctx in self._ctx.values():
