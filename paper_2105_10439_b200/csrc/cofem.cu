@@ -202,7 +202,8 @@ struct cofem_ctx {
   // 2-D partial DCT (kind 2): n x n images, D = n^2, N = mask size
   int dct_n = 0;
   int64_t* dct_mask = nullptr;      // N flat coefficient indices k n + l
-  uint8_t* dct_grid = nullptr;      // n x n 0/1 mask grid
+  uint8_t* dct_grid = nullptr;      // n x n 0/1 mask grid [k][l]
+  uint8_t* dct_gridT = nullptr;     // its transpose [l][k] (the column pass reads one l at a time)
   double *bufA = nullptr, *bufB = nullptr;  // n x n ldq pass buffers
   double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n}
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
@@ -625,7 +626,7 @@ template <int N1, int N2, int MODE>
 void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
   const int64_t n = c->dct_n, ldq = c->ldq;
   constexpr int NT = 4 * N2;
-  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2);
+  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dctf::k_dct_pass<N1, N2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -637,8 +638,8 @@ void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const S
   if (per_sm > 16) per_sm = 16;
   const int grid = std::min(items, per_sm * c->sm_count);
   dctf::k_dct_pass<N1, N2, MODE><<<grid, NT, smem, c->stream>>>(
-      src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / 8), c->dct_wN, c->dct_tw, c->dct_cn,
-      c->dct_grid, stt);
+      src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / 8), c->dct_wN, c->dct_tw,
+      c->dct_gridT, stt);
   c->launches++;
 }
 
@@ -1603,7 +1604,7 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   for (int j = 0; j < 64; ++j) w64[j] = make_double2(std::cos(2.0 * M_PI * j / 64), -std::sin(2.0 * M_PI * j / 64));
   if (cudaMalloc(&c->dct_wN, n * sizeof(double2)) || cudaMalloc(&c->dct_tw, n * sizeof(double2)) ||
       cudaMalloc(&c->dct_cn, n * sizeof(double)) || cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) ||
-      cudaMalloc(&c->dct_grid, grid.size()))
+      cudaMalloc(&c->dct_grid, grid.size()) || cudaMalloc(&c->dct_gridT, grid.size()))
     return bail(fail(COFEM_ENOMEM, "DCT tables"));
   cudaMemcpy(c->dct_wN, wN.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
   cudaMemcpy(c->dct_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
@@ -1613,6 +1614,10 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   std::sort(sorted.begin(), sorted.end());
   cudaMemcpy(c->dct_mask, sorted.data(), nmask * sizeof(int64_t), cudaMemcpyHostToDevice);
   cudaMemcpy(c->dct_grid, grid.data(), grid.size(), cudaMemcpyHostToDevice);
+  std::vector<uint8_t> gridT(grid.size());
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t l = 0; l < n; ++l) gridT[l * n + k] = grid[k * n + l];
+  cudaMemcpy(c->dct_gridT, gridT.data(), gridT.size(), cudaMemcpyHostToDevice);
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
@@ -1629,7 +1634,7 @@ int cofem_destroy(cofem_ctx* c) {
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
                   c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
-                  c->dct_mask, c->dct_grid, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn};
+                  c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

@@ -84,8 +84,16 @@ __device__ __forceinline__ void dft_reg(double2 (&x)[R]) {
 // (thread k2) -> X[k2 + N2 k1].  The intermediate uses the padded stride
 // N2 + 1 (conflict-free transposes).  Contains __syncthreads: every thread of
 // the block must call it.
+// Step-1 twiddles w_N^{lt k2} of one thread: the table value every 8th k2,
+// powers of the thread constant w1 = w_N^{lt} in between (<= 7 products).
+template <int N2>
+struct Tw1 {
+  double2 w1;
+  const double2* wN;
+};
+
 template <int N1, int N2, int SIGN>
-__device__ __forceinline__ void fft4step(double2* z, int lt, const double2* __restrict__ wN) {
+__device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1) {
   constexpr int B2 = ilog2(N2), B1 = ilog2(N1);
   {
     double2 r[N2];
@@ -96,14 +104,17 @@ __device__ __forceinline__ void fft4step(double2* z, int lt, const double2* __re
     }
     __syncthreads();
     if (lt < N1) {
+      const double2 w1 = SIGN < 0 ? tw1.w1 : conj2(tw1.w1);
+      double2 cur = make_double2(1.0, 0.0);
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
-        double2 v = r[brev(k2, B2)];
-        if (k2 != 0) {
-          const double2 w = __ldg(wN + lt * k2);
-          v = cmul(v, SIGN < 0 ? w : conj2(w));
+        if (k2 % 8 == 0) {
+          const double2 w = __ldg(tw1.wN + lt * k2);
+          cur = SIGN < 0 ? w : conj2(w);
         }
-        z[lt * (N2 + 1) + k2] = v;
+        else cur = cmul(cur, w1);
+        const double2 v = r[brev(k2, B2)];
+        z[lt * (N2 + 1) + k2] = k2 == 0 ? v : cmul(v, cur);
       }
     }
     __syncthreads();
@@ -151,20 +162,30 @@ __device__ __forceinline__ void inv_pre(double2 xk, double2 xnk, double2 twk, do
 
 // One pass over an (nouter x n x ldq) float64 block: item (o, g) transforms
 // the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
-//   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(grid .* DCT-II)
-//   with grid[k n + o] (coefficient index k along m, outer index o)
+//   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(mask .* DCT-II)
+//   with the transposed 0/1 grid gridT[o n + k] (outer index o, coefficient k along m)
 template <int N1, int N2, int MODE>
 __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
     k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
                int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tw,
-               const double* __restrict__ cn, const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
+               const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
   constexpr int N = N1 * N2, FPI = 4, TPF = N2, NT = FPI * TPF;
   constexpr int ZS = N1 * (N2 + 1);  // complex entries per FFT region (padded transpose)
+  constexpr int KS = NT / FPI;       // k stride between a thread's loop iterations
   if (stt && stt->done) return;
-  extern __shared__ double2 zsm[];  // [FPI][ZS]
+  extern __shared__ double2 zsm[];  // [FPI][ZS], then the item's mask column (P_FMI)
+  uint8_t* mcol = reinterpret_cast<uint8_t*>(zsm + FPI * ZS);
   const int t = threadIdx.x;
   const int f_own = t / TPF, lt = t % TPF;
   const double inv_n = 1.0 / N;
+  // thread constants: step-1 twiddles, Makhoul twiddle at k0 = t / FPI and its
+  // step e^{-i pi KS / 2n}; orthonormal scales in closed form
+  Tw1<N2> tw1;
+  tw1.w1 = __ldg(wN + (lt < N1 ? lt : 0));
+  tw1.wN = wN;
+  const int k0 = t / FPI;
+  const double2 tw0 = __ldg(tw + k0), tws = __ldg(tw + KS);
+  const double c_0 = sqrt(1.0 / N), c_k = sqrt(2.0 / N);
   for (int item = blockIdx.x; item < nouter * ngroups; item += gridDim.x) {
     const int o = item / ngroups, g = item % ngroups;
     const int64_t base = (int64_t)o * stride_o + g * 8;
@@ -177,54 +198,60 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
       const int dst_i = MODE == P_INV ? m : ((m & 1) ? N - 1 - (m >> 1) : (m >> 1));  // Makhoul reorder
       cp_async16(zsm + f * ZS + dst_i, src + base + m * stride_m + 2 * f);
     }
+    if (MODE == P_FMI)  // gridT[o n + k]: this item's mask column, n bytes
+      for (int b = t; b < N / 16; b += NT) cp_async16(mcol + 16 * b, grid + (int64_t)o * N + 16 * b);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     if (MODE == P_INV) {
       // W at the pairs (k, n - k), in place (pairs are disjoint across threads)
-      for (int e = t; e < FPI * (N / 2 + 1); e += NT) {
+      double2 twk = tw0;
+      for (int e = t; e < FPI * (N / 2 + 1); e += NT, twk = cmul(twk, tws)) {
         const int f = e % FPI, k = e / FPI;
         double2* z = zsm + f * ZS;
         const int nk = (N - k) & (N - 1);
+        const double2 twnk = make_double2(-twk.y, -twk.x);  // e^{-i pi (n-k) / 2n} = -i conj(tw_k)
         double2 wk, wnk;
-        inv_pre(z[k], z[nk], __ldg(tw + k), __ldg(tw + nk), 1.0 / __ldg(cn + k), 1.0 / __ldg(cn + nk), inv_n,
+        inv_pre(z[k], z[nk], twk, twnk, k == 0 ? 1.0 / c_0 : 1.0 / c_k, nk == 0 ? 1.0 / c_0 : 1.0 / c_k, inv_n,
                 k == 0, wk, wnk);
         z[k] = wk;
         if (k != 0 && k != N / 2) z[nk] = wnk;
       }
       __syncthreads();
     }
-    fft4step<N1, N2, (MODE == P_INV) ? 1 : -1>(zsm + f_own * ZS, lt, wN);
+    fft4step<N1, N2, (MODE == P_INV) ? 1 : -1>(zsm + f_own * ZS, lt, tw1);
     if (MODE == P_FWD) {
-      for (int e = t; e < FPI * N; e += NT) {
+      double2 twk = tw0;
+      for (int e = t; e < FPI * N; e += NT, twk = cmul(twk, tws)) {
         const int f = e % FPI, k = e / FPI;
         const double2* z = zsm + f * ZS;
         const int nk = (N - k) & (N - 1);
         double2 xk, xnk;
-        fwd_post(z[k], z[nk], __ldg(tw + k), __ldg(tw + nk), __ldg(cn + k), __ldg(cn + nk), xk, xnk);
+        fwd_post(z[k], z[nk], twk, make_double2(-twk.y, -twk.x), k == 0 ? c_0 : c_k, nk == 0 ? c_0 : c_k, xk, xnk);
         __stcs(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), xk);
       }
       continue;
     }
     if (MODE == P_FMI) {
       // coefficients at (k, n - k) -> mask -> inverse-FFT input, in place per pair
-      for (int e = t; e < FPI * (N / 2 + 1); e += NT) {
+      double2 twk = tw0;
+      for (int e = t; e < FPI * (N / 2 + 1); e += NT, twk = cmul(twk, tws)) {
         const int f = e % FPI, k = e / FPI;
         double2* z = zsm + f * ZS;
         const int nk = (N - k) & (N - 1);
-        const double2 twk = __ldg(tw + k), twnk = __ldg(tw + nk);
-        const double ck = __ldg(cn + k), cnk = __ldg(cn + nk);
+        const double2 twnk = make_double2(-twk.y, -twk.x);
+        const double ck = k == 0 ? c_0 : c_k, cnk = nk == 0 ? c_0 : c_k;
         double2 xk, xnk;
         fwd_post(z[k], z[nk], twk, twnk, ck, cnk, xk, xnk);
-        if (!__ldg(grid + (int64_t)k * N + o)) xk = make_double2(0.0, 0.0);
-        if (!__ldg(grid + (int64_t)nk * N + o)) xnk = make_double2(0.0, 0.0);
+        if (!mcol[k]) xk = make_double2(0.0, 0.0);
+        if (!mcol[nk]) xnk = make_double2(0.0, 0.0);
         double2 wk, wnk;
         inv_pre(xk, xnk, twk, twnk, 1.0 / ck, 1.0 / cnk, inv_n, k == 0, wk, wnk);
         z[k] = wk;
         if (k != 0 && k != N / 2) z[nk] = wnk;
       }
       __syncthreads();
-      fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, wN);
+      fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, tw1);
     }
     // ---- DCT-III output: x[m] = v[p(m)] (real part: vector 2f, imaginary: 2f + 1)
 #pragma unroll 4
