@@ -185,6 +185,21 @@ int cofem_run(cofem_ctx* ctx, const double* y, double beta, const cofem_em_confi
               int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration,
               int32_t* failed_step);
 
+/* ---- the reference's probe stream on the device ---------------------------------
+ * probes.draw_rademacher (probes.py:13-17) over numpy's PCG64 generator
+ * substream(seed, 3) (cofem.py:143): cofem_set_probe_stream(ctx, state, inc)
+ * hands the generator's 128-bit state and increment ({hi, lo} words, as in
+ * Generator.bit_generator.state) to the context; a later cofem_run with
+ * probes == NULL then draws EM iteration t's D x K signs on the device from
+ * the 32-bit halves [(t - 1) D K, t D K) of the generator's output -- bit for
+ * bit the reference's probes, with no host draw or upload (the generator
+ * must not hold a buffered half: has_uint32 == 0).  NULL state restores host
+ * / dseed probes.  cofem_pcg64_rademacher draws rows [row0, row0 + rows) of
+ * the D x K draw starting at half half_offset into host memory (a checker). */
+int cofem_set_probe_stream(cofem_ctx* ctx, const uint64_t* state, const uint64_t* inc);
+int cofem_pcg64_rademacher(int device, const uint64_t* state, const uint64_t* inc, uint64_t half_offset, int64_t row0,
+                           int64_t rows, int32_t k, int8_t* out);
+
 /* ---- multi-task CoFEM ----------------------------------------------------------
  * cofem.run_cofem_multitask (cofem.py:160-214): L tasks (one context each,
  * same D and precision, one GPU) share alpha; every EM iteration solves all

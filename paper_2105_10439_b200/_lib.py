@@ -52,6 +52,8 @@ EXPORTED = (
     "cofem_pcg_solve",
     "cofem_run",
     "cofem_run_multitask",
+    "cofem_set_probe_stream",
+    "cofem_pcg64_rademacher",
     "cofem_bench_prepare",
     "cofem_bench_iterations",
 )
@@ -153,6 +155,9 @@ def load():
                                         POINTER(c_int8), POINTER(c_double), POINTER(POINTER(c_double)),
                                         POINTER(POINTER(c_double)), POINTER(c_int32), POINTER(c_double),
                                         POINTER(c_int32), POINTER(c_int32)]),
+        "cofem_set_probe_stream": (c_int, [vp, POINTER(c_uint64), POINTER(c_uint64)]),
+        "cofem_pcg64_rademacher": (c_int, [c_int, POINTER(c_uint64), POINTER(c_uint64), c_uint64, c_int64, c_int64,
+                                           c_int32, POINTER(c_int8)]),
         "cofem_bench_prepare": (c_int, [vp, POINTER(c_double), c_double, POINTER(EmConfigC),
                                         POINTER(CgConfigC), c_uint64]),
         "cofem_bench_iterations": (c_int, [vp, c_int, c_int, POINTER(TimingC)]),
@@ -337,6 +342,15 @@ class Context:
         check(rc)
         return (alpha, mu, s, steps, resid), None
 
+    def set_probe_stream(self, rng):
+        """Draw the probes on the device from numpy Generator ``rng``'s PCG64
+        stream (bit for bit the reference's draw); None restores host probes."""
+        if rng is None:
+            check(load().cofem_set_probe_stream(self.handle, None, None))
+            return
+        state, inc = pcg64_words(rng)
+        check(load().cofem_set_probe_stream(self.handle, state, inc))
+
     # -- benchmark hooks
     def bench_prepare(self, y, beta, probes, max_steps, tolerance, theta_policy=0, variant=0, seed=0,
                       clamp_max=1e12, floor_eps=1e-12):
@@ -390,6 +404,31 @@ def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_m
         return None, (fit.value, fst.value)
     check(rc)
     return (alpha, mus, ss, steps, resid), None
+
+
+def pcg64_words(rng):
+    """(state, inc) of a numpy PCG64 Generator as two {hi, lo} uint64 arrays."""
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("the device probe stream reproduces numpy's PCG64 only")
+    if st.get("has_uint32"):
+        raise ValueError("the generator holds a buffered 32-bit half; draw probes on the host")
+    mask = (1 << 64) - 1
+
+    def words(v):
+        return (c_uint64 * 2)((v >> 64) & mask, v & mask)
+
+    return words(st["state"]["state"]), words(st["state"]["inc"])
+
+
+def pcg64_rademacher(rng, half_offset, row0, rows, k, device=0):
+    """Rows [row0, row0 + rows) of the D x K sign draw that starts at 32-bit
+    half ``half_offset`` of ``rng``'s stream, generated on the GPU (int8)."""
+    state, inc = pcg64_words(rng)
+    out = np.empty((rows, k), dtype=np.int8)
+    check(load().cofem_pcg64_rademacher(int(device), state, inc, int(half_offset), int(row0), int(rows), int(k),
+                                        out.ctypes.data_as(POINTER(c_int8))))
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -154,6 +154,10 @@ struct cofem_ctx {
   int device = 0, prec = COFEM_FP32;
   int64_t N = 0, D = 0, Np = 0, Dp = 0;
   int64_t col_offset = 0, global_cols = 0;
+  // reference probe stream (cofem_set_probe_stream): PCG64 state before the
+  // first draw; EM iteration t draws raw outputs [t ceil(D K / 2), ...)
+  bool pcg_stream = false;
+  uint64_t pcg_state[2] = {0, 0}, pcg_inc[2] = {0, 0};
   cudaStream_t stream = nullptr;
   float* phi = nullptr;
   bool have_phi = false;
@@ -1222,6 +1226,15 @@ int em_iteration(cofem_ctx* c, int t, int T_total, double beta, const cofem_em_c
   const int ldq = c->ldq;
   if (probes_host_iter) {
     CK(cudaMemcpyAsync(c->probes, probes_host_iter, (size_t)c->D * K, cudaMemcpyHostToDevice, c->stream));
+  } else if (c->pcg_stream) {
+    // this iteration's draw of the reference stream, this shard's rows
+    const uint64_t per_draw = (uint64_t)c->global_cols * K;  // 32-bit halves per draw
+    const int64_t nchunk = ((int64_t)c->D * K + 65) / 64 + 1;
+    k_pcg64_rademacher<<<(int)std::min<int64_t>((nchunk + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+        c->pcg_state[0], c->pcg_state[1], c->pcg_inc[0], c->pcg_inc[1], (uint64_t)(t - 1) * per_draw,
+        c->col_offset, c->D, K, c->probes);
+    c->launches++;
+    probes_host_iter = c->probes;  // (only tested for non-null below)
   }
   const int bs = 256;
   const int64_t n = c->Dp * ldq;
@@ -1878,6 +1891,36 @@ int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const
   std::vector<cofem_ctx*> cs(ctxs, ctxs + n_tasks);
   return DISPATCH(c0, run_multi_impl, cs.data(), n_tasks, ys, betas, em, cg, theta, probes, alpha, mus, ss,
                   cg_steps, cg_residuals, failed_iteration, failed_step);
+}
+
+int cofem_set_probe_stream(cofem_ctx* c, const uint64_t* state, const uint64_t* inc) {
+  CKR(check_ctx(c));
+  if (!state || !inc) {
+    c->pcg_stream = false;
+    return 0;
+  }
+  if (!(inc[1] & 1)) return fail(COFEM_EINVAL, "PCG64 increment must be odd");
+  c->pcg_stream = true;
+  c->pcg_state[0] = state[0];
+  c->pcg_state[1] = state[1];
+  c->pcg_inc[0] = inc[0];
+  c->pcg_inc[1] = inc[1];
+  return 0;
+}
+
+int cofem_pcg64_rademacher(int device, const uint64_t* state, const uint64_t* inc, uint64_t half_offset, int64_t row0,
+                           int64_t rows, int32_t k, int8_t* out) {
+  if (!state || !inc || !out || rows < 1 || k < 1 || row0 < 0) return fail(COFEM_EINVAL, "bad argument");
+  CK(cudaSetDevice(device));
+  int8_t* d = nullptr;
+  CK(cudaMalloc(&d, (size_t)rows * k));
+  const int64_t nchunk = (rows * k + 65) / 64 + 1;
+  k_pcg64_rademacher<<<(int)std::min<int64_t>((nchunk + 255) / 256, 4096), 256>>>(state[0], state[1], inc[0], inc[1],
+                                                                                 half_offset, row0, rows, k, d);
+  cudaError_t e = cudaMemcpy(out, d, (size_t)rows * k, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(COFEM_ECUDA, cudaGetErrorString(e));
+  return 0;
 }
 
 int cofem_bench_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em,

@@ -388,6 +388,66 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// ---- the reference's probe stream on the device ------------------------------
+// numpy's Generator(PCG64).integers(0, 2, size=(D, K)) (probes.py:13-17, the
+// reference's draw_rademacher) takes, for element e of the row-major D x K
+// draw, the top bit of the next 32-bit value of the generator -- Lemire's
+// bounded draw for a range of 2 never rejects -- and the generator hands out
+// 32-bit values as the low then the high half of each raw PCG64 output,
+// buffering an unused high half across calls.  So the probes of all draws
+// form one stream of 32-bit halves u_0, u_1, ... (u_{2r} = low(raw_r),
+// u_{2r+1} = high(raw_r)) and EM iteration t uses u_{t D K + e}.  PCG64 is a
+// 128-bit LCG (state = state M + inc, then output the new state) with the
+// XSL-RR output; threads jump ahead in O(log n).
+typedef unsigned __int128 u128;
+constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ull, PCG_MULT_LO = 0x4385DF649FCCF645ull;
+
+__host__ __device__ __forceinline__ uint64_t pcg64_output(u128 s) {
+  const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+  const unsigned rot = (unsigned)(s >> 122);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// state after `delta` LCG steps
+__host__ __device__ __forceinline__ u128 pcg64_advance(u128 s, u128 inc, uint64_t delta) {
+  u128 cur_mult = ((u128)PCG_MULT_HI << 64) | PCG_MULT_LO, cur_plus = inc;
+  u128 acc_mult = 1, acc_plus = 0;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * s + acc_plus;
+}
+
+// rows [row0, row0 + rows) of the row-major D x K sign matrix whose element 0
+// is 32-bit half `half_base` of the stream that starts at state (hi, lo).
+// Each thread produces the elements of 32 consecutive raw outputs.
+__global__ void k_pcg64_rademacher(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                                   uint64_t half_base, int64_t row0, int64_t rows, int K, int8_t* __restrict__ out) {
+  constexpr int RCH = 32;
+  const u128 s0 = ((u128)state_hi << 64) | state_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+  const u128 mult = ((u128)PCG_MULT_HI << 64) | PCG_MULT_LO;
+  const uint64_t h_begin = half_base + (uint64_t)(row0 * K), h_end = h_begin + (uint64_t)(rows * K);
+  const uint64_t r_begin = h_begin >> 1, r_end = (h_end + 1) >> 1;
+  const int64_t nchunk = (int64_t)((r_end - r_begin + RCH - 1) / RCH);
+  for (int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ch < nchunk; ch += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r0 = r_begin + (uint64_t)ch * RCH;
+    u128 st = pcg64_advance(s0, inc, r0);  // state before raw output r0
+#pragma unroll 4
+    for (int i = 0; i < RCH; ++i) {
+      st = st * mult + inc;
+      const uint64_t v = pcg64_output(st);
+      const uint64_t h = 2 * (r0 + i);
+      if (h >= h_begin && h < h_end) out[h - h_begin] = ((v >> 31) & 1) ? int8_t(1) : int8_t(-1);
+      if (h + 1 >= h_begin && h + 1 < h_end) out[h + 1 - h_begin] = ((v >> 63) & 1) ? int8_t(1) : int8_t(-1);
+    }
+  }
+}
+
 // Rademacher sign of (seed, iteration, global coordinate, probe)
 __device__ __forceinline__ int8_t device_probe(uint64_t seed, int iter, int64_t jg, int k) {
   const uint64_t h = splitmix64(seed ^ splitmix64(((uint64_t)iter << 40) ^ ((uint64_t)jg << 8) ^ (uint64_t)k));

@@ -14,7 +14,8 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from .cofem import PrecisionState, PosteriorEstimate, _theta_args, draw_probe_blocks
+from .cofem import PROBE_STREAM, PrecisionState, PosteriorEstimate, _theta_args
+from .problem import substream
 from .cg import DivergenceError
 
 ALIGN = 4  # shard boundaries on 4-column multiples (device RNG / vector loads)
@@ -93,11 +94,15 @@ def run_cofem_sharded(problem, cfg, device=0, sharded=None):
         sharded = ShardedContext(problem.op.n_rows, dim, cfg.cg.precision, device, phi=problem.op.matrix)
     c0, c1 = sharded.col_range
     theta_code, theta = _theta_args(cfg.cg.theta_policy, dim)
-    blocks = draw_probe_blocks(dim, cfg.probes, cfg.iterations, cfg.seed)[:, c0:c1, :]
-    out, failure = sharded.ctx.run(problem.y, problem.beta, cfg.iterations, cfg.probes,
-                                   _lib.VARIANT_CODES[cfg.variant], theta_code, cfg.clamp_max, cfg.floor_eps,
-                                   cfg.cg.max_steps, cfg.cg.tolerance, cfg.cg.printed_recursion,
-                                   None if theta is None else theta[c0:c1], blocks)
+    # every rank draws its rows of the reference's probe stream on its device
+    sharded.ctx.set_probe_stream(substream(cfg.seed, PROBE_STREAM))
+    try:
+        out, failure = sharded.ctx.run(problem.y, problem.beta, cfg.iterations, cfg.probes,
+                                       _lib.VARIANT_CODES[cfg.variant], theta_code, cfg.clamp_max, cfg.floor_eps,
+                                       cfg.cg.max_steps, cfg.cg.tolerance, cfg.cg.printed_recursion,
+                                       None if theta is None else theta[c0:c1], None)
+    finally:
+        sharded.ctx.set_probe_stream(None)
     if failure is not None:
         it, step = failure
         raise DivergenceError(step, f"EM iteration {it}")

@@ -575,3 +575,34 @@ def test_multitask_rejects_nonneg_and_mismatch():
     prob = _multitask_golden_tasks(g, "dense")[0]
     with pytest.raises(ValueError, match="standard"):
         run_cofem_multitask(MultiTaskProblem((prob,)), CofemConfig(variant="nonneg"))
+
+
+# ---- the reference's probe stream on the device ------------------------------
+
+@pytest.mark.parametrize("dim,k,t,row0,rows", [(1000, 20, 0, 0, 1000), (777, 3, 2, 0, 777), (777, 3, 1, 100, 200),
+                                                 (65536, 21, 5, 4096, 8192)])
+def test_device_probe_stream_matches_numpy(dim, k, t, row0, rows):
+    """probes.py:13-17 draws via numpy PCG64: the device stream gives the same
+    signs for iteration t's draw (odd D K included), for any row range."""
+    from paper_2105_10439_b200 import _lib, substream
+    from paper_2105_10439_b200.probes import draw_rademacher_int8
+
+    rng = substream(11, 3)
+    host = [draw_rademacher_int8(dim, k, rng) for _ in range(t + 1)][t]
+    dev = _lib.pcg64_rademacher(substream(11, 3), t * dim * k, row0, rows, k)
+    np.testing.assert_array_equal(dev, host[row0:row0 + rows])
+
+
+def test_run_cofem_device_probes_equal_host_probes():
+    """run_cofem draws its probes on the device; explicit host blocks of the
+    same stream give bitwise identical results."""
+    from paper_2105_10439_b200 import draw_probe_blocks
+
+    g = golden("multitask.npz")
+    prob = SblProblem(g["dense_y0"], DenseOperator(g["dense_phi0"]), 1e4)
+    cfg = CofemConfig(iterations=4, probes=9, seed=21)
+    st1, est1, d1 = run_cofem(prob, cfg)
+    st2, est2, d2 = run_cofem(prob, cfg, probe_blocks=draw_probe_blocks(prob.dim, 9, 4, 21))
+    np.testing.assert_array_equal(st1.alpha, st2.alpha)
+    np.testing.assert_array_equal(est1.mu, est2.mu)
+    assert [d["cg_steps"] for d in d1] == [d["cg_steps"] for d in d2]
