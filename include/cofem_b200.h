@@ -197,6 +197,12 @@ int cofem_run(cofem_ctx* ctx, const double* y, double beta, const cofem_em_confi
  * / dseed probes.  cofem_pcg64_rademacher draws rows [row0, row0 + rows) of
  * the D x K draw starting at half half_offset into host memory (a checker). */
 int cofem_set_probe_stream(cofem_ctx* ctx, const uint64_t* state, const uint64_t* inc);
+/* the same with an explicit layout: iteration t's draw starts at half
+ * first_half + (t - 1) halves_per_iteration (0: D K).  Task l of L in
+ * run_cofem_multitask (cofem.py:178-184) uses first_half = l D K,
+ * halves_per_iteration = L D K; with share_probes, 0 and D K. */
+int cofem_set_probe_stream_ex(cofem_ctx* ctx, const uint64_t* state, const uint64_t* inc, uint64_t first_half,
+                              uint64_t halves_per_iteration);
 int cofem_pcg64_rademacher(int device, const uint64_t* state, const uint64_t* inc, uint64_t half_offset, int64_t row0,
                            int64_t rows, int32_t k, int8_t* out);
 

@@ -53,6 +53,7 @@ EXPORTED = (
     "cofem_run",
     "cofem_run_multitask",
     "cofem_set_probe_stream",
+    "cofem_set_probe_stream_ex",
     "cofem_pcg64_rademacher",
     "cofem_bench_prepare",
     "cofem_bench_iterations",
@@ -156,6 +157,7 @@ def load():
                                         POINTER(POINTER(c_double)), POINTER(c_int32), POINTER(c_double),
                                         POINTER(c_int32), POINTER(c_int32)]),
         "cofem_set_probe_stream": (c_int, [vp, POINTER(c_uint64), POINTER(c_uint64)]),
+        "cofem_set_probe_stream_ex": (c_int, [vp, POINTER(c_uint64), POINTER(c_uint64), c_uint64, c_uint64]),
         "cofem_pcg64_rademacher": (c_int, [c_int, POINTER(c_uint64), POINTER(c_uint64), c_uint64, c_int64, c_int64,
                                            c_int32, POINTER(c_int8)]),
         "cofem_bench_prepare": (c_int, [vp, POINTER(c_double), c_double, POINTER(EmConfigC),
@@ -342,14 +344,14 @@ class Context:
         check(rc)
         return (alpha, mu, s, steps, resid), None
 
-    def set_probe_stream(self, rng):
+    def set_probe_stream(self, rng, first_half=0, halves_per_iteration=0):
         """Draw the probes on the device from numpy Generator ``rng``'s PCG64
         stream (bit for bit the reference's draw); None restores host probes."""
         if rng is None:
             check(load().cofem_set_probe_stream(self.handle, None, None))
             return
         state, inc = pcg64_words(rng)
-        check(load().cofem_set_probe_stream(self.handle, state, inc))
+        check(load().cofem_set_probe_stream_ex(self.handle, state, inc, int(first_half), int(halves_per_iteration)))
 
     # -- benchmark hooks
     def bench_prepare(self, y, beta, probes, max_steps, tolerance, theta_policy=0, variant=0, seed=0,
@@ -370,7 +372,8 @@ def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_m
                   tolerance, printed=False, theta=None, probe_blocks=None):
     """cofem_run_multitask over L contexts (one per task, same D, one GPU).
 
-    probe_blocks: T x L x D x K signs; theta: L x D (custom policy).  Returns
+    probe_blocks: T x L x D x K signs or None (every context has a probe
+    stream set); theta: L x D (custom policy).  Returns
     ((alpha, mus, ss, steps, resid), None) or (None, (iteration, step)) on divergence."""
     L = len(contexts)
     d = contexts[0].n_cols
@@ -386,8 +389,11 @@ def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_m
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         assert theta.shape == (L, d)
         th = _dp(theta)
-    probe_blocks = np.ascontiguousarray(probe_blocks, dtype=np.int8)
-    assert probe_blocks.shape == (iterations, L, d, probes)
+    pr = None
+    if probe_blocks is not None:
+        probe_blocks = np.ascontiguousarray(probe_blocks, dtype=np.int8)
+        assert probe_blocks.shape == (iterations, L, d, probes)
+        pr = probe_blocks.ctypes.data_as(POINTER(c_int8))
     alpha = np.empty(d)
     mus = [np.empty(d) for _ in range(L)]
     ss = [np.empty(d) for _ in range(L)]
@@ -397,7 +403,7 @@ def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_m
     resid = np.zeros(iterations)
     fit, fst = c_int32(0), c_int32(0)
     rc = load().cofem_run_multitask(handles, L, y_ptrs, _dp(betas), ctypes.byref(em), ctypes.byref(cg), th,
-                                    probe_blocks.ctypes.data_as(POINTER(c_int8)), _dp(alpha), mu_ptrs, s_ptrs,
+                                    pr, _dp(alpha), mu_ptrs, s_ptrs,
                                     steps.ctypes.data_as(POINTER(c_int32)), _dp(resid), ctypes.byref(fit),
                                     ctypes.byref(fst))
     if rc == COFEM_EDIVERGED:

@@ -158,6 +158,7 @@ struct cofem_ctx {
   // first draw; EM iteration t draws raw outputs [t ceil(D K / 2), ...)
   bool pcg_stream = false;
   uint64_t pcg_state[2] = {0, 0}, pcg_inc[2] = {0, 0};
+  uint64_t pcg_first = 0, pcg_stride = 0;  // halves before draw 0; halves between iterations (0: D K)
   cudaStream_t stream = nullptr;
   float* phi = nullptr;
   bool have_phi = false;
@@ -1219,6 +1220,16 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   return 0;
 }
 
+// EM iteration t's draw of the reference probe stream, this shard's rows, into c->probes
+void draw_stream_probes(cofem_ctx* c, int t, int K) {
+  const uint64_t stride = c->pcg_stride ? c->pcg_stride : (uint64_t)c->global_cols * K;  // 32-bit halves
+  const int64_t nchunk = ((int64_t)c->D * K + 65) / 64 + 1;
+  k_pcg64_rademacher<<<(int)std::min<int64_t>((nchunk + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+      c->pcg_state[0], c->pcg_state[1], c->pcg_inc[0], c->pcg_inc[1], c->pcg_first + (uint64_t)(t - 1) * stride,
+      c->col_offset, c->D, K, c->probes);
+  c->launches++;
+}
+
 template <typename T>
 int em_iteration(cofem_ctx* c, int t, int T_total, double beta, const cofem_em_config* em,
                  const cofem_cg_config* cg, const int8_t* probes_host_iter, uint64_t dseed, cofem_cg_report* rep) {
@@ -1227,13 +1238,7 @@ int em_iteration(cofem_ctx* c, int t, int T_total, double beta, const cofem_em_c
   if (probes_host_iter) {
     CK(cudaMemcpyAsync(c->probes, probes_host_iter, (size_t)c->D * K, cudaMemcpyHostToDevice, c->stream));
   } else if (c->pcg_stream) {
-    // this iteration's draw of the reference stream, this shard's rows
-    const uint64_t per_draw = (uint64_t)c->global_cols * K;  // 32-bit halves per draw
-    const int64_t nchunk = ((int64_t)c->D * K + 65) / 64 + 1;
-    k_pcg64_rademacher<<<(int)std::min<int64_t>((nchunk + 255) / 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-        c->pcg_state[0], c->pcg_state[1], c->pcg_inc[0], c->pcg_inc[1], (uint64_t)(t - 1) * per_draw,
-        c->col_offset, c->D, K, c->probes);
-    c->launches++;
+    draw_stream_probes(c, t, K);
     probes_host_iter = c->probes;  // (only tested for non-null below)
   }
   const int bs = 256;
@@ -1332,10 +1337,14 @@ int run_multi_impl(cofem_ctx** cs, int L, const double* const* ys, const double*
   for (int t = 1; t <= em->iterations && !rc; ++t) {
     for (int l = 0; l < L; ++l) {
       cofem_ctx* c = cs[l];
-      const int8_t* pt = probes + ((size_t)(t - 1) * L + l) * dk;
-      if (cudaMemcpyAsync(c->probes, pt, (size_t)dk, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess) {
-        rc = fail(COFEM_ECUDA, "probe upload");
-        break;
+      if (probes) {
+        const int8_t* pt = probes + ((size_t)(t - 1) * L + l) * dk;
+        if (cudaMemcpyAsync(c->probes, pt, (size_t)dk, cudaMemcpyHostToDevice, c0->stream) != cudaSuccess) {
+          rc = fail(COFEM_ECUDA, "probe upload");
+          break;
+        }
+      } else {
+        draw_stream_probes(c, t, K);  // c->stream is c0's stream here
       }
       const int64_t n = c->Dp * c->ldq;
       k_build_rhs<T><<<(int)std::min<int64_t>((n + 255) / 256, 8 * c->sm_count), 256, 0, c0->stream>>>(
@@ -1873,7 +1882,7 @@ int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const
                         const cofem_em_config* em, const cofem_cg_config* cg, const double* theta,
                         const int8_t* probes, double* alpha, double* const* mus, double* const* ss,
                         int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration, int32_t* failed_step) {
-  if (!ctxs || n_tasks < 1 || !ys || !betas || !em || !cg || !probes) return fail(COFEM_EINVAL, "null argument");
+  if (!ctxs || n_tasks < 1 || !ys || !betas || !em || !cg) return fail(COFEM_EINVAL, "null argument");
   cofem_ctx* c0 = ctxs[0];
   CKR(check_ctx(c0));
   if (em->variant != COFEM_STANDARD) return fail(COFEM_EINVAL, "multi-task loop supports the standard variant only");
@@ -1887,13 +1896,15 @@ int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const
       return fail(COFEM_EINVAL, "tasks must share D, precision and device (single GPU)");
     for (int m = 0; m < l; ++m)
       if (ctxs[m] == c) return fail(COFEM_EINVAL, "each task needs its own context");
+    if (!probes && !c->pcg_stream) return fail(COFEM_EINVAL, "no probes: pass host signs or set a probe stream");
   }
   std::vector<cofem_ctx*> cs(ctxs, ctxs + n_tasks);
   return DISPATCH(c0, run_multi_impl, cs.data(), n_tasks, ys, betas, em, cg, theta, probes, alpha, mus, ss,
                   cg_steps, cg_residuals, failed_iteration, failed_step);
 }
 
-int cofem_set_probe_stream(cofem_ctx* c, const uint64_t* state, const uint64_t* inc) {
+int cofem_set_probe_stream_ex(cofem_ctx* c, const uint64_t* state, const uint64_t* inc, uint64_t first_half,
+                              uint64_t halves_per_iteration) {
   CKR(check_ctx(c));
   if (!state || !inc) {
     c->pcg_stream = false;
@@ -1905,7 +1916,13 @@ int cofem_set_probe_stream(cofem_ctx* c, const uint64_t* state, const uint64_t* 
   c->pcg_state[1] = state[1];
   c->pcg_inc[0] = inc[0];
   c->pcg_inc[1] = inc[1];
+  c->pcg_first = first_half;
+  c->pcg_stride = halves_per_iteration;
   return 0;
+}
+
+int cofem_set_probe_stream(cofem_ctx* c, const uint64_t* state, const uint64_t* inc) {
+  return cofem_set_probe_stream_ex(c, state, inc, 0, 0);
 }
 
 int cofem_pcg64_rademacher(int device, const uint64_t* state, const uint64_t* inc, uint64_t half_offset, int64_t row0,
