@@ -263,7 +263,8 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": args.precision,
+        "dtype": {"ozaki": "i8 x i8 -> exact i32 Phi contractions (32-bit fixed-point Phi), f64 vectors",
+                  "fp64": "f64 (fp32 Phi)", "fp32": "f32 (fp64 scalars)"}[args.precision],
         "data": "synthetic (Gaussian Phi from a device Philox stream, 1% N(0,1) spikes, sigma=0.01)",
         "config": {"workload": f"{args.config}: dense Gaussian CS N={c.N} D={c.D} K={c.K} T={c.T} "
                                f"PCG cap {c.U} tol {c.tol}", "N": c.N, "D": c.D, "K": c.K,
