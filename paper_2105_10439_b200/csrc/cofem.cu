@@ -624,6 +624,51 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   return 0;
 }
 
+// Phi^T V of a PCG step with the combine fused into the band epilogue:
+// Psi[:, qoff:qoff+QW] = beta Phi^T V + alpha .* P and pi[qoff:...] directly
+// (no U round trip, no k_combine).  Returns 1 when the band does not fit the
+// smem-resident kernel (caller falls back to conv_bwd + k_combine).
+template <int QW>
+int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const Status* st) {
+  const int nk = oz::BM + c->conv_lpad;
+  const size_t sm = oz::BandCfg<QW>::smem(nk);
+  if (sm > 227 * 1024 - 64) return 1;  // (the last-block fold adds a little static smem)
+  CKR(oz_init_kernels<QW>());
+  const int slot = QW / 8;
+  if (!c->map_v_ok[slot]) {
+    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
+    c->map_v_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
+                               nullptr, st)));
+  c->v_colmax_valid = false;
+  const int nmb = (int)(c->Dp / oz::BM);
+  const int grid = std::min(nmb, std::min(c->sm_count, c->nblk_elem));
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(oz::band_kernel<QW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 64));
+    attr = true;
+  }
+  if (c->time_kernels) {
+    cudaEvent_t e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  Scalars sc = c->sc();
+  CK(cudaGetLastError());
+  oz::band_kernel<QW, true><<<grid, oz::NTHREADS, sm, c->stream>>>(
+      c->map_band_adj, c->map_v[slot], nmb, nk, 0, c->hrows, c->opscale, (double*)c->Psi + qoff, c->D, nullptr, st,
+      (const double*)c->P + qoff, c->ldq, c->alpha, beta, sc.pi + qoff, sc.partials, sc.ticket + 1);
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({1, c->evnext - 2});
+  }
+  c->launches++;
+  c->bwd_launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // ---- 2-D partial DCT: fused float64 FFT passes (dct.cuh) ------------------
 // pass over an n x n x ldq block; row passes run along j (outer i), column
 // passes along i (outer j / l)
@@ -816,6 +861,19 @@ int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
     const int qpc = chunk_width(c->ldq, qoff);
     CKR(fwd_chunk<T>(c, qpc, (const T*)c->P, c->ldq, qoff, (T*)c->V, st));
     CKR(allreduce(c, c->V, (size_t)c->Np * qpc, nccl_t<T>()));
+    if constexpr (std::is_same<T, double>::value) {
+      if (c->kind == 1) {  // convolution: combine fused into the band epilogue
+        int rc = 1;
+        switch (qpc) {
+          case 8: rc = conv_bwd_comb<8>(c, (const double*)c->V, qoff, beta, st); break;
+          case 16: rc = conv_bwd_comb<16>(c, (const double*)c->V, qoff, beta, st); break;
+          case 24: rc = conv_bwd_comb<24>(c, (const double*)c->V, qoff, beta, st); break;
+          case 32: rc = conv_bwd_comb<32>(c, (const double*)c->V, qoff, beta, st); break;
+        }
+        if (rc < 0) return rc;
+        if (rc == 0) continue;
+      }
+    }
     int ns = 1;
     CKR(bwd_chunk<T>(c, qpc, (const T*)c->V, &ns, st));
     const int bs = elem_block(qpc);

@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include "kernels.cuh"
+#include "pcg.cuh"
 
 namespace cofem {
 namespace oz {
@@ -219,6 +220,64 @@ __device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, c
         cm[q0 + t] = m > cm[q0 + t] ? m : cm[q0 + t];
       }
     }
+  }
+}
+
+// Epilogue with the PCG combine fused in (the conv Phi^T V launch): instead of
+// U = Phi^T V the row writes Psi = beta U + alpha_j P_j (k_combine's formula)
+// and accumulates p * psi per column for pi = <P, Psi>.
+// P values of the row's column groups (group g of this half at pv[8 g ..]),
+// loaded before the accumulator wait
+template <int QW>
+__host__ __device__ constexpr int comb_pv() { return (QW + 15) / 16 * 8; }
+template <int QW, int HALF>
+__device__ __forceinline__ void comb_prefetch(const double* __restrict__ prow, double (&pv)[comb_pv<QW>()]) {
+#pragma unroll
+  for (int q0 = HALF * 8, g = 0; q0 < QW; q0 += 16, ++g)
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(prow + q0 + t));
+      pv[8 * g + t] = v.x;
+      pv[8 * g + t + 1] = v.y;
+    }
+}
+
+template <int QW, int HALF>
+__device__ __forceinline__ void epilogue_row_comb(uint32_t tset_lane, double scale, const double* __restrict__ op_scale,
+                                                  double* o, const double (&pv)[comb_pv<QW>()], double alpha_j,
+                                                  double beta, double (&pacc)[QW]) {
+#pragma unroll
+  for (int q0 = HALF * 8, g = 0; q0 < QW; q0 += 16, ++g) {
+    double f[8], p[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      f[t] = scale * __ldg(op_scale + q0 + t);
+      p[t] = pv[8 * g + t];
+    }
+    uint32_t r[5][8];
+#pragma unroll
+    for (int sb = 0; sb < 5; ++sb)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]),
+                     "=r"(r[sb][5]), "=r"(r[sb][6]), "=r"(r[sb][7])
+                   : "r"(tset_lane + sb * QW + q0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int sb = 0; sb < 5; ++sb)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tset_lane + sb * QW + q0),
+                   "r"(0));
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                           ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+      const double u = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * f[t];
+      v[t] = beta * u + alpha_j * p[t];
+      pacc[q0 + t] += p[t] * v[t];
+    }
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + q0 + t) = make_double2(v[t], v[t + 1]);
   }
 }
 
@@ -429,12 +488,17 @@ struct BandCfg {
   static size_t smem(int nk) { return (size_t)nk * 4 * BM + (size_t)BSTAGES * B_STAGE + 1024 + 1280; }
 };
 
-template <int QW>
+// COMB (the Phi^T V launch of a PCG step): out = Psi = beta Phi^T V + alpha .* P
+// (P / out row stride p_ld, column offset of the chunk already applied) and
+// pi_out[q] = <P_q, Psi_q> through fixed-order block partials + last-block fold.
+template <int QW, bool COMB = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     band_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 int n_mblocks, int nk, int band_offset, const double* __restrict__ row_scale,
                 const double* __restrict__ op_scale, double* __restrict__ out, int64_t rows_real,
-                unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st) {
+                unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st,
+                const double* __restrict__ Pc = nullptr, int p_ld = 0, const double* __restrict__ alpha = nullptr,
+                double beta = 0.0, double* pi_out = nullptr, double* partials = nullptr, unsigned* ticket = nullptr) {
   using C = Cfg<QW>;
   using BC = BandCfg<QW>;
   if (st && st->done) return;
@@ -536,13 +600,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
     unsigned long long cm[QW];
+    double pacc[QW];
 #pragma unroll
-    for (int q = 0; q < QW; ++q) cm[q] = 0ull;
+    for (int q = 0; q < QW; ++q) {
+      cm[q] = 0ull;
+      pacc[q] = 0.0;
+    }
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
       const int buf = it & 1;
       const int64_t row = (int64_t)mb * BM + row_in_tile;
       const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
+      const double alpha_j = COMB ? alpha[row] : 0.0;
+      double pv[comb_pv<QW>()];
+      if (COMB) {
+        if (half == 0) comb_prefetch<QW, 0>(Pc + row * p_ld, pv);
+        else comb_prefetch<QW, 1>(Pc + row * p_ld, pv);
+      }
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (OZ_VARIANT == 2) {
@@ -560,6 +634,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                          "r"(0));
           if (r[0][0] == 0x12345 && scale == 3.0) out[row] = 1.0;
         }
+      } else if (COMB) {
+        const uint32_t tl = tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16);
+        if (half == 0)
+          epilogue_row_comb<QW, 0>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
+        else
+          epilogue_row_comb<QW, 1>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
       } else if (OZ_VARIANT != 3 && OZ_VARIANT != 4)
         epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16),
                           scale, op_scale, out + row * QW, cm);
@@ -568,6 +648,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_arrive(&tempty[buf]);
     }
     if (out_colmax) warp_fold_max<QW>(cm, cmax + (warp - 2) * QW);
+    if (COMB) {
+      // pi partial of this warp: fixed shuffle tree per column -> smem slice
+      double* psl = reinterpret_cast<double*>(cmax) + (warp - 2) * QW;
+#pragma unroll
+      for (int q = 0; q < QW; ++q) {
+        double v = pacc[q];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) psl[q] = v;
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -575,6 +666,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     unsigned long long m = cmax[threadIdx.x];
     for (int w = 1; w < EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
     atomicMax(&out_colmax[threadIdx.x], m);
+  }
+  if (COMB) {
+    const double* psl = reinterpret_cast<const double*>(cmax);
+    if (threadIdx.x < QW) {
+      double v = 0.0;
+      for (int w = 0; w < EPI_WARPS; ++w) v += psl[w * QW + threadIdx.x];  // fixed warp order
+      partials[(int64_t)blockIdx.x * QW + threadIdx.x] = v;
+    }
+    double* outs[1] = {pi_out};
+    last_block_reduce(ticket, partials, QW, 1, outs, reinterpret_cast<double*>(cmax) + EPI_WARPS * QW);
   }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
