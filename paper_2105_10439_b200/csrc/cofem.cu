@@ -339,15 +339,19 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->R, dbytes));
   CK(cudaMalloc(&c->P, dbytes));
   CK(cudaMalloc(&c->Psi, dbytes));
-  CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * QCHUNK * ts));
-  CK(cudaMalloc(&c->V, (size_t)c->Np * QCHUNK * ts));
+  // the DCT passes transform all ldq columns at once; the contractions run
+  // 32-column chunks
+  const int vcols = c->kind == 2 ? std::max(ldq, QCHUNK) : QCHUNK;
+  CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * vcols * ts));
+  CK(cudaMalloc(&c->V, (size_t)c->Np * vcols * ts));
   // split partial capacity: up to MAX_SPLITS partial blocks of a 32-column
-  // chunk for dense dictionaries; the banded operator writes one partial
-  const int max_splits = c->kind == 1 ? 1 : MAX_SPLITS;
-  c->vpart_cap = c->kind == 1 ? 0 : (size_t)max_splits * c->Np * QCHUNK * ts;
-  c->ppart_cap = (size_t)max_splits * c->Dp * QCHUNK * ts;
+  // chunk for dense dictionaries; the banded operator writes one partial; the
+  // DCT needs none
+  const int max_splits = c->kind == 0 ? MAX_SPLITS : 1;
+  c->vpart_cap = c->kind == 0 ? (size_t)max_splits * c->Np * QCHUNK * ts : 0;
+  c->ppart_cap = c->kind == 2 ? 0 : (size_t)max_splits * c->Dp * QCHUNK * ts;
   if (c->vpart_cap) CK(cudaMalloc(&c->vpart, c->vpart_cap));
-  CK(cudaMalloc(&c->ppart, c->ppart_cap));
+  if (c->ppart_cap) CK(cudaMalloc(&c->ppart, c->ppart_cap));
   CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
   c->nblk_elem = 2 * c->sm_count;

@@ -36,6 +36,15 @@ namespace dctf {
 
 __constant__ double2 c_w64[64];  // e^{-2 pi i j / 64}
 
+#ifndef DCT_STORE
+#define DCT_STORE 0  // timing builds: 0 streaming (.cs), 1 default write-back, 2 write-through
+#endif
+__device__ __forceinline__ void st_out(double2* p, double2 v) {
+  if (DCT_STORE == 0) __stcs(p, v);
+  else if (DCT_STORE == 1) *p = v;
+  else __stwt(p, v);
+}
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -228,7 +237,7 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
         const int nk = (N - k) & (N - 1);
         double2 xk, xnk;
         fwd_post(z[k], z[nk], twk, make_double2(-twk.y, -twk.x), k == 0 ? c_0 : c_k, nk == 0 ? c_0 : c_k, xk, xnk);
-        __stcs(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), xk);
+        st_out(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), xk);
       }
       continue;
     }
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
     for (int e = t; e < FPI * N; e += NT) {
       const int f = e % FPI, m = e / FPI;
       const double2 v = zsm[f * ZS + ((m & 1) ? N - 1 - (m >> 1) : (m >> 1))];
-      __stcs(reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f), v);
+      st_out(reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f), v);
     }
   }
 }

@@ -316,7 +316,8 @@ def test_convolution_apply_matches_reference_golden():
     np.testing.assert_allclose(op.context().column_sq_norms(), g["colsq"], rtol=1e-12)
 
 
-@pytest.mark.parametrize("dim,ntaps,q", [(4096, 256, 31), (1000, 37, 5), (300, 300, 2), (64, 1, 8)])
+@pytest.mark.parametrize("dim,ntaps,q", [(4096, 256, 31), (1000, 37, 5), (300, 300, 2), (64, 1, 8), (2048, 100, 40),
+                                         (777, 64, 70)])
 def test_fir_convolution_matches_numpy(dim, ntaps, q):
     from paper_2105_10439_b200 import ConvolutionOperator
 
@@ -356,8 +357,24 @@ def test_run_cofem_convolution_parity():
     assert abs(nour - nref) <= 0.01 * nref
 
 
+def test_run_cofem_convolution_many_probes():
+    """K = 40 probes: the 41 right-hand sides run as two column chunks (the
+    second through the fused-combine band epilogue too); against the oracle."""
+    from paper_2105_10439_b200 import build_exp_convolution
+
+    g = golden("conv_cases.npz")
+    prob = SblProblem(g["y"], build_exp_convolution(512, 0.04), float(g["beta"]))
+    cfg = CofemConfig(iterations=3, probes=40, seed=4, cg=CgConfig(max_steps=400, tolerance=1e-6))
+    st, est, diag = run_cofem(prob, cfg)
+    ocfg = O.CofemConfig(iterations=3, probes=40, seed=4, cg=O.CgConfig(max_steps=400, tolerance=1e-6))
+    alpha, mu, s, odiag = O.run_cofem(O.conv_op(512, (1.0 - 0.04) ** np.arange(512, dtype=np.float64)),
+                                      g["y"], float(g["beta"]), ocfg)
+    assert rel(est.mu, mu) <= 1e-4 and rel(st.alpha, alpha) <= 1e-4
+    assert np.all(np.abs(np.array([d["cg_steps"] for d in diag]) - [d["cg_steps"] for d in odiag]) <= 2)
+
+
 # ------------------------------------------------------- 2-D partial DCT ----
-@pytest.mark.parametrize("n,q", [(64, 1), (128, 21), (256, 5), (512, 9), (1024, 3)])
+@pytest.mark.parametrize("n,q", [(64, 1), (128, 21), (256, 5), (512, 9), (1024, 3), (64, 40), (128, 70)])
 def test_dct2_apply_matches_oracle(n, q):
     """The fused float64 FFT passes against scipy's dctn (oracle) to 1e-12."""
     from paper_2105_10439_b200 import PartialDct2Operator, variable_density_mask, substream
