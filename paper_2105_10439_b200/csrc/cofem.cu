@@ -179,7 +179,8 @@ struct cofem_ctx {
   double* partials = nullptr;
   unsigned* tickets = nullptr;
   Status* st = nullptr;
-  Status* h_st = nullptr;  // pinned, LAG slots
+  Status* h_st = nullptr;  // pinned + mapped, LAG slots (k_direction writes them)
+  Status* d_hst = nullptr; // device alias of h_st
   cudaEvent_t ev[LAG] = {};
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int nblk_elem = 0;
@@ -960,13 +961,13 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     c->launches++;
     CK(cudaGetLastError());
     CKR(allreduce(c, sc.rho_new, 2 * ldq, ncclFloat64));  // rho_new | rn2
+    const int slot = u % LAG;
+    // the kernel mirrors the status into the host-mapped slot: no copy in the stream
     k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
-        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st);
+        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot);
     c->launches++;
     CK(cudaGetLastError());
-    const int slot = u % LAG;
-    CK(cudaMemcpyAsync(&c->h_st[slot], c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaEventRecord(c->ev[slot], c->stream));
   }
   c->p_colmax_valid = false;
@@ -1065,17 +1066,17 @@ int pcg_multi(cofem_ctx** cs, int L, const double* betas, int q_real, const cofe
       c->launches++;
     }
     k_sum_tasks<<<1, 1, 0, c0->stream>>>(L, ldq, (const double* const*)dptrs, (const double* const*)(dptrs + L), agg);
+    const int slot = u % LAG;
     for (int l = 0; l < L; ++l) {
       cofem_ctx* c = cs[l];
       const bool fused = oz && c->kind != 2;
       k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c0->stream>>>(
           c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
-          c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg);
+          c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg,
+          l == L - 1 ? c0->d_hst + slot : nullptr);
       c->launches++;
     }
     CK(cudaGetLastError());
-    const int slot = u % LAG;
-    CK(cudaMemcpyAsync(&c0->h_st[slot], st, sizeof(Status), cudaMemcpyDeviceToHost, c0->stream));
     CK(cudaEventRecord(c0->ev[slot], c0->stream));
   }
   for (int l = 0; l < L; ++l) cs[l]->p_colmax_valid = false;
@@ -1509,7 +1510,8 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
   cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
-  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "pinned status"));
   for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   cudaEventCreate(&c->t0);
@@ -1576,7 +1578,8 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
   cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
-  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "pinned status"));
   for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   cudaEventCreate(&c->t0);
@@ -1669,7 +1672,8 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
   cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
-  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocDefault) != cudaSuccess)
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "pinned status"));
   for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   cudaEventCreate(&c->t0);

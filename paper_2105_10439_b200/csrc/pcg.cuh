@@ -276,9 +276,16 @@ template <typename T>
 __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
                             T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
                             const double* pre, unsigned long long* colmax, Status* st,
-                            const double* agg = nullptr) {
+                            const double* agg = nullptr, Status* mirror = nullptr) {
   // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
-  if (st->done) return;
+  // mirror: host-mapped status slot the host polls (no copy in the stream)
+  if (st->done) {
+    if (mirror && blockIdx.x == 0 && threadIdx.x == 0) {
+      *mirror = *st;
+      __threadfence_system();
+    }
+    return;
+  }
   extern __shared__ double sm_dir[];
   const int cur = step & 1, nxt = (step + 1) & 1;
   if (step == 0) {
@@ -305,6 +312,10 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
       st->converged = conv ? 1 : 0;
       st->diverged = finite ? 0 : 1;
       if (stop) st->done = 1;
+      if (mirror) {
+        *mirror = *st;
+        __threadfence_system();
+      }
     }
     if (stop) return;
   }
