@@ -428,26 +428,46 @@ def cpu_sample_conv(c, prob, seconds, steps_per_em, is_conv=True):
                       f"{steps_per_em:.1f} PCG steps per EM iteration"}
 
 
+# PCG steps per EM iteration of each config's default 20-iteration run, measured
+# on the GPU arm (profiles/r1d_bench_*.json).  The reference runs the identical
+# recursion (the parity tests match its step counts), so its EM iteration costs
+# the same number of PCG steps; the CPU arm times a bounded sample of steps.
+PCG_STEPS_PER_EM = {"dense-large": 179.35, "dense-mid": 170.0, "dense-small": 100.0, "conv-large": 172.55,
+                    "dct-large": 30.6}
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return
     from paper_2105_10439_b200 import simulate as S
 
-    c = S.CONFIGS[args.config]
-    steps_per_em = float(c.U)  # the PCG cap: nearly every iteration of this workload runs to it
-    cb = CpuBaseline(c)
+    structured = args.config in S.CONV_CONFIGS or args.config in S.DCT_CONFIGS
+    if structured:
+        is_conv = args.config in S.CONV_CONFIGS
+        c = S.CONV_CONFIGS[args.config] if is_conv else S.DCT_CONFIGS[args.config]
+        prob, _ = S.conv_problem(c) if is_conv else S.dct2_problem(c)
+    else:
+        c = S.CONFIGS[args.config]
+        cb = CpuBaseline(c)
+    steps_per_em = PCG_STEPS_PER_EM.get(args.config, float(c.U))
+
+    def sample(seconds):
+        if structured:
+            return cpu_sample_conv(c, prob, seconds, steps_per_em, is_conv)
+        return cb.sample(seconds, steps_per_em)
+
     for _ in range(args.warmup):
-        base = cb.sample(1.0, steps_per_em)
+        base = sample(1.0)
     per = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        base = cb.sample(max(1.0, args.cpu_seconds / max(args.steps, 1)), steps_per_em)
+        base = sample(max(1.0, args.cpu_seconds / max(args.steps, 1)))
         per.append(base["value"])
     el = time.perf_counter() - t0
     value = float(np.median(per))
     line = {
-        "metric": METRIC,
+        "metric": METRICS.get(args.config, METRIC),
         "value": value,
         "unit": UNIT,
         "n_gpus": world,
@@ -459,14 +479,16 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (same generator as the GPU arm)",
-        "config": {"workload": f"{args.config}: dense Gaussian CS N={c.N} D={c.D} K={c.K} T={c.T} "
-                               f"PCG cap {c.U} tol {c.tol}", "N": c.N, "D": c.D, "K": c.K},
+        "config": ({"workload": f"{args.config}: D={c.D} K={c.K}", "D": c.D, "K": c.K} if structured else
+                   {"workload": f"{args.config}: dense Gaussian CS N={c.N} D={c.D} K={c.K} T={c.T} "
+                                f"PCG cap {c.U} tol {c.tol}", "N": c.N, "D": c.D, "K": c.K}),
         "impl": "reference",
         "cpu_baseline": {**{k: base[k] for k in ("unit", "cores", "kind", "sample")}, "value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_seconds": el,
         "note": "each step = one bounded PCG sample of the full-size float64 system; EM it/s assumes "
-                f"{steps_per_em:.0f} PCG steps per EM iteration (the config's cap)",
+                f"{steps_per_em:.1f} PCG steps per EM iteration (measured on the GPU arm with the identical "
+                "recursion)",
     }
     print(json.dumps(line), flush=True)
 
