@@ -347,7 +347,8 @@ def run_ours_conv(args):
     is_conv = args.config in S.CONV_CONFIGS
     c = S.CONV_CONFIGS[args.config] if is_conv else S.DCT_CONFIGS[args.config]
     prob, z = S.conv_problem(c) if is_conv else S.dct2_problem(c)
-    ctx = prob.op.context("ozaki")
+    prec = args.precision if args.precision in ("ozaki", "fp64") else "ozaki"
+    ctx = prob.op.context(prec)
     dseed = 0xC0FE
     ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
     if args.warmup:
@@ -390,7 +391,7 @@ def run_ours_conv(args):
     }
     prob.op.release()
     if not args.no_e2e:
-        cfg = c.cofem_config("ozaki", iterations=args.steps)
+        cfg = c.cofem_config(prec, iterations=args.steps)
         t0 = time.perf_counter()
         st, est, diag = run_cofem(prob, cfg)
         el = time.perf_counter() - t0

@@ -48,7 +48,9 @@ int fail(int code, const std::string& msg) {
     if (r_ != 0) return r_; \
   } while (0)
 
-constexpr int LAG = 3;          // host status poll distance (steps)
+constexpr int LAG = 3;
+constexpr int CONV_FFT_N = 1024;        // overlap-save block of the FP64 convolution path
+constexpr int CONV_FFT_MAX_TAPS = 512;  // >= 513 outputs per block          // host status poll distance (steps)
 constexpr int QCHUNK = 32;      // max columns per contraction launch
 constexpr int64_t PAD = 256;    // Np, Dp multiples (tile sizes divide it)
 constexpr int MAX_SPLITS = 32;  // split-K partial blocks per contraction
@@ -204,6 +206,10 @@ struct cofem_ctx {
   int8_t *band_fwd = nullptr, *band_adj = nullptr;   // [4][128][128 + lpad] digit planes
   double* hrows = nullptr;                           // Dp copies of the band's power-of-two scale
   CUtensorMap map_band_fwd{}, map_band_adj{};
+  // float64 FFT path (precision FP64, <= 512 taps): overlap-save spectra of h
+  // and of reversed h (1024 points, 1/1024 folded in); FFT twiddles in dct_wN
+  bool conv_fft = false;
+  double2 *cf_H = nullptr, *cf_Hr = nullptr;
 
   // 2-D partial DCT (kind 2): n x n images, D = n^2, N = mask size
   int dct_n = 0;
@@ -342,7 +348,8 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->Psi, dbytes));
   // the DCT passes transform all ldq columns at once; the contractions run
   // 32-column chunks
-  const int vcols = c->kind == 2 ? std::max(ldq, QCHUNK) : QCHUNK;
+  const bool whole = c->kind == 2 || c->conv_fft;  // passes over all ldq columns at once
+  const int vcols = whole ? std::max(ldq, QCHUNK) : QCHUNK;
   CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * vcols * ts));
   CK(cudaMalloc(&c->V, (size_t)c->Np * vcols * ts));
   // split partial capacity: up to MAX_SPLITS partial blocks of a 32-column
@@ -350,7 +357,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   // DCT needs none
   const int max_splits = c->kind == 0 ? MAX_SPLITS : 1;
   c->vpart_cap = c->kind == 0 ? (size_t)max_splits * c->Np * QCHUNK * ts : 0;
-  c->ppart_cap = c->kind == 2 ? 0 : (size_t)max_splits * c->Dp * QCHUNK * ts;
+  c->ppart_cap = whole ? 0 : (size_t)max_splits * c->Dp * QCHUNK * ts;
   if (c->vpart_cap) CK(cudaMalloc(&c->vpart, c->vpart_cap));
   if (c->ppart_cap) CK(cudaMalloc(&c->ppart, c->ppart_cap));
   CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
@@ -674,6 +681,55 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   return 0;
 }
 
+// ---- convolution, float64 FFT path (dct.cuh k_conv_fft_pass) ----------------
+// dst (D x ldq) = Phi src (adj: Phi^T src) for all ldq columns at once
+int conv_fft_pass(cofem_ctx* c, const double* src, double* dst, bool adj, const Status* stt) {
+  constexpr int N1 = 32, N2 = 32, NT = 4 * N2;
+  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(dctf::k_conv_fft_pass<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int L = c->conv_L, valid = CONV_FFT_N - (L - 1);
+  const int nblocks = (int)((c->D + valid - 1) / valid);
+  const int items = nblocks * (c->ldq / 8);
+  const int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));
+  const int grid = std::min(items, per_sm * c->sm_count);
+  dctf::k_conv_fft_pass<N1, N2><<<grid, NT, smem, c->stream>>>(src, dst, c->D, c->ldq, c->ldq / 8, nblocks, valid,
+                                                                adj ? 0 : L - 1, L - 1, adj ? c->cf_Hr : c->cf_H,
+                                                                c->dct_wN, stt);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Psi = beta Phi^T Phi P + alpha .* P, pi: two FFT passes + the streaming combine
+int conv_fft_system_apply(cofem_ctx* c, double beta, const Status* stt) {
+  cudaEvent_t e0 = nullptr;
+  if (c->time_kernels) {
+    e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  CKR(conv_fft_pass(c, (const double*)c->P, (double*)c->V, false, stt));
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({0, c->evnext - 2});
+    c->fwd_launches++;
+  }
+  (void)e0;
+  CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, stt));
+  Scalars sc = c->sc();
+  const int bs = elem_block(c->ldq);
+  k_combine<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->tmpD, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
+      stt);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // ---- 2-D partial DCT: fused float64 FFT passes (dct.cuh) ------------------
 // pass over an n x n x ldq block; row passes run along j (outer i), column
 // passes along i (outer j / l)
@@ -860,6 +916,7 @@ template <typename T>
 int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
   if constexpr (std::is_same<T, double>::value) {
     if (c->kind == 2) return dct_system_apply(c, beta, st);
+    if (c->conv_fft) return conv_fft_system_apply(c, beta, st);
   }
   Scalars sc = c->sc();
   for (int qoff = 0; qoff < c->ldq; qoff += QCHUNK) {
@@ -1137,6 +1194,10 @@ int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
   const int ldq = ldq_for(q);
   CKR(ensure_ws(c, ldq));
   CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
+  if (c->conv_fft) {
+    CKR(conv_fft_pass(c, (const double*)c->P, (double*)c->V, false, nullptr));
+    return download_block<T>(c, c->V, c->N, q, ldq, 0, out);
+  }
   if (c->kind == 2) {
     CKR(dct_forward_dev(c, (const double*)c->P, nullptr));
     dctf::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, ldq, c->dct_mask, c->bufB, (double*)c->V);
@@ -1163,6 +1224,11 @@ template <typename T>
 int adjoint_impl(cofem_ctx* c, const double* U, int64_t q, double* out) {
   const int ldq = ldq_for(q);
   CKR(ensure_ws(c, ldq));
+  if (c->conv_fft) {
+    CKR(upload_block<T>(c, U, c->N, q, c->Np, ldq, c->V));
+    CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, nullptr));
+    return download_block<T>(c, c->tmpD, c->D, q, ldq, 0, out);
+  }
   if (c->kind == 2) {
     CKR(upload_block<T>(c, U, c->N, q, c->Np, ldq, c->V));
     CKR(dct_adjoint_from_V(c));
@@ -1213,11 +1279,12 @@ template <typename T>
 int compute_aty(cofem_ctx* c, const double* y_host) {
   // V[:, 0] = y, other columns 0 -> Phi^T V via the bwd contraction (8-wide)
   CKR(ensure_ws(c, std::max(c->ldq, 8)));
-  if (c->kind == 2) {
+  if (c->kind == 2 || c->conv_fft) {
     std::vector<double> vb((size_t)c->Np * c->ldq, 0.0);
     for (int64_t i = 0; i < c->N; ++i) vb[i * c->ldq] = y_host[i];
     CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CKR(dct_adjoint_from_V(c));
+    if (c->conv_fft) CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, nullptr));
+    else CKR(dct_adjoint_from_V(c));
     std::vector<double> out((size_t)c->Dp * c->ldq);
     CK(cudaMemcpyAsync(out.data(), c->tmpD, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1544,7 +1611,10 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   if (!out || !taps) return fail(COFEM_EINVAL, "null argument");
   *out = nullptr;
   if (dim < 1 || ntaps < 1 || ntaps > dim) return fail(COFEM_EINVAL, "need 1 <= ntaps <= dim");
-  if (precision != COFEM_OZAKI) return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI precision");
+  if (precision != COFEM_OZAKI && precision != COFEM_FP64)
+    return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI (int8 band) or FP64 (FFT) precision");
+  if (precision == COFEM_FP64 && ntaps > CONV_FFT_MAX_TAPS)
+    return fail(COFEM_EINVAL, "the FP64 (FFT) convolution path takes at most 512 taps");
   if (ntaps > oz::MAX_K_PER_ITEM - 2 * oz::BM) return fail(COFEM_EINVAL, "at most 32512 taps");
   double hmax = 0.0;
   for (int64_t m = 0; m < ntaps; ++m) {
@@ -1584,6 +1654,47 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
   cudaEventCreate(&c->t0);
   cudaEventCreate(&c->t1);
+  // column j of the lower-triangular Toeplitz matrix holds taps[0 : min(L, D - j)]
+  {
+    std::vector<double> csq(c->Dp, 0.0), cum(ntaps + 1, 0.0);
+    for (int64_t m = 0; m < ntaps; ++m) cum[m + 1] = cum[m] + taps[m] * taps[m];
+    for (int64_t j = 0; j < dim; ++j) csq[j] = cum[std::min<int64_t>(ntaps, dim - j)];
+    cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (precision == COFEM_FP64) {
+    // overlap-save spectra (1024 points, 1/1024 folded in) of h and of reversed h
+    c->conv_fft = true;
+    const int n = CONV_FFT_N;
+    std::vector<double2> H(n), Hr(n), wN(n), w64(64);
+    for (int k = 0; k < n; ++k) {
+      double hr = 0, hi = 0, rr = 0, ri = 0;
+      for (int64_t m = 0; m < ntaps; ++m) {
+        const double ang = -2.0 * M_PI * (double)((k * m) % n) / n;
+        hr += taps[m] * std::cos(ang);
+        hi += taps[m] * std::sin(ang);
+        const double tr = taps[ntaps - 1 - m];
+        rr += tr * std::cos(ang);
+        ri += tr * std::sin(ang);
+      }
+      H[k] = make_double2(hr / n, hi / n);
+      Hr[k] = make_double2(rr / n, ri / n);
+      wN[k] = make_double2(std::cos(2.0 * M_PI * k / n), -std::sin(2.0 * M_PI * k / n));
+    }
+    for (int j = 0; j < 64; ++j) w64[j] = make_double2(std::cos(2.0 * M_PI * j / 64), -std::sin(2.0 * M_PI * j / 64));
+    if (cudaMalloc(&c->cf_H, n * sizeof(double2)) || cudaMalloc(&c->cf_Hr, n * sizeof(double2)) ||
+        cudaMalloc(&c->dct_wN, n * sizeof(double2)) ||
+        cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess)
+      return bail(fail(COFEM_ENOMEM, "FFT tables"));
+    cudaMemcpy(c->cf_H, H.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(c->cf_Hr, Hr.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(c->dct_wN, wN.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpyToSymbol(dctf::c_w64, w64.data(), 64 * sizeof(double2));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+    c->have_phi = true;
+    *out = c;
+    return 0;
+  }
   // operand buffers of the int8 path
   if (cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp) != cudaSuccess ||
       cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np) != cudaSuccess ||
@@ -1616,14 +1727,9 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   if (!rc) rc = encode_u8_3d(&c->map_band_adj, c->band_adj, nk, oz::BM, 4, oz::KT, oz::BM, 4);
   if (rc) return bail(rc);
   // scales: output rows carry hs; operands are not pre-scaled (ones)
-  std::vector<double> hv(c->Dp, hs), ones(c->Dp, 1.0), csq(c->Dp, 0.0);
-  // column j of the lower-triangular Toeplitz matrix holds taps[0 : min(L, D - j)]
-  std::vector<double> cum(ntaps + 1, 0.0);
-  for (int64_t m = 0; m < ntaps; ++m) cum[m + 1] = cum[m] + taps[m] * taps[m];
-  for (int64_t j = 0; j < dim; ++j) csq[j] = cum[std::min<int64_t>(ntaps, dim - j)];
+  std::vector<double> hv(c->Dp, hs), ones(c->Dp, 1.0);
   cudaMemcpy(c->hrows, hv.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
   cudaMemcpy(c->colscale, ones.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
@@ -1722,7 +1828,8 @@ int cofem_destroy(cofem_ctx* c) {
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
                   c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
-                  c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn};
+                  c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
+                  c->cf_H, c->cf_Hr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

@@ -293,3 +293,63 @@ __global__ void k_scatter(int64_t nm, int ldq, const int64_t* __restrict__ mask,
 
 }  // namespace dctf
 }  // namespace cofem
+
+// ---------------------------------------------------------------------------
+// Convolution dictionaries on the same FFT machinery: overlap-save with
+// 1024-point blocks.  Phi x (causal conv with h, L taps) and Phi^T x (the
+// correlation) are both "circular convolution of a 1024-sample window with a
+// fixed spectrum, keep samples [L-1, 1024)": window start b V - (L - 1) with
+// the spectrum of h (Phi), or b V with the spectrum of reversed h (Phi^T),
+// V = 1024 - (L - 1) outputs per block.  Two real columns ride in one complex
+// FFT (h is real, so the packed pair convolves independently), and the
+// spectrum carries the 1/1024 of the inverse transform.  Float64 throughout.
+namespace cofem {
+namespace dctf {
+
+template <int N1, int N2>
+__global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
+    k_conv_fft_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t rows, int ldq, int ngroups,
+                    int nblocks, int valid, int in_shift, int keep0, const double2* __restrict__ spec,
+                    const double2* __restrict__ wN, const Status* __restrict__ stt) {
+  constexpr int N = N1 * N2, FPI = 4, TPF = N2, NT = FPI * TPF;
+  constexpr int ZS = N1 * (N2 + 1);
+  if (stt && stt->done) return;
+  extern __shared__ double2 zsm[];
+  const int t = threadIdx.x;
+  const int f_own = t / TPF, lt = t % TPF;
+  Tw1<N2> tw1;
+  tw1.w1 = __ldg(wN + (lt < N1 ? lt : 0));
+  tw1.wN = wN;
+  for (int item = blockIdx.x; item < nblocks * ngroups; item += gridDim.x) {
+    const int b = item / ngroups, g = item % ngroups;
+    const int64_t w0 = (int64_t)b * valid - in_shift;  // first window row
+    __syncthreads();
+#pragma unroll 8
+    for (int e = t; e < FPI * N; e += NT) {
+      const int f = e % FPI, m = e / FPI;
+      const int64_t row = w0 + m;
+      if (row >= 0 && row < rows) cp_async16(zsm + f * ZS + m, src + row * ldq + g * 8 + 2 * f);
+      else zsm[f * ZS + m] = make_double2(0.0, 0.0);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    fft4step<N1, N2, -1>(zsm + f_own * ZS, lt, tw1);
+    for (int e = t; e < FPI * N; e += NT) {
+      const int f = e % FPI, k = e / FPI;
+      zsm[f * ZS + k] = cmul(zsm[f * ZS + k], __ldg(spec + k));
+    }
+    __syncthreads();
+    fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, tw1);
+    // outputs rows b V + m', m' < valid, from circular samples keep0 + m'
+    const int64_t o0 = (int64_t)b * valid;
+    for (int e = t; e < FPI * valid; e += NT) {
+      const int f = e % FPI, mm = e / FPI;
+      const int64_t row = o0 + mm;
+      if (row < rows) st_out(reinterpret_cast<double2*>(dst + row * ldq + g * 8 + 2 * f), zsm[f * ZS + keep0 + mm]);
+    }
+  }
+}
+
+}  // namespace dctf
+}  // namespace cofem

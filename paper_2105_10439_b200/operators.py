@@ -226,9 +226,13 @@ class ConvolutionOperator(LinearOperator):
         return ctx
 
     def new_context(self, precision="ozaki"):
-        if precision != "ozaki":
-            raise NotImplementedError("convolution dictionaries run in the 'ozaki' precision mode")
-        return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
+        """'ozaki': banded int8 tensor-core kernel (any filter length);
+        'fp64': float64 overlap-save FFT passes (filters up to 512 taps)."""
+        if precision == "ozaki":
+            return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
+        if precision == "fp64":
+            return _lib.Context.convolution(self.n_cols, self.filter, _lib.FP64, self.device)
+        raise NotImplementedError("convolution dictionaries run in the 'ozaki' or 'fp64' precision mode")
 
     def release(self):
         for ctx in self._ctx.values():
