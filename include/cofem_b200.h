@@ -125,7 +125,11 @@ int cofem_set_dictionary_f64(cofem_ctx* ctx, const double* phi, int64_t ld);
 
 /* Declare this context's place in a column-sharded dictionary: it holds
  * global columns [col_offset, col_offset + n_cols) of `global_cols`.  Used by
- * the device generators so every shard draws the same global Phi / probes. */
+ * the device generators so every shard draws the same global Phi / probes.
+ * Convolution contexts are time shards: samples [col_offset, col_offset +
+ * dim) of a length-global_cols sequence (rows = columns); col_offset is a
+ * multiple of 256, every shard but the last holds a multiple of 256 samples
+ * and at least the filter halo.  2-D DCT contexts are not sharded. */
 int cofem_set_shard(cofem_ctx* ctx, int64_t col_offset, int64_t global_cols);
 
 /* Generate Phi on the device: entries scale * N(0,1) from a counter-based
@@ -141,6 +145,26 @@ int cofem_get_dictionary(cofem_ctx* ctx, float* out);
  * nranks == 1 the collectives are real single-rank NCCL calls.        */
 int cofem_nccl_get_unique_id(void* out128);
 int cofem_set_comm(cofem_ctx* ctx, const void* unique_id128, int nranks, int rank);
+/* Exchanges per PCG step (call cofem_set_shard first):
+ *   dense:        all-reduce(sum) of the N x (K+1) partial Phi_r P_r; pi and
+ *                 (rho, ||R||^2) all-reduces.
+ *   convolution:  all-reduce(max) of the operand column maxima (common int8
+ *                 scales), then a neighbour halo send/recv of lpad operand rows
+ *                 (int8 digit planes) before each banded contraction -- Phi P
+ *                 takes the left neighbour's last rows, Phi^T V the right
+ *                 neighbour's first rows; pi and (rho, ||R||^2) all-reduces.
+ *
+ * In-process shard group: the same exchanges between contexts driven from
+ * host threads of one process (one thread per rank, each calling the usual
+ * entry points on its context).  The ranks' buffers are read directly (same
+ * device or peer memory) after stream-ordered events; a rank that fails
+ * breaks the group so the others return an error instead of waiting.
+ * A context joins either an NCCL communicator or a group, once.        */
+typedef struct cofem_group cofem_group;
+int cofem_group_create(cofem_group** out, int nranks);  /* 1 <= nranks <= 8 */
+int cofem_group_destroy(cofem_group* group);            /* after its contexts */
+int cofem_group_abort(cofem_group* group);              /* a host-side failure: release the ranks */
+int cofem_set_group(cofem_ctx* ctx, cofem_group* group, int rank);
 
 /* ---- operator applications (host float64 buffers) ---------------------
  * LinearOperator.apply / apply_adjoint, operators.py:61-71.            */

@@ -45,6 +45,10 @@ EXPORTED = (
     "cofem_get_dictionary",
     "cofem_nccl_get_unique_id",
     "cofem_set_comm",
+    "cofem_group_create",
+    "cofem_group_destroy",
+    "cofem_group_abort",
+    "cofem_set_group",
     "cofem_apply",
     "cofem_apply_adjoint",
     "cofem_system_apply",
@@ -139,6 +143,10 @@ def load():
         "cofem_get_dictionary": (c_int, [vp, POINTER(c_float)]),
         "cofem_nccl_get_unique_id": (c_int, [vp]),
         "cofem_set_comm": (c_int, [vp, vp, c_int, c_int]),
+        "cofem_group_create": (c_int, [POINTER(vp), c_int]),
+        "cofem_group_destroy": (c_int, [vp]),
+        "cofem_group_abort": (c_int, [vp]),
+        "cofem_set_group": (c_int, [vp, vp, c_int]),
         "cofem_apply": (c_int, [vp, POINTER(c_double), c_int64, POINTER(c_double)]),
         "cofem_apply_adjoint": (c_int, [vp, POINTER(c_double), c_int64, POINTER(c_double)]),
         "cofem_system_apply": (c_int, [vp, c_double, POINTER(c_double), POINTER(c_double), c_int64,
@@ -267,15 +275,24 @@ class Context:
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         check(load().cofem_set_comm(self.handle, ctypes.cast(buf, c_void_p), int(nranks), int(rank)))
 
+    def set_group(self, group, rank):
+        """Join an in-process ShardGroup as `rank` (instead of an NCCL communicator)."""
+        check(load().cofem_set_group(self.handle, group.handle, int(rank)))
+        self.group = group  # the group must outlive its contexts
+
     # -- operator applications (float64 host blocks)
     def apply(self, V):
         V = np.ascontiguousarray(V, dtype=np.float64)
+        if V.ndim != 2 or V.shape[0] != self.n_cols:
+            raise ValueError(f"apply: expected ({self.n_cols}, q), got {V.shape}")
         out = np.empty((self.n_rows, V.shape[1]))
         check(load().cofem_apply(self.handle, _dp(V), V.shape[1], _dp(out)))
         return out
 
     def apply_adjoint(self, U):
         U = np.ascontiguousarray(U, dtype=np.float64)
+        if U.ndim != 2 or U.shape[0] != self.n_rows:
+            raise ValueError(f"apply_adjoint: expected ({self.n_rows}, q), got {U.shape}")
         out = np.empty((self.n_cols, U.shape[1]))
         check(load().cofem_apply_adjoint(self.handle, _dp(U), U.shape[1], _dp(out)))
         return out
@@ -366,6 +383,33 @@ class Context:
         t = TimingC()
         check(load().cofem_bench_iterations(self.handle, int(n_iter), 1 if time_kernels else 0, ctypes.byref(t)))
         return {k: getattr(t, k) for k, _ in TimingC._fields_}
+
+
+class ShardGroup:
+    """cofem_group: the exchanges of a sharded problem between contexts driven
+    from host threads of one process (one thread per rank)."""
+
+    def __init__(self, nranks):
+        h = c_void_p()
+        check(load().cofem_group_create(ctypes.byref(h), int(nranks)))
+        self._h = h
+        self.nranks = int(nranks)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def abort(self):
+        """Release ranks waiting at the group's barriers (a rank failed on the host)."""
+        check(load().cofem_group_abort(self._h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None:
+                load().cofem_group_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_max, floor_eps, max_steps,

@@ -11,6 +11,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -64,6 +67,11 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
+  // point-to-point (halo exchange of time-sharded convolutions)
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi g_nccl;
 
@@ -80,6 +88,10 @@ int nccl_load() {
   g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+  g_nccl.send = (decltype(g_nccl.send))dlsym(h, "ncclSend");
+  g_nccl.recv = (decltype(g_nccl.recv))dlsym(h, "ncclRecv");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy;
   return g_nccl.ok ? 0 : fail(COFEM_ENCCL, "libnccl missing symbols");
 }
@@ -152,6 +164,26 @@ struct SplitPlan {
   int per_split = 0;  // rows (bwd) or columns (fwd) per split, multiple of the tile depth
 };
 
+// In-process shard group: the ranks of one sharded problem driven from host
+// threads of ONE process (one context per rank, on one or several devices).
+// It implements the same exchanges as the NCCL communicator -- all-reduce
+// (sum / max) and the neighbour halo send/recv -- with stream-ordered events:
+// a rank records "ready" after producing its buffer, a host barrier publishes
+// the buffers, every rank's stream waits on the peers' events and reads the
+// peers' buffers directly (device or peer memory), then a second event /
+// barrier round keeps a buffer alive until every peer has read it.  No kernel
+// ever waits on another rank's kernel.
+struct cofem_group {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  std::vector<void*> bufs;
+  std::vector<cudaEvent_t> ready, done;
+};
+
 struct cofem_ctx {
   int device = 0, prec = COFEM_FP32;
   int64_t N = 0, D = 0, Np = 0, Dp = 0;
@@ -205,6 +237,7 @@ struct cofem_ctx {
   int conv_L = 0, conv_lpad = 0;                     // taps, taps-1 rounded up to 64
   int8_t *band_fwd = nullptr, *band_adj = nullptr;   // [4][128][128 + lpad] digit planes
   double* hrows = nullptr;                           // Dp copies of the band's power-of-two scale
+  std::vector<double> taps;                          // host copy (column norms of a time shard)
   CUtensorMap map_band_fwd{}, map_band_adj{};
   // float64 FFT path (precision FP64, <= 512 taps): overlap-save spectra of h
   // and of reversed h (1024 points, 1/1024 folded in); FFT twiddles in dct_wN
@@ -222,7 +255,13 @@ struct cofem_ctx {
 
   // multi-GPU
   ncclComm_t comm = nullptr;
+  cofem_group* lgroup = nullptr;  // in-process shard group (instead of comm)
+  void* lg_tmp = nullptr;         // its all-reduce result staging
+  size_t lg_tmp_cap = 0;
   int nranks = 1, rank = 0;
+  // time-sharded convolution: operand planes carry the neighbours' halo rows
+  // (pq: conv_lpad rows before the data for rank > 0; vq: after it for rank < nranks-1)
+  int8_t* pq_base = nullptr;
 
   // bench state
   bool bench_ready = false;
@@ -388,10 +427,125 @@ int ensure_groups(cofem_ctx* c, int n) {
   return 0;
 }
 
-int allreduce(cofem_ctx* c, void* buf, size_t count, ncclDataType_t dt) {
-  if (c->nranks <= 1 || !c->comm) return 0;
-  ncclResult_t r = g_nccl.allReduce(buf, buf, count, dt, ncclSum, c->comm, c->stream);
+// ---- exchanges: NCCL communicator or in-process shard group ---------------
+int group_barrier(cofem_group* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  if (g->broken) return fail(COFEM_ENCCL, "shard group broken (a rank failed)");
+  const uint64_t my = g->gen;
+  if (++g->arrived == g->n) {
+    g->arrived = 0;
+    g->gen++;
+    g->cv.notify_all();
+    return 0;
+  }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(300), [&] { return g->gen != my || g->broken; })) {
+    g->broken = true;
+    g->cv.notify_all();
+    return fail(COFEM_ENCCL, "shard group barrier timed out");
+  }
+  if (g->gen == my) return fail(COFEM_ENCCL, "shard group broken (a rank failed)");
+  return 0;
+}
+
+void group_break(cofem_group* g) {
+  if (!g) return;
+  std::lock_guard<std::mutex> lk(g->m);
+  g->broken = true;
+  g->cv.notify_all();
+}
+
+// publish `mine`; run work(bufs) on c->stream once every rank's buffer is
+// ready; return once every rank has finished reading this rank's buffer
+template <class F>
+int group_phase(cofem_ctx* c, void* mine, F&& work) {
+  cofem_group* g = c->lgroup;
+  const int r = c->rank;
+  CK(cudaEventRecord(g->ready[r], c->stream));
+  g->bufs[r] = mine;
+  CKR(group_barrier(g));
+  std::vector<void*> bufs(g->bufs);
+  for (int i = 0; i < g->n; ++i)
+    if (i != r) CK(cudaStreamWaitEvent(c->stream, g->ready[i], 0));
+  int rc = work(bufs);
+  if (rc) {
+    group_break(g);
+    return rc;
+  }
+  CK(cudaEventRecord(g->done[r], c->stream));
+  CKR(group_barrier(g));
+  for (int i = 0; i < g->n; ++i)
+    if (i != r) CK(cudaStreamWaitEvent(c->stream, g->done[i], 0));
+  return 0;
+}
+
+int group_allreduce(cofem_ctx* c, void* buf, size_t count, ncclDataType_t dt, ncclRedOp_t op) {
+  const size_t es = dt == ncclFloat32 ? 4 : 8;
+  if (dt != ncclFloat32 && dt != ncclFloat64 && dt != ncclUint64) return fail(COFEM_EINVAL, "group all-reduce type");
+  if (c->lg_tmp_cap < count * es) {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->lg_tmp) cudaFree(c->lg_tmp);
+    c->lg_tmp = nullptr;
+    c->lg_tmp_cap = 0;
+    CK(cudaMalloc(&c->lg_tmp, count * es));
+    c->lg_tmp_cap = count * es;
+  }
+  const int mx = op == ncclMax ? 1 : 0;
+  CKR(group_phase(c, buf, [&](std::vector<void*>& bufs) -> int {
+    GroupPtrs gp{};
+    for (int i = 0; i < c->nranks; ++i) gp.p[i] = bufs[i];
+    const int grid = (int)std::min<size_t>((count + 255) / 256, 4 * (size_t)c->sm_count);
+    if (dt == ncclFloat64) k_group_reduce<double><<<grid, 256, 0, c->stream>>>(gp, c->nranks, count, mx, (double*)c->lg_tmp);
+    else if (dt == ncclFloat32) k_group_reduce<float><<<grid, 256, 0, c->stream>>>(gp, c->nranks, count, mx, (float*)c->lg_tmp);
+    else k_group_reduce<unsigned long long><<<grid, 256, 0, c->stream>>>(gp, c->nranks, count, mx,
+                                                                         (unsigned long long*)c->lg_tmp);
+    c->launches++;
+    CK(cudaGetLastError());
+    return 0;
+  }));
+  CK(cudaMemcpyAsync(buf, c->lg_tmp, count * es, cudaMemcpyDeviceToDevice, c->stream));
+  return 0;
+}
+
+int allreduce(cofem_ctx* c, void* buf, size_t count, ncclDataType_t dt, ncclRedOp_t op = ncclSum) {
+  if (c->nranks <= 1) return 0;
+  if (c->lgroup) return group_allreduce(c, buf, count, dt, op);
+  if (!c->comm) return 0;
+  ncclResult_t r = g_nccl.allReduce(buf, buf, count, dt, op, c->comm, c->stream);
   if (r != ncclSuccess) return fail(COFEM_ENCCL, std::string("ncclAllReduce: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+  return 0;
+}
+
+// neighbour exchange along the rank order: dir +1 sends `send` to rank+1 and
+// receives `recv` from rank-1; dir -1 the reverse.  Ends of the chain keep
+// their (zero) halo.
+int halo_exchange(cofem_ctx* c, const void* send, void* recv, size_t bytes, int dir) {
+  if (c->nranks <= 1) return 0;
+  const int to = c->rank + dir, from = c->rank - dir;
+  const bool has_to = to >= 0 && to < c->nranks, has_from = from >= 0 && from < c->nranks;
+  if (c->lgroup) {
+    return group_phase(c, const_cast<void*>(send), [&](std::vector<void*>& bufs) -> int {
+      if (has_from) CK(cudaMemcpyAsync(recv, bufs[from], bytes, cudaMemcpyDefault, c->stream));
+      return 0;
+    });
+  }
+  if (!c->comm) return 0;
+  if (!g_nccl.send || !g_nccl.recv || !g_nccl.groupStart || !g_nccl.groupEnd)
+    return fail(COFEM_ENCCL, "libnccl lacks ncclSend / ncclRecv");
+  ncclResult_t r = g_nccl.groupStart();
+  if (r == ncclSuccess && has_to) r = g_nccl.send(send, bytes, ncclInt8, to, c->comm, c->stream);
+  if (r == ncclSuccess && has_from) r = g_nccl.recv(recv, bytes, ncclInt8, from, c->comm, c->stream);
+  ncclResult_t r2 = g_nccl.groupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return fail(COFEM_ENCCL, std::string("halo send/recv: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+  return 0;
+}
+
+// the all-reduce of a dense shard's partial Phi_r P_r; its column maxima are
+// no longer those of the local partial
+int reduce_partial_v(cofem_ctx* c, size_t count, ncclDataType_t dt) {
+  if (c->kind != 0 || c->nranks <= 1) return 0;
+  CKR(allreduce(c, c->V, count, dt));
+  c->v_colmax_valid = false;
   return 0;
 }
 
@@ -456,7 +610,7 @@ int oz_init_kernels() {
 template <typename T, int QW>
 int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int64_t k_pad, const double* pre,
                 int8_t* planes, unsigned long long* colmax, bool colmax_ready, unsigned long long* reset,
-                const Status* st) {
+                const Status* st, bool global_max = false) {
   if (!colmax_ready) {
     CK(cudaMemsetAsync(colmax, 0, QW * sizeof(unsigned long long), c->stream));
     const int bs = QW * (256 / QW);
@@ -464,6 +618,9 @@ int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int
                                                                              st);
     c->launches++;
   }
+  // a time-sharded operand: every rank quantises with the global column
+  // maxima, so halo rows received from a neighbour share this rank's scales
+  if (global_max && c->nranks > 1) CKR(allreduce(c, colmax, QW, ncclUint64, ncclMax));
   const int64_t nchunk = k_pad / oz::QCHUNK_K;  // one warp each, 8 warps per block
   oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>((nchunk + 7) / 8, 16 * c->sm_count), 256, 0, c->stream>>>(
       k_real, k_pad, ldm, qoff, M, pre, colmax, c->opscale, planes, reset, st);
@@ -577,23 +734,47 @@ void launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_
   }
 }
 
+// V -> operand planes for Phi^T (global column maxima), then the halo: the
+// right neighbour's first lpad rows land after this shard's Np rows
+template <int QW>
+int conv_quantize_v(cofem_ctx* c, const double* v, const Status* st) {
+  const int slot = QW / 8;
+  const int64_t lp = c->conv_lpad;
+  const bool right = c->nranks > 1 && c->rank < c->nranks - 1;
+  if (!c->map_v_ok[slot]) {
+    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np + (right ? lp : 0), QW, QW));
+    c->map_v_ok[slot] = true;
+  }
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
+                               nullptr, st, true)));
+  c->v_colmax_valid = false;
+  return halo_exchange(c, c->vq, c->vq + c->Np * 4 * QW, (size_t)lp * 4 * QW, -1);
+}
+
 template <int QW>
 int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, const Status* st) {
   CKR(oz_init_kernels<QW>());
   const int slot = QW / 8;
+  const int64_t lp = c->conv_lpad;
+  const bool left = c->nranks > 1 && c->rank > 0;  // a left neighbour's rows precede the data
   if (!c->map_p_ok[slot]) {
-    CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
+    if (left) CKR(encode_u8_kblocked(&c->map_p[slot], c->pq - lp * 4 * QW, lp + c->Dp, QW, QW));
+    else CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
     c->map_p_ok[slot] = true;
   }
   CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
-                               c->p_colmax_valid, c->vcolmax, st)));
+                               c->p_colmax_valid, c->vcolmax, st, true)));
+  // halo: this shard's last lpad operand rows become the right neighbour's
+  // first window rows (K-blocked planes: lpad / 64 contiguous blocks)
+  CKR(halo_exchange(c, c->pq + std::max<int64_t>(c->D - lp, 0) * 4 * QW, c->pq - lp * 4 * QW,
+                    (size_t)lp * 4 * QW, +1));
   const int nmb = (int)(c->Np / oz::BM);
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  launch_band<QW>(c, c->map_band_fwd, c->map_p[slot], nmb, oz::BM + c->conv_lpad, -c->conv_lpad, vout, c->Np,
-                  c->N, c->vcolmax, st);
+  launch_band<QW>(c, c->map_band_fwd, c->map_p[slot], nmb, oz::BM + c->conv_lpad, left ? 0 : -c->conv_lpad, vout,
+                  c->Np, c->N, c->vcolmax, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -609,20 +790,13 @@ int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, c
 template <int QW>
 int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
   CKR(oz_init_kernels<QW>());
-  const int slot = QW / 8;
-  if (!c->map_v_ok[slot]) {
-    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
-    c->map_v_ok[slot] = true;
-  }
-  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
-                               nullptr, st)));
-  c->v_colmax_valid = false;
+  CKR(conv_quantize_v<QW>(c, v, st));
   const int nmb = (int)(c->Dp / oz::BM);
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  launch_band<QW>(c, c->map_band_adj, c->map_v[slot], nmb, oz::BM + c->conv_lpad, 0, (double*)c->ppart, c->Dp,
+  launch_band<QW>(c, c->map_band_adj, c->map_v[QW / 8], nmb, oz::BM + c->conv_lpad, 0, (double*)c->ppart, c->Dp,
                   c->D, nullptr, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
@@ -646,14 +820,7 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   const size_t sm = oz::BandCfg<QW>::smem(nk);
   if (sm > 227 * 1024 - 64) return 1;  // (the last-block fold adds a little static smem)
   CKR(oz_init_kernels<QW>());
-  const int slot = QW / 8;
-  if (!c->map_v_ok[slot]) {
-    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
-    c->map_v_ok[slot] = true;
-  }
-  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
-                               nullptr, st)));
-  c->v_colmax_valid = false;
+  CKR(conv_quantize_v<QW>(c, v, st));
   const int nmb = (int)(c->Dp / oz::BM);
   const int grid = std::min(nmb, std::min(c->sm_count, c->nblk_elem));
   static bool attr = false;
@@ -668,7 +835,7 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   Scalars sc = c->sc();
   CK(cudaGetLastError());
   oz::band_kernel<QW, true><<<grid, oz::NTHREADS, sm, c->stream>>>(
-      c->map_band_adj, c->map_v[slot], nmb, nk, 0, c->hrows, c->opscale, (double*)c->Psi + qoff, c->D, nullptr, st,
+      c->map_band_adj, c->map_v[QW / 8], nmb, nk, 0, c->hrows, c->opscale, (double*)c->Psi + qoff, c->D, nullptr, st,
       (const double*)c->P + qoff, c->ldq, c->alpha, beta, sc.pi + qoff, sc.partials, sc.ticket + 1);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
@@ -922,7 +1089,7 @@ int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
   for (int qoff = 0; qoff < c->ldq; qoff += QCHUNK) {
     const int qpc = chunk_width(c->ldq, qoff);
     CKR(fwd_chunk<T>(c, qpc, (const T*)c->P, c->ldq, qoff, (T*)c->V, st));
-    CKR(allreduce(c, c->V, (size_t)c->Np * qpc, nccl_t<T>()));
+    CKR(reduce_partial_v(c, (size_t)c->Np * qpc, nccl_t<T>()));
     if constexpr (std::is_same<T, double>::value) {
       if (c->kind == 1) {  // convolution: combine fused into the band epilogue
         int rc = 1;
@@ -1209,7 +1376,7 @@ int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
   for (int qoff = 0; qoff < ldq; qoff += QCHUNK) {
     const int qpc = chunk_width(ldq, qoff);
     CKR(fwd_chunk<T>(c, qpc, (const T*)c->P, ldq, qoff, (T*)c->V, nullptr));
-    CKR(allreduce(c, c->V, (size_t)c->Np * qpc, nccl_t<T>()));
+    CKR(reduce_partial_v(c, (size_t)c->Np * qpc, nccl_t<T>()));
     const int64_t qn = std::min<int64_t>(qpc, q - qoff);
     if (qn <= 0) break;
     chunk.assign((size_t)c->N * qn, 0.0);
@@ -1631,6 +1798,7 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   c->global_cols = dim;
   c->conv_L = (int)ntaps;
   c->conv_lpad = (int)round_up(ntaps - 1, oz::KT);
+  c->taps.assign(taps, taps + ntaps);
   auto bail = [&](int rc) {
     cofem_destroy(c);
     return rc;
@@ -1696,12 +1864,18 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
     return 0;
   }
   // operand buffers of the int8 path
-  if (cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp) != cudaSuccess ||
-      cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np) != cudaSuccess ||
+  // operand planes with room for a neighbour's halo rows (time sharding):
+  // lpad rows before P's planes, lpad rows after V's
+  const size_t lpb = (size_t)4 * QCHUNK * c->conv_lpad;
+  if (cudaMalloc(&c->pq_base, (size_t)4 * QCHUNK * c->Dp + lpb) != cudaSuccess ||
+      cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np + lpb) != cudaSuccess ||
       cudaMalloc(&c->opscale, QCHUNK * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "operand buffers"));
+  cudaMemset(c->pq_base, 0, (size_t)4 * QCHUNK * c->Dp + lpb);
+  cudaMemset(c->vq, 0, (size_t)4 * QCHUNK * c->Np + lpb);
+  c->pq = c->pq_base + lpb;
   // band digit planes: lower band (Phi) and upper band (Phi^T), one scale 2^e >= max |h|
   const double hs = host_pow2_ceil(hmax);
   const int nk = oz::BM + c->conv_lpad;
@@ -1827,9 +2001,9 @@ int cofem_destroy(cofem_ctx* c) {
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
-                  c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
+                  c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr};
+                  c->cf_H, c->cf_Hr, c->lg_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -1891,8 +2065,96 @@ int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {
   if (!c) return fail(COFEM_EINVAL, "null context");
   if (col_offset < 0 || col_offset + c->D > global_cols || col_offset % 4 != 0)
     return fail(COFEM_EINVAL, "shard must be 4-aligned and inside the global columns");
+  if (c->kind == 2 && (col_offset != 0 || global_cols != c->D))
+    return fail(COFEM_EINVAL, "2-D DCT dictionaries are not sharded");
+  if (c->kind == 1) {
+    // time shard [t0, t0 + D) of a length-global_cols sequence: boundaries on
+    // PAD-row multiples, and a shard followed by another one holds at least
+    // the halo (the neighbours exchange only lpad rows)
+    if (col_offset % PAD != 0) return fail(COFEM_EINVAL, "convolution shards start on 256-sample boundaries");
+    if (col_offset + c->D < global_cols && (c->D % PAD != 0 || c->D < c->conv_lpad))
+      return fail(COFEM_EINVAL, "inner convolution shards need a multiple of 256 samples and >= the filter halo");
+    if (c->conv_fft && global_cols != c->D) return fail(COFEM_EINVAL, "the FP64 FFT convolution path is not sharded");
+    // column j of the global Toeplitz matrix holds taps[0 : min(L, global - j)]
+    const int64_t L = (int64_t)c->taps.size();
+    std::vector<double> csq(c->Dp, 0.0), cum(L + 1, 0.0);
+    for (int64_t m = 0; m < L; ++m) cum[m + 1] = cum[m] + c->taps[m] * c->taps[m];
+    for (int64_t j = 0; j < c->D; ++j) csq[j] = cum[std::min<int64_t>(L, global_cols - col_offset - j)];
+    CKR(set_dev(c));
+    CK(cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  }
   c->col_offset = col_offset;
   c->global_cols = global_cols;
+  return 0;
+}
+
+namespace {
+// shared by cofem_set_comm / cofem_set_group: what may be sharded, and how
+int attach_ranks(cofem_ctx* c, int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
+  if (nranks > 1) {
+    if (c->kind == 2) return fail(COFEM_EINVAL, "2-D DCT dictionaries run on one GPU (not sharded)");
+    if (c->kind == 1 && c->conv_fft) return fail(COFEM_EINVAL, "the FP64 FFT convolution path runs on one GPU");
+    if (c->kind == 1 && c->col_offset + c->D < c->global_cols && rank == nranks - 1)
+      return fail(COFEM_EINVAL, "the last rank must hold the end of the sequence");
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  // operand maps depend on the neighbours (halo extents): re-encode on next use
+  for (int i = 0; i < 5; ++i) c->map_p_ok[i] = c->map_v_ok[i] = false;
+  return 0;
+}
+}  // namespace
+
+int cofem_group_create(cofem_group** out, int nranks) {
+  if (!out) return fail(COFEM_EINVAL, "null argument");
+  *out = nullptr;
+  if (nranks < 1 || nranks > GROUP_MAX) return fail(COFEM_EINVAL, "a shard group holds 1..8 ranks");
+  cofem_group* g = new cofem_group();
+  g->n = nranks;
+  g->bufs.assign(nranks, nullptr);
+  g->ready.assign(nranks, nullptr);
+  g->done.assign(nranks, nullptr);
+  *out = g;
+  return 0;
+}
+
+int cofem_group_destroy(cofem_group* g) {
+  if (!g) return 0;
+  for (cudaEvent_t e : g->ready)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->done)
+    if (e) cudaEventDestroy(e);
+  delete g;
+  return 0;
+}
+
+int cofem_group_abort(cofem_group* g) {
+  group_break(g);
+  return 0;
+}
+
+int cofem_set_group(cofem_ctx* c, cofem_group* g, int rank) {
+  CKR(check_ctx(c, false));
+  if (!g) return fail(COFEM_EINVAL, "null group");
+  if (c->comm) return fail(COFEM_ESTATE, "context already joined an NCCL communicator");
+  if (rank < 0 || rank >= g->n) return fail(COFEM_EINVAL, "bad rank");
+  if (g->ready[rank]) return fail(COFEM_ESTATE, "rank already attached to this group");
+  CKR(attach_ranks(c, g->n, rank));
+  CKR(set_dev(c));
+  // peers on other devices are read directly: enable peer access both ways
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  for (int d = 0; d < ndev; ++d)
+    if (d != c->device) {
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, c->device, d);
+      if (ok) cudaDeviceEnablePeerAccess(d, 0);
+    }
+  cudaGetLastError();  // (already-enabled peers)
+  CK(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
+  c->lgroup = g;
   return 0;
 }
 
@@ -1929,8 +2191,8 @@ int cofem_nccl_get_unique_id(void* out128) {
 
 int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
   CKR(check_ctx(c, false));
-  if (c->kind != 0 && nranks > 1) return fail(COFEM_EINVAL, "sharding is implemented for dense dictionaries only");
-  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
+  if (c->lgroup) return fail(COFEM_ESTATE, "context already joined a shard group");
+  CKR(attach_ranks(c, nranks, rank));
   CKR(nccl_load());
   ncclUniqueId id;
   memcpy(&id, uid, sizeof(id));
@@ -1943,23 +2205,31 @@ int cofem_set_comm(cofem_ctx* c, const void* uid, int nranks, int rank) {
 
 #define DISPATCH(c, fn, ...) ((c)->prec == COFEM_FP32 ? fn<float>(__VA_ARGS__) : fn<double>(__VA_ARGS__))
 
+namespace {
+// a rank that fails outside an exchange releases the group's other ranks
+int grouped(cofem_ctx* c, int rc) {
+  if (rc && rc != COFEM_EDIVERGED && c->lgroup) group_break(c->lgroup);
+  return rc;
+}
+}  // namespace
+
 int cofem_apply(cofem_ctx* c, const double* V, int64_t q, double* out) {
   CKR(check_ctx(c));
   if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
-  return DISPATCH(c, apply_impl, c, V, q, out);
+  return grouped(c, DISPATCH(c, apply_impl, c, V, q, out));
 }
 
 int cofem_apply_adjoint(cofem_ctx* c, const double* U, int64_t q, double* out) {
   CKR(check_ctx(c));
   if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
-  return DISPATCH(c, adjoint_impl, c, U, q, out);
+  return grouped(c, DISPATCH(c, adjoint_impl, c, U, q, out));
 }
 
 int cofem_system_apply(cofem_ctx* c, double beta, const double* alpha, const double* V, int64_t q, double* out) {
   CKR(check_ctx(c));
   if (q < 1) return fail(COFEM_EINVAL, "q must be >= 1");
   if (!(beta > 0)) return fail(COFEM_EINVAL, "beta must be positive");
-  return DISPATCH(c, system_apply_impl, c, beta, alpha, V, q, out);
+  return grouped(c, DISPATCH(c, system_apply_impl, c, beta, alpha, V, q, out));
 }
 
 int cofem_column_sq_norms(cofem_ctx* c, double* out) {
@@ -2035,7 +2305,7 @@ int cofem_pcg_solve(cofem_ctx* c, double beta, const double* alpha, const double
   if (!alpha || !minv || !B || !X || !cg || !rep || q < 1) return fail(COFEM_EINVAL, "null argument");
   if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
   if (n_groups < 1 || (n_groups > 1 && !group_of_col)) return fail(COFEM_EINVAL, "bad groups");
-  return DISPATCH(c, pcg_solve_impl, c, beta, alpha, minv, n_groups, group_of_col, B, q, cg, X, rep, breakdown);
+  return grouped(c, DISPATCH(c, pcg_solve_impl, c, beta, alpha, minv, n_groups, group_of_col, B, q, cg, X, rep, breakdown));
 }
 
 int cofem_run(cofem_ctx* c, const double* y, double beta, const cofem_em_config* em, const cofem_cg_config* cg,
@@ -2047,8 +2317,8 @@ int cofem_run(cofem_ctx* c, const double* y, double beta, const cofem_em_config*
   if (em->probes + 1 > 1024) return fail(COFEM_EINVAL, "too many probes");
   if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
   if (!(beta > 0) || !std::isfinite(beta)) return fail(COFEM_EINVAL, "beta must be positive and finite");
-  return DISPATCH(c, run_impl, c, y, beta, em, cg, theta, probes, dseed, alpha, mu, s, cg_steps, cg_residuals,
-                  failed_iteration, failed_step);
+  return grouped(c, DISPATCH(c, run_impl, c, y, beta, em, cg, theta, probes, dseed, alpha, mu, s, cg_steps,
+                             cg_residuals, failed_iteration, failed_step));
 }
 
 int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const* ys, const double* betas,

@@ -601,4 +601,23 @@ __global__ void k_colsq(const float* phi, int64_t ld, int64_t n_real, int64_t d_
   out[j] = s;
 }
 
+// ---- in-process shard group (cofem_group): element-wise reduction over the
+// ranks' buffers, in rank order so every rank gets the same bits.  op 0 sum,
+// 1 max (used on non-negative doubles' bit patterns as uint64).
+constexpr int GROUP_MAX = 8;
+struct GroupPtrs {
+  const void* p[GROUP_MAX];
+};
+template <typename T>
+__global__ void k_group_reduce(GroupPtrs src, int n, int64_t count, int op, T* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    T a = ((const T*)src.p[0])[i];
+    for (int r = 1; r < n; ++r) {
+      const T b = ((const T*)src.p[r])[i];
+      a = op ? (b > a ? b : a) : a + b;
+    }
+    out[i] = a;
+  }
+}
+
 }  // namespace cofem

@@ -1,0 +1,134 @@
+"""Sharded execution on one GPU through the in-process shard group.
+
+The ranks of a sharded problem run as host threads of one process, each on
+its own context and stream; the library's exchanges (all-reduce sum / max,
+neighbour halo send/recv) run between them through stream-ordered events --
+the same code path as the NCCL communicator up to the transport, so the
+sharding arithmetic (column shards of a dense Phi, time shards of a
+convolution with halo exchange) is checked on the one available GPU.
+
+* convolution apply / adjoint: time shards reproduce the unsharded banded
+  contraction BITWISE (the ranks agree on the int8 scales through the max
+  all-reduce, and every output row sees the same operand window);
+* convolution CoFEM: same CG step counts as the unsharded run, mu / alpha
+  equal up to the summation order of the PCG dot products (~5e-9);
+* dense CoFEM: column shards (each with its own row scales) against the
+  float64 oracle, with the north_star tolerances.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import cofem_oracle as O
+from paper_2105_10439_b200 import ConvolutionOperator, DenseOperator, SblProblem, run_cofem
+from paper_2105_10439_b200 import simulate as S
+from paper_2105_10439_b200.distributed import (
+    run_cofem_threaded,
+    run_threaded,
+    threaded_contexts,
+    time_shards,
+)
+
+pytestmark = pytest.mark.gpu
+PRUNE = 1e6
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def exp_taps(ntaps, tau=20.0):
+    h = np.exp(-np.arange(ntaps) / tau)
+    return h / np.linalg.norm(h)
+
+
+def sharded_apply(op, X, world, adjoint=False):
+    contexts, shards = threaded_contexts(op, "ozaki", [0] * world)
+    try:
+        parts = run_threaded(world, lambda r: (contexts[r].apply_adjoint if adjoint else contexts[r].apply)(
+            np.ascontiguousarray(X[shards[r][0]:shards[r][1]])), contexts[0].group)
+    finally:
+        for c in contexts:
+            c.close()
+    return np.concatenate(parts, axis=0)
+
+
+@pytest.mark.parametrize("dim,ntaps,world,q", [(4096, 256, 2, 31), (4096, 256, 3, 8), (5000, 100, 4, 21),
+                                               (2048, 257, 2, 1), (1536, 64, 5, 40)])
+def test_time_sharded_convolution_apply_is_bitwise(dim, ntaps, world, q):
+    h = exp_taps(ntaps)
+    op = ConvolutionOperator.from_taps(dim, h)
+    rng = np.random.default_rng(dim + world)
+    V = rng.standard_normal((dim, q))
+    full_f, full_a = op.apply(V), op.apply_adjoint(V)
+    np.testing.assert_array_equal(sharded_apply(op, V, world), full_f)
+    np.testing.assert_array_equal(sharded_apply(op, V, world, adjoint=True), full_a)
+    # and both are the convolution (float64 numpy) to the int8 path's accuracy
+    ref = np.stack([np.convolve(V[:, k], h)[:dim] for k in range(q)], axis=1)
+    assert rel(full_f, ref) <= 1e-8
+
+
+def test_time_shards_geometry():
+    assert time_shards(4096, 2, 256) == [(0, 2048), (2048, 4096)]
+    s = time_shards(2**22, 8, 256)
+    assert all(a % 256 == 0 for a, _ in s) and s[-1][1] == 2**22
+    with pytest.raises(ValueError):
+        time_shards(1024, 4, 513)  # 256-sample shards shorter than the 512-row halo
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_sharded_convolution_cofem_matches_unsharded(world):
+    c = S.ConvConfig("conv-shard", 8192, 256, 20.0, 0.01, 0.05, 20, 3, 200, 1e-5)
+    prob, z = S.conv_problem(c)
+    cfg = c.cofem_config("ozaki")
+    st1, est1, d1 = run_cofem(prob, cfg)
+    st2, est2, d2 = run_cofem_threaded(prob, cfg, devices=[0] * world)
+    assert [d["cg_steps"] for d in d1] == [d["cg_steps"] for d in d2]
+    # the shards' dot products sum in another order; the int8 operand rounding
+    # turns those last-bit differences into ~1e-9-level ones
+    assert rel(est2.mu, est1.mu) <= 1e-7 and rel(st2.alpha, st1.alpha) <= 1e-7
+    np.testing.assert_array_equal(st2.alpha < PRUNE, st1.alpha < PRUNE)
+
+
+@pytest.mark.parametrize("precision,world", [("ozaki", 2), ("ozaki", 3), ("fp64", 2)])
+def test_column_sharded_dense_cofem_matches_oracle(precision, world):
+    """Dense column shards: the partial Phi_r P_r all-reduce, then each rank
+    re-derives the V column maxima for its Phi_r^T quantisation."""
+    rng = np.random.default_rng(5)
+    n, d = 512, 2048
+    phi = (rng.standard_normal((n, d)) / np.sqrt(n)).astype(np.float32)
+    z = np.zeros(d)
+    z[rng.choice(d, 40, replace=False)] = rng.standard_normal(40)
+    y = phi.astype(np.float64) @ z + 0.01 * rng.standard_normal(n)
+    prob = SblProblem(y, DenseOperator(phi), 1e4)
+    from paper_2105_10439_b200 import CgConfig, CofemConfig
+
+    cfg = CofemConfig(iterations=4, probes=12, seed=1, cg=CgConfig(max_steps=200, tolerance=1e-5, precision=precision))
+    st, est, diag = run_cofem_threaded(prob, cfg, devices=[0] * world)
+    ocfg = O.CofemConfig(iterations=4, probes=12, seed=1, cg=O.CgConfig(max_steps=200, tolerance=1e-5))
+    alpha, mu, s, odiag = O.run_cofem(O.dense_op(phi), y, 1e4, ocfg)
+    assert rel(est.mu, mu) <= 1e-4 and rel(st.alpha, alpha) <= 1e-4
+    # ~180-step solves at beta = 1e4: 1e-9-level contraction differences move
+    # the stopping step by a step or two (the unsharded int8 path does too)
+    assert np.all(np.abs(np.array([x["cg_steps"] for x in diag]) - [x["cg_steps"] for x in odiag]) <= 3)
+    np.testing.assert_array_equal(st.alpha < PRUNE, alpha < PRUNE)
+
+
+def test_group_failure_releases_the_other_ranks():
+    """A rank that fails outside an exchange breaks the group: the others
+    return an error instead of waiting at the next barrier."""
+    op = ConvolutionOperator.from_taps(2048, exp_taps(64))
+    contexts, shards = threaded_contexts(op, "ozaki", [0, 0])
+    V = np.ones((2048, 3))
+
+    def body(r):
+        if r == 1:
+            raise RuntimeError("host-side failure before the first exchange")
+        return contexts[r].apply(V[shards[r][0]:shards[r][1]])
+
+    try:
+        with pytest.raises(RuntimeError, match="host-side failure"):
+            run_threaded(2, body, contexts[0].group)
+    finally:
+        for c in contexts:
+            c.close()
