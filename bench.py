@@ -342,29 +342,54 @@ def run_ours_conv(args):
     from paper_2105_10439_b200 import simulate as S
 
     world, rank, local = dist_env()
-    if world > 1:
-        raise SystemExit("structured dictionaries run on one GPU this round (no sharded halo exchange yet)")
     is_conv = args.config in S.CONV_CONFIGS
+    if world > 1 and not is_conv:
+        raise SystemExit("2-D DCT dictionaries run on one GPU (their transposes are not sharded)")
     c = S.CONV_CONFIGS[args.config] if is_conv else S.DCT_CONFIGS[args.config]
     prob, z = S.conv_problem(c) if is_conv else S.dct2_problem(c)
     prec = args.precision if args.precision in ("ozaki", "fp64") else "ozaki"
-    ctx = prob.op.context(prec)
+    dist, device, y_local = None, 0, np.asarray(prob.y)
+    if world > 1:
+        # time shards: each rank holds its samples; halo send/recv + scalar all-reduces over NCCL
+        import torch.distributed as dist
+
+        from paper_2105_10439_b200.distributed import ShardedContext, local_observation
+
+        device = local
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        sharded = ShardedContext.for_operator(prob.op, "ozaki", device)
+        ctx = sharded.ctx
+        t0_, t1_ = sharded.col_range
+        y_local = local_observation(prob.op, prob.y, t0_, t1_)
+    else:
+        ctx = prob.op.context(prec)
     dseed = 0xC0FE
-    ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
+    ctx.bench_prepare(y_local, c.beta, c.K, c.U, c.tol, seed=dseed)
     if args.warmup:
         ctx.bench_iterations(args.warmup)
-    ctx.bench_prepare(np.asarray(prob.y), c.beta, c.K, c.U, c.tol, seed=dseed)
-    torch.cuda.synchronize(0)
-    with ClockSampler(0) as clk:
+    ctx.bench_prepare(y_local, c.beta, c.K, c.U, c.tol, seed=dseed)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    with ClockSampler(device) as clk:
         tim = ctx.bench_iterations(args.steps, time_kernels=True)
+    torch.cuda.synchronize(device)
+    if dist:
+        dist.barrier()
     total_ms = tim["total_ms"]
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
     value = args.steps / (total_ms / 1e3)
     pcg_steps = tim["pcg_steps"]
     qw = 32 if c.K + 1 > 24 else 24
     fwd_avg = tim["fwd_ms"] / max(tim["fwd_launches"], 1)
     bwd_avg = tim["bwd_ms"] / max(tim["bwd_launches"], 1)
     if is_conv:
-        alg_bytes = 4.0 * qw * c.D + 8.0 * qw * c.D  # operand digit planes in, fp64 result out
+        d_loc = c.D // world  # per-rank launch (balanced time shards)
+        alg_bytes = 4.0 * qw * d_loc + 8.0 * qw * d_loc  # operand digit planes in, fp64 result out
         dom, avg_ms = (("bwd (Phi^T U band)", bwd_avg) if tim["bwd_ms"] >= tim["fwd_ms"] else
                        ("fwd (Phi P band)", fwd_avg))
     else:  # the fused column pass: one fp64 n^2 x ldq block in, one out (+ n^2 mask bytes)
@@ -373,7 +398,7 @@ def run_ours_conv(args):
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     line = {
-        "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "i8 x i8 -> exact i32 (ozaki) / f64" if is_conv else "f64 (FFT passes)",
         "data": ("synthetic (Bernoulli(0.01) x Exp(1) spikes, exp(-t/20) filter, sigma=0.05)" if is_conv else
@@ -381,7 +406,8 @@ def run_ours_conv(args):
         "config": {"workload": (f"{args.config}: causal convolution N=D={c.D}, {c.ntaps} taps, K={c.K}, "
                                 f"PCG cap {c.U} tol {c.tol}" if is_conv else
                                 f"{args.config}: 2-D partial DCT n={c.n} (D={c.D}, N={prob.op.n_rows}), K={c.K}, "
-                                f"PCG cap {c.U} tol {c.tol}"), "D": c.D, "K": c.K},
+                                f"PCG cap {c.U} tol {c.tol}"), "D": c.D, "K": c.K,
+                   "parallelism": f"time-shard x{world}" if is_conv else "single GPU"},
         "pcg_steps_per_sec": pcg_steps / (total_ms / 1e3), "pcg_steps_per_em_iteration": pcg_steps / args.steps,
         "gpu_launches": int(tim["kernel_launches"]), "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -390,11 +416,21 @@ def run_ours_conv(args):
                      "contraction_share_of_step": (tim["fwd_ms"] + tim["bwd_ms"]) / tim["total_ms"]},
     }
     prob.op.release()
+    if world > 1:
+        sharded.ctx.close()
     if not args.no_e2e:
         cfg = c.cofem_config(prec, iterations=args.steps)
+        if dist:
+            from paper_2105_10439_b200.distributed import run_cofem_sharded
+
+            dist.barrier()
         t0 = time.perf_counter()
-        st, est, diag = run_cofem(prob, cfg)
+        st, est, diag = run_cofem_sharded(prob, cfg, device) if dist else run_cofem(prob, cfg)
         el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
         prob.op.release()
         line["e2e"] = {"value": args.steps / el, "unit": UNIT,
                        "h2d_bytes_per_step": (8.0 * prob.op.n_rows + 32.0) / args.steps,
@@ -402,9 +438,13 @@ def run_ours_conv(args):
                        "pcg_steps": int(sum(d["cg_steps"] for d in diag)),
                        "note": "run_cofem(problem, cfg) from host numpy y, context created inside the timed region, "
                                "probes drawn on the device from the reference's PCG64 stream"}
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_sample_conv(c, prob, args.cpu_seconds, pcg_steps / args.steps, is_conv)
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def cpu_sample_conv(c, prob, seconds, steps_per_em, is_conv=True):

@@ -16,8 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import cofem_oracle as O
-from oracle.sharded import pcg_solve_sharded
-from paper_2105_10439_b200.distributed import column_shards
+from oracle.sharded import pcg_solve_sharded, pcg_solve_time_sharded
+from paper_2105_10439_b200.distributed import column_shards, time_shards
 
 
 def _free_port():
@@ -97,6 +97,73 @@ def test_sharded_pcg_matches_unsharded_oracle(tmp_path):
     np.testing.assert_array_equal(res[d * q + 3:], np.arange(d))  # gather preserves rank order
 
 
+def _conv_case():
+    rng = np.random.default_rng(3)
+    d, L, q = 1024, 90, 5
+    h = np.exp(-np.arange(L) / 20.0)
+    taps = h / np.linalg.norm(h)
+    alpha = rng.random(d) + 0.5
+    B = rng.standard_normal((d, q))
+    beta = 400.0
+    minv = 1.0 / (beta * O.conv_op(d, taps).col_sq_norms() + alpha)
+    return d, taps, alpha, B, beta, minv
+
+
+def _time_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).copy())
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def halo(rows, direction):
+        """Send `rows` towards `direction`, receive the same-shaped block from the other side."""
+        to, frm = rank + direction, rank - direction
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        recv = torch.zeros(rows.shape, dtype=torch.float64)
+        reqs = []
+        if 0 <= to < world:
+            reqs.append(dist.isend(torch.from_numpy(rows.copy()), to))
+        if 0 <= frm < world:
+            reqs.append(dist.irecv(recv, frm))
+        for r in reqs:
+            r.wait()
+        return recv.numpy()
+
+    d, taps, alpha, B, beta, minv = _conv_case()
+    t0, t1 = time_shards(d, world, taps.size)[rank]
+    cfg = O.CgConfig(max_steps=300, tolerance=1e-10)
+    rep = pcg_solve_time_sharded(taps, beta, alpha[t0:t1], B[t0:t1], minv[t0:t1], cfg, allreduce, halo)
+    parts = [None] * world
+    dist.all_gather_object(parts, (rep.solution, rep.steps_taken))
+    if rank == 0:
+        np.save(out_path, np.concatenate([np.concatenate([p[0] for p in parts], axis=0).ravel(),
+                                          [p[1] for p in parts]]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_sharded_convolution_pcg_matches_unsharded_oracle(tmp_path, world):
+    """The convolution's time-shard decomposition (halo rows from the
+    neighbours, scalars all-reduced) reproduces the unsharded float64 solve."""
+    out = str(tmp_path / "res.npy")
+    mp.start_processes(_time_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    res = np.load(out)
+    d, taps, alpha, B, beta, minv = _conv_case()
+    op = O.conv_op(d, taps)
+    ref = O.pcg_solve(lambda V: beta * op.adjoint(op.apply(V)) + alpha[:, None] * V, B, minv,
+                      O.CgConfig(max_steps=300, tolerance=1e-10))
+    q = B.shape[1]
+    X = res[: d * q].reshape(d, q)
+    assert np.all(res[d * q:] == ref.steps_taken)
+    assert np.linalg.norm(X - ref.solution) <= 1e-9 * np.linalg.norm(ref.solution)
+
+
 @pytest.mark.gpu
 def test_sharded_run_single_rank_nccl_matches_unsharded():
     """run_cofem_sharded over a real 1-rank NCCL communicator == run_cofem, bitwise."""
@@ -112,6 +179,31 @@ def test_sharded_run_single_rank_nccl_matches_unsharded():
         c = S.CONFIGS["dense-small"]
         prob, z, _ = S.dense_cs_problem(c)
         cfg = c.cofem_config("ozaki", iterations=5)
+        st1, est1, d1 = run_cofem_sharded(prob, cfg)
+        st2, est2, d2 = run_cofem(prob, cfg)
+        np.testing.assert_array_equal(est1.mu, est2.mu)
+        np.testing.assert_array_equal(st1.alpha, st2.alpha)
+        assert [x["cg_steps"] for x in d1] == [x["cg_steps"] for x in d2]
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_time_sharded_convolution_single_rank_nccl_matches_unsharded():
+    """The convolution through ShardedContext.for_operator / run_cofem_sharded
+    over a real 1-rank NCCL communicator == run_cofem, bitwise."""
+    from paper_2105_10439_b200 import _lib, run_cofem
+    from paper_2105_10439_b200 import simulate as S
+    from paper_2105_10439_b200.distributed import run_cofem_sharded
+
+    if _lib.device_count() < 1:
+        pytest.fail("needs a GPU")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        c = S.ConvConfig("conv-nccl", 4096, 256, 20.0, 0.01, 0.05, 10, 3, 200, 1e-5)
+        prob, z = S.conv_problem(c)
+        cfg = c.cofem_config("ozaki")
         st1, est1, d1 = run_cofem_sharded(prob, cfg)
         st2, est2, d2 = run_cofem(prob, cfg)
         np.testing.assert_array_equal(est1.mu, est2.mu)
