@@ -323,7 +323,7 @@ void free_ws(cofem_ctx* c) {
 
 // column-block kernels: blockDim a multiple of ldq near 512 (few blocks -> a
 // short deterministic final reduction; 4 rows per thread trip for MLP)
-int elem_block(int ldq) { return ldq >= 512 ? ldq : ldq * (512 / ldq); }
+int elem_block(int ldq) { return ldq >= 256 ? ldq : ldq * (256 / ldq); }  // 3 blocks / SM resident (<= 85 regs)
 
 // choose split count for a contraction: minimise wave quantisation plus the
 // extra traffic of the split partials relative to the Phi stream
@@ -401,7 +401,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   if (c->ppart_cap) CK(cudaMalloc(&c->ppart, c->ppart_cap));
   CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
-  c->nblk_elem = 2 * c->sm_count;
+  c->nblk_elem = 3 * c->sm_count;
   CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
   CK(cudaMemset(c->X, 0, dbytes));
   CK(cudaMemset(c->R, 0, dbytes));
@@ -622,7 +622,8 @@ int oz_quantize(cofem_ctx* c, const T* M, int ldm, int qoff, int64_t k_real, int
   // maxima, so halo rows received from a neighbour share this rank's scales
   if (global_max && c->nranks > 1) CKR(allreduce(c, colmax, QW, ncclUint64, ncclMax));
   const int64_t nchunk = k_pad / oz::QCHUNK_K;  // one warp each, 8 warps per block
-  oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>((nchunk + 7) / 8, 16 * c->sm_count), 256, 0, c->stream>>>(
+  // one wave of resident blocks (3 / SM at <= 85 registers), grid-stride over the chunks
+  oz::k_quantize<T, QW><<<(unsigned)std::min<int64_t>((nchunk + 7) / 8, 3 * c->sm_count), 256, 0, c->stream>>>(
       k_real, k_pad, ldm, qoff, M, pre, colmax, c->opscale, planes, reset, st);
   c->launches++;
   CK(cudaGetLastError());
@@ -1180,7 +1181,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     CKR(system_apply_dev<T>(c, beta, c->st));
     CKR(allreduce(c, sc.pi, ldq, ncclFloat64));
     k_update<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
-        c->Dp, ldq, q_real, u & 1, (T*)c->X, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, ngroups, groups,
+        c->Dp, ldq, q_real, u & 1, nullptr, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, ngroups, groups,
         sc, pmax, c->st);
     c->launches++;
     CK(cudaGetLastError());
@@ -1189,7 +1190,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     // the kernel mirrors the status into the host-mapped slot: no copy in the stream
     k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
-        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot);
+        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot, (T*)c->X);
     c->launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[slot], c->stream));
@@ -1285,7 +1286,7 @@ int pcg_multi(cofem_ctx** cs, int L, const double* betas, int q_real, const cofe
       const bool fused = oz && c->kind != 2;
       CKR(system_apply_dev<T>(c, betas[l], st));
       k_update<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c0->stream>>>(
-          c->Dp, ldq, q_real, u & 1, (T*)c->X, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, 1, nullptr,
+          c->Dp, ldq, q_real, u & 1, nullptr, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, 1, nullptr,
           c->sc(), fused ? c->colmax : nullptr, st);
       c->launches++;
     }
@@ -1297,7 +1298,7 @@ int pcg_multi(cofem_ctx** cs, int L, const double* betas, int q_real, const cofe
       k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c0->stream>>>(
           c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
           c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg,
-          l == L - 1 ? c0->d_hst + slot : nullptr);
+          l == L - 1 ? c0->d_hst + slot : nullptr, (T*)c->X);
       c->launches++;
     }
     CK(cudaGetLastError());

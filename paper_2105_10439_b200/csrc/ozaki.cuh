@@ -743,7 +743,7 @@ __device__ __forceinline__ double col_scale(unsigned long long bits) {
 // block 0 for the next fused column max.
 constexpr int QCHUNK_K = 16;
 template <typename T, int QW>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     k_quantize(int64_t k_real, int64_t k_pad, int ldm, int qoff, const T* __restrict__ M,
                const double* __restrict__ pre, const unsigned long long* __restrict__ colmax,
                double* __restrict__ scale_out, int8_t* __restrict__ planes, unsigned long long* __restrict__ reset,
@@ -764,19 +764,23 @@ __global__ void __launch_bounds__(256)
       const int64_t k = k0 + r;
       x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * __ldg(pre + k) : 0.0;
     }
+    // |x is| <= 2^30, so v fits int32 and its four balanced base-256 digits
+    // (those of digits4) are the bytes of (v + 0x80808080) ^ 0x80808080; a
+    // 4 x 4 byte transpose per 4 rows packs them plane by plane
     uint32_t w[4][QCHUNK_K / 4];
+    const bool ok = is == is;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int j = 0; j < QCHUNK_K / 4; ++j) {
+      uint32_t u[4];
 #pragma unroll
-      for (int j = 0; j < QCHUNK_K / 4; ++j) w[a][j] = 0u;
-    if (is == is) {
-#pragma unroll
-      for (int r = 0; r < QCHUNK_K; ++r) {
-        int8_t d[4];
-        digits4(x[r] * is, d);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) w[a][r / 4] |= (uint32_t)(uint8_t)d[a] << (8 * (r % 4));
-      }
+      for (int i = 0; i < 4; ++i)
+        u[i] = ok ? (((uint32_t)__double2int_rn(x[4 * j + i] * is) + 0x80808080u) ^ 0x80808080u) : 0u;
+      const uint32_t A = __byte_perm(u[0], u[1], 0x5140), B = __byte_perm(u[0], u[1], 0x7362);
+      const uint32_t C = __byte_perm(u[2], u[3], 0x5140), E = __byte_perm(u[2], u[3], 0x7362);
+      w[3][j] = __byte_perm(A, C, 0x5410);  // byte 0 (least significant digit)
+      w[2][j] = __byte_perm(A, C, 0x7632);
+      w[1][j] = __byte_perm(B, E, 0x5410);
+      w[0][j] = __byte_perm(B, E, 0x7632);  // byte 3 (most significant digit)
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a)

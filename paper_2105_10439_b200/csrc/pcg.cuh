@@ -212,9 +212,11 @@ __global__ void k_sum_splits(int64_t rows, int qw, int nsplit, const T* part, T*
   if (colmax) block_col_max(sm_sum, qw, vmax, colmax);
 }
 
-// ---- solution update (kernels.py step_solution) fused with the residual
+// ---- residual update (kernels.py step_solution) fused with the residual
 // norms and the next direction's rho:  gamma = rho/pi (0 when pi == 0),
-// X += P gamma, R -= Psi gamma, rn2 = ||R||^2, rho_new = <R, M^-1 R>
+// R -= Psi gamma, rn2 = ||R||^2, rho_new = <R, M^-1 R>.  With X == nullptr
+// the solution update X += P gamma is left to k_direction, which reads P
+// anyway (one D x ldq block less per step); otherwise it is done here.
 template <typename T>
 __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T* R, const T* P, const T* Psi,
                          const double* minv, int ngroups, const int* group_of_col, Scalars sc,
@@ -240,8 +242,10 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
       const int64_t j = j0 + (int64_t)u * m.rstep;
       if (j < rows) {
         const int64_t e = j * ldq + q;
-        x[u] = X[e];
-        p[u] = P[e];
+        if (X) {
+          x[u] = X[e];
+          p[u] = P[e];
+        }
         r[u] = R[e];
         ps[u] = Psi[e];
         mv[u] = minv[j * ngroups + g];
@@ -252,7 +256,7 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
       const int64_t j = j0 + (int64_t)u * m.rstep;
       if (j < rows) {
         const int64_t e = j * ldq + q;
-        X[e] = x[u] + p[u] * gm;
+        if (X) X[e] = x[u] + p[u] * gm;
         const T rn = r[u] - ps[u] * gm;
         R[e] = rn;
         const double rd = dd(rn);
@@ -272,19 +276,31 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
 // (or R for the printed recursion), rho <- rho_new.  step == 0 is the
 // initialisation pass (no convergence test).  With `colmax` set, also the
 // per-column max of |pre_j P_jq| for the next Phi P quantisation.
+// With X set (step >= 1) the kernel first applies the step's solution update
+// X += P gamma (gamma = rho/pi as k_update derived it), also on the step that
+// stops the solve.
 template <typename T>
 __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
                             T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
                             const double* pre, unsigned long long* colmax, Status* st,
-                            const double* agg = nullptr, Status* mirror = nullptr) {
+                            const double* agg = nullptr, Status* mirror = nullptr, T* X = nullptr) {
   // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
   // mirror: host-mapped status slot the host polls (no copy in the stream)
-  if (st->done) {
-    if (mirror && blockIdx.x == 0 && threadIdx.x == 0) {
-      *mirror = *st;
-      __threadfence_system();
+  {
+    // a solve finished by an EARLIER step: nothing to do.  (Block 0 of this
+    // very launch may already have set `done` for this step -- then the X
+    // update below must still run: steps is published before done.)
+    const volatile Status* vs = st;
+    const int done = vs->done;
+    __threadfence();
+    const int sdone = vs->steps;
+    if (done && !(X && step >= 1 && sdone == step)) {
+      if (mirror && blockIdx.x == 0 && threadIdx.x == 0) {
+        *mirror = *st;
+        __threadfence_system();
+      }
+      return;
     }
-    return;
   }
   extern __shared__ double sm_dir[];
   const int cur = step & 1, nxt = (step + 1) & 1;
@@ -307,26 +323,40 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
     const bool conv = finite && delta <= tol;
     const bool stop = !finite || conv || step >= max_steps;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->steps = step;
-      st->delta = delta;
-      st->converged = conv ? 1 : 0;
-      st->diverged = finite ? 0 : 1;
-      if (stop) st->done = 1;
+      volatile Status* vs = st;
+      vs->steps = step;
+      vs->delta = delta;
+      vs->converged = conv ? 1 : 0;
+      vs->diverged = finite ? 0 : 1;
+      __threadfence();
+      if (stop) vs->done = 1;
       if (mirror) {
         *mirror = *st;
         __threadfence_system();
       }
     }
-    if (stop) return;
+    if (stop) {
+      if (X) {  // the last step's solution update
+        const ColMap m(ldq);
+        const T gm = T(safe_ratio(sc.rho[cur][m.q], sc.pi[m.q]));
+        for (int64_t j = m.r0; j < rows; j += m.rstep) {
+          const int64_t e = j * ldq + m.q;
+          X[e] = X[e] + P[e] * gm;
+        }
+      }
+      return;
+    }
   }
   const ColMap m(ldq);
   const int q = m.q;
   const int g = group_of_col ? group_of_col[q] : 0;
   const double eta = safe_ratio(sc.rho_new[q], sc.rho[cur][q]);
   const T et = T(eta);
+  const bool upd_x = X && step >= 1;
+  const T gm = upd_x ? T(safe_ratio(sc.rho[cur][q], sc.pi[q])) : T(0);
   double pmax = 0.0;
   for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
-    T r[UNR], p[UNR];
+    T r[UNR], p[UNR], x[UNR];
     double mv[UNR], pr[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -335,8 +365,16 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
         const int64_t e = j * ldq + q;
         r[u] = R[e];
         p[u] = P[e];
+        if (upd_x) x[u] = X[e];
         mv[u] = minv[j * ngroups + g];
         pr[u] = colmax ? pre[j] : 0.0;
+      }
+    }
+    if (upd_x) {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t j = j0 + (int64_t)u * m.rstep;
+        if (j < rows) X[j * ldq + q] = x[u] + p[u] * gm;
       }
     }
 #pragma unroll
