@@ -174,6 +174,17 @@ __device__ __forceinline__ void tmem_zero_all(uint32_t tmem, int quarter) {
   asm volatile("tcgen05.wait::st.sync.aligned;");
 }
 
+// 256-bit global accesses (sm_100): an epilogue thread owns one output row, so
+// a warp instruction touches 32 rows; moving a whole 32-B sector per thread
+// keeps every requested sector fully used (16-B accesses fetched each sector
+// twice and, for streamed reads, let L2 evict it in between)
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 // Epilogue of one tile for the calling thread's row: read the five
 // significance blocks, re-zero them, combine exactly in int64 and write
 // out[q] = value * scale * op_scale[q].  With TRACK the thread keeps running
@@ -210,8 +221,8 @@ __device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, c
                            ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
       v[t] = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * f[t];
     }
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + q0 + t) = make_double2(v[t], v[t + 1]);
+    st_v4(o + q0, v[0], v[1], v[2], v[3]);
+    st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
     if (TRACK) {
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -235,11 +246,7 @@ __device__ __forceinline__ void comb_prefetch(const double* __restrict__ prow, d
 #pragma unroll
   for (int q0 = HALF * 8, g = 0; q0 < QW; q0 += 16, ++g)
 #pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      const double2 v = __ldcs(reinterpret_cast<const double2*>(prow + q0 + t));
-      pv[8 * g + t] = v.x;
-      pv[8 * g + t + 1] = v.y;
-    }
+    for (int t = 0; t < 8; t += 4) ld_v4(prow + q0 + t, pv[8 * g + t], pv[8 * g + t + 1], pv[8 * g + t + 2], pv[8 * g + t + 3]);
 }
 
 template <int QW, int HALF>
@@ -276,8 +283,8 @@ __device__ __forceinline__ void epilogue_row_comb(uint32_t tset_lane, double sca
       v[t] = beta * u + alpha_j * p[t];
       pacc[q0 + t] += p[t] * v[t];
     }
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + q0 + t) = make_double2(v[t], v[t + 1]);
+    st_v4(o + q0, v[0], v[1], v[2], v[3]);
+    st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
   }
 }
 

@@ -1,0 +1,6 @@
+D=gpurun_out/r1e
+mkdir -p $D
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 2>&1 | tail -3 > $D/tests_v4.txt
+python bench.py --config conv-large --no-cpu --no-e2e > $D/bench_conv_v4.json 2> $D/bench_conv_v4.err
+python bench.py --no-cpu --no-e2e > $D/bench_dense_v4.json 2> $D/bench_dense_v4.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:band_kernel -c 6 --csv --log-file $D/launches_band_v4.csv python bench.py --config conv-large --steps 1 --warmup 0 --no-e2e --no-cpu > $D/ncu_band_v4.log 2>&1
