@@ -61,7 +61,7 @@ def build(force=False, verbose=False):
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
            "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
-           os.path.join(CSRC, "cofem.cu"), "-o", OUT + ".tmp", "-ldl"]
+           os.path.join(CSRC, "cofem.cu"), "-o", OUT + ".tmp", "-ldl", "-lpthread"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

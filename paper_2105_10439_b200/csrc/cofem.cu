@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cofem_b200.h"
@@ -2019,12 +2020,64 @@ int cofem_destroy(cofem_ctx* c) {
   return 0;
 }
 
+namespace {
+// Host -> device upload of a pitched row block from pageable memory: host
+// threads copy row chunks into two pinned staging buffers while the copy
+// engine drains the other one (pageable cudaMemcpy stages through one driver
+// buffer at ~11 GB/s; this runs at the PCIe rate).
+int upload_rows(cofem_ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch, size_t row_bytes,
+                int64_t rows) {
+  constexpr size_t CHUNK = (size_t)64 << 20;
+  if ((size_t)rows * row_bytes < 2 * CHUNK) {  // small: one pageable copy
+    CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice, c->stream));
+    return 0;
+  }
+  const int64_t rpc = std::max<int64_t>(1, (int64_t)(CHUNK / row_bytes));
+  void* pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int rc = 0;
+  for (int b = 0; b < 2 && !rc; ++b) {
+    if (cudaHostAlloc(&pin[b], (size_t)rpc * row_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(COFEM_ENOMEM, "pinned staging buffers");
+  }
+  const int nthr = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  for (int64_t r0 = 0, i = 0; r0 < rows && !rc; r0 += rpc, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t nr = std::min(rpc, rows - r0);
+    if (i >= 2 && cudaEventSynchronize(ev[b]) != cudaSuccess) rc = fail(COFEM_ECUDA, "staging event");
+    if (rc) break;
+    auto copy = [&](int t) {
+      for (int64_t r = r0 + t; r < r0 + nr; r += nthr)
+        memcpy((char*)pin[b] + (size_t)(r - r0) * row_bytes, (const char*)src + (size_t)r * spitch, row_bytes);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthr; ++t) pool.emplace_back(copy, t);
+    copy(0);
+    for (auto& th : pool) th.join();
+    if (cudaMemcpy2DAsync((char*)dst + (size_t)r0 * dpitch, dpitch, pin[b], row_bytes, row_bytes, nr,
+                          cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaEventRecord(ev[b], c->stream) != cudaSuccess)
+      rc = fail(COFEM_ECUDA, "staged upload");
+  }
+  cudaStreamSynchronize(c->stream);
+  for (int b = 0; b < 2; ++b) {
+    if (pin[b]) cudaFreeHost(pin[b]);
+    if (ev[b]) cudaEventDestroy(ev[b]);
+  }
+  return rc;
+}
+}  // namespace
+
 int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_device) {
   CKR(check_ctx(c, false));
   if (c->kind != 0) return fail(COFEM_EINVAL, "not a dense dictionary context");
   if (!phi || ld < c->D) return fail(COFEM_EINVAL, "dictionary pointer / leading dimension");
-  CK(cudaMemcpy2DAsync(c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N,
-                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  if (on_device)
+    CK(cudaMemcpy2DAsync(c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N,
+                         cudaMemcpyDeviceToDevice, c->stream));
+  else
+    CKR(upload_rows(c, c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N));
   CK(cudaStreamSynchronize(c->stream));
   c->have_phi = true;
   c->oz_ready = false;
@@ -2047,9 +2100,7 @@ int cofem_set_dictionary_f64(cofem_ctx* c, const double* phi, int64_t ld) {
   CK(cudaMalloc(&tmp, bytes));
   CK(cudaMemsetAsync(tmp, 0, bytes, c->stream));
   int rc = 0;
-  cudaError_t e = cudaMemcpy2DAsync(tmp, c->Dp * sizeof(double), phi, ld * sizeof(double), c->D * sizeof(double),
-                                    c->N, cudaMemcpyHostToDevice, c->stream);
-  if (e != cudaSuccess) rc = fail(COFEM_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
+  rc = upload_rows(c, tmp, c->Dp * sizeof(double), phi, ld * sizeof(double), c->D * sizeof(double), c->N);
   if (!rc) {
     k_round_f32<<<16 * c->sm_count, 256, 0, c->stream>>>(tmp, c->phi, (int64_t)c->Np * c->Dp);
     c->launches++;
