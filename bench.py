@@ -389,9 +389,15 @@ def run_ours_conv(args):
     bwd_avg = tim["bwd_ms"] / max(tim["bwd_launches"], 1)
     if is_conv:
         d_loc = c.D // world  # per-rank launch (balanced time shards)
-        alg_bytes = 4.0 * qw * d_loc + 8.0 * qw * d_loc  # operand digit planes in, fp64 result out
-        dom, avg_ms = (("bwd (Phi^T U band)", bwd_avg) if tim["bwd_ms"] >= tim["fwd_ms"] else
-                       ("fwd (Phi P band)", fwd_avg))
+        # Phi P band: operand digit planes in (4 B / entry), fp64 V out; Phi^T V
+        # band with the PCG combine fused: planes in, P in, Psi out
+        if tim["bwd_ms"] >= tim["fwd_ms"]:
+            dom, avg_ms = ("bwd (Phi^T V band + fused combine: Psi = beta Phi^T V + alpha P; MMA-issue bound, "
+                           "see DESIGN.md)", bwd_avg)
+            alg_bytes = (4.0 + 8.0 + 8.0) * qw * d_loc
+        else:
+            dom, avg_ms = "fwd (Phi P band)", fwd_avg
+            alg_bytes = (4.0 + 8.0) * qw * d_loc
     else:  # the fused column pass: one fp64 n^2 x ldq block in, one out (+ n^2 mask bytes)
         alg_bytes = 16.0 * qw * c.D + c.D
         dom, avg_ms = "column pass (DCT-II, mask, DCT-III; fp64 FFT)", fwd_avg

@@ -489,6 +489,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // the window alone.  Same significance-aligned, double-buffered accumulation
 // and epilogue as contract_kernel.
 constexpr int BSTAGES = 4;
+// band_kernel accumulator sets: 5 significance blocks of QW <= 32 columns
+// (160 TMEM columns), three sets in the 512-column allocation so the MMA
+// issuer can run two tiles ahead of a slow epilogue
+#ifndef BAND_SETS_OVERRIDE
+constexpr int BAND_SETS = 3;
+#else
+constexpr int BAND_SETS = BAND_SETS_OVERRIDE;
+#endif
+constexpr int BAND_SET_COLS = 160;
 template <int QW>
 struct BandCfg {
   static constexpr int B_STAGE = 4 * QW * KT;
@@ -517,9 +526,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + BSTAGES * BC::B_STAGE);
   uint64_t* empty = full + BSTAGES;
   uint64_t* band_full = empty + BSTAGES;
-  uint64_t* tfull = band_full + 1;  // [2]
-  uint64_t* tempty = tfull + 2;     // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = band_full + 1;  // [BAND_SETS]
+  uint64_t* tempty = tfull + BAND_SETS;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + BAND_SETS);
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);  // [EPI_WARPS][QW], after the last tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -529,7 +538,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(band_full, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < BAND_SETS; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 32 * EPI_WARPS);
     }
@@ -584,10 +593,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
-        const int buf = it & 1;
-        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        const int buf = it % BAND_SETS;
+        mbar_wait(&tempty[buf], ((it / BAND_SETS) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t tset = tmem + buf * C::SET_COLS;
+        const uint32_t tset = tmem + buf * BAND_SET_COLS;
         for (int s = 0; s < nst; ++s) {
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -615,7 +624,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
-      const int buf = it & 1;
+      const int buf = it % BAND_SETS;
       const int64_t row = (int64_t)mb * BM + row_in_tile;
       const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
       const double alpha_j = COMB ? alpha[row] : 0.0;
@@ -624,11 +633,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (half == 0) comb_prefetch<QW, 0>(Pc + row * p_ld, pv);
         else comb_prefetch<QW, 1>(Pc + row * p_ld, pv);
       }
-      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      mbar_wait(&tfull[buf], (it / BAND_SETS) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (OZ_VARIANT == 2) {
         uint32_t r[5][8];
-        const uint32_t tl = tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
         for (int q0 = half * 8; q0 < QW; q0 += 16) {
           for (int sb = 0; sb < 5; ++sb)
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -642,13 +651,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (r[0][0] == 0x12345 && scale == 3.0) out[row] = 1.0;
         }
       } else if (COMB) {
-        const uint32_t tl = tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
         if (half == 0)
           epilogue_row_comb<QW, 0>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
         else
           epilogue_row_comb<QW, 1>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
       } else if (OZ_VARIANT != 3 && OZ_VARIANT != 4)
-        epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * C::SET_COLS + ((uint32_t)(quarter * 32) << 16),
+        epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16),
                           scale, op_scale, out + row * QW, cm);
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");

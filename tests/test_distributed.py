@@ -40,6 +40,20 @@ def test_column_shards_partition():
         column_shards(4, 3)
 
 
+def test_time_shards_geometry():
+    from paper_2105_10439_b200.distributed import conv_halo
+
+    assert time_shards(4096, 2, 256) == [(0, 2048), (2048, 4096)]
+    s = time_shards(2**22, 8, 256)
+    assert all(a % 256 == 0 for a, _ in s) and s[-1][1] == 2**22
+    assert [b - a for a, b in s] == [2**19] * 8
+    assert conv_halo(256) == 256 and conv_halo(257) == 256 and conv_halo(258) == 320 and conv_halo(1) == 0
+    with pytest.raises(ValueError):
+        time_shards(1024, 4, 513)  # 256-sample shards shorter than the 512-row halo
+    with pytest.raises(ValueError):
+        time_shards(512, 3, 2)  # fewer 256-sample units than ranks
+
+
 def _worker(rank, world, port, out_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)

@@ -26,7 +26,6 @@ from paper_2105_10439_b200.distributed import (
     run_cofem_threaded,
     run_threaded,
     threaded_contexts,
-    time_shards,
 )
 
 pytestmark = pytest.mark.gpu
@@ -66,14 +65,6 @@ def test_time_sharded_convolution_apply_is_bitwise(dim, ntaps, world, q):
     # and both are the convolution (float64 numpy) to the int8 path's accuracy
     ref = np.stack([np.convolve(V[:, k], h)[:dim] for k in range(q)], axis=1)
     assert rel(full_f, ref) <= 1e-8
-
-
-def test_time_shards_geometry():
-    assert time_shards(4096, 2, 256) == [(0, 2048), (2048, 4096)]
-    s = time_shards(2**22, 8, 256)
-    assert all(a % 256 == 0 for a, _ in s) and s[-1][1] == 2**22
-    with pytest.raises(ValueError):
-        time_shards(1024, 4, 513)  # 256-sample shards shorter than the 512-row halo
 
 
 @pytest.mark.parametrize("world", [2, 3])
