@@ -302,6 +302,17 @@ int set_dev(cofem_ctx* c) {
   return 0;
 }
 
+// Host -> device copy ordered on the context stream, complete on return.
+// (A plain cudaMemcpy runs on the legacy default stream, which does not order
+// against the non-blocking context stream, and from pageable memory it may
+// return before its DMA lands: kernels on the context stream could then read
+// the old contents.)
+cudaError_t h2d_sync(cofem_ctx* c, void* dst, const void* src, size_t bytes) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(c->stream);
+}
+
 cudaEvent_t next_event(cofem_ctx* c) {
   if (c->evnext == c->evpool.size()) {
     cudaEvent_t e;
@@ -404,16 +415,16 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
   c->nblk_elem = 3 * c->sm_count;
   CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
-  CK(cudaMemset(c->X, 0, dbytes));
-  CK(cudaMemset(c->R, 0, dbytes));
-  CK(cudaMemset(c->P, 0, dbytes));
-  CK(cudaMemset(c->Psi, 0, dbytes));
+  CK(cudaMemsetAsync(c->X, 0, dbytes, c->stream));
+  CK(cudaMemsetAsync(c->R, 0, dbytes, c->stream));
+  CK(cudaMemsetAsync(c->P, 0, dbytes, c->stream));
+  CK(cudaMemsetAsync(c->Psi, 0, dbytes, c->stream));
   if (c->kind == 2) {
     const int64_t n = c->dct_n, nc = n * ldq;
     for (double** b : {&c->bufA, &c->bufB}) {
       if (*b) cudaFree(*b);
       CK(cudaMalloc(b, (size_t)n * nc * sizeof(double)));
-      CK(cudaMemset(*b, 0, (size_t)n * nc * sizeof(double)));
+      CK(cudaMemsetAsync(*b, 0, (size_t)n * nc * sizeof(double), c->stream));
     }
   }
   c->ldq = ldq;
@@ -1435,7 +1446,7 @@ int system_apply_impl(cofem_ctx* c, double beta, const double* alpha, const doub
   CKR(ensure_ws(c, ldq));
   std::vector<double> a(c->Dp, 0.0);
   std::copy(alpha, alpha + c->D, a.begin());
-  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h2d_sync(c, c->alpha, a.data(), c->Dp * sizeof(double)));
   CKR(upload_block<T>(c, V, c->D, q, c->Dp, ldq, c->P));
   CK(cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream));
   CKR(system_apply_dev<T>(c, beta, nullptr));
@@ -1446,25 +1457,29 @@ int system_apply_impl(cofem_ctx* c, double beta, const double* alpha, const doub
 // ---- EM loop ---------------------------------------------------------------
 template <typename T>
 int compute_aty(cofem_ctx* c, const double* y_host) {
-  // V[:, 0] = y, other columns 0 -> Phi^T V via the bwd contraction (8-wide)
+  // V[:, 0] = y, other columns 0 -> Phi^T V (structured: all ldq columns of
+  // the passes; dense / band: the 8-wide bwd contraction); aty = column 0.
+  // y goes up as N doubles and aty is gathered on the device (no host
+  // staging of the Np x ldq blocks).
   CKR(ensure_ws(c, std::max(c->ldq, 8)));
-  if (c->kind == 2 || c->conv_fft) {
-    std::vector<double> vb((size_t)c->Np * c->ldq, 0.0);
-    for (int64_t i = 0; i < c->N; ++i) vb[i * c->ldq] = y_host[i];
-    CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const bool whole = c->kind == 2 || c->conv_fft;
+  const int ld = whole ? c->ldq : 8;
+  if (!c->ybuf) CK(cudaMalloc(&c->ybuf, c->Np * sizeof(double)));
+  CK(cudaMemcpyAsync(c->ybuf, y_host, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const int g = 8 * c->sm_count;
+  if (whole) {
+    k_put_col0<double><<<g, 256, 0, c->stream>>>(c->ybuf, c->N, c->Np, ld, (double*)c->V);
+    c->launches++;
     if (c->conv_fft) CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, nullptr));
     else CKR(dct_adjoint_from_V(c));
-    std::vector<double> out((size_t)c->Dp * c->ldq);
-    CK(cudaMemcpyAsync(out.data(), c->tmpD, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    k_get_col0<double><<<g, 256, 0, c->stream>>>((const double*)c->tmpD, c->D, c->Dp, ld, c->aty);
+    c->launches++;
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
-    std::vector<double> aty(c->Dp, 0.0);
-    for (int64_t j = 0; j < c->D; ++j) aty[j] = out[j * c->ldq];
-    CK(cudaMemcpy(c->aty, aty.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
     return 0;
   }
-  std::vector<T> vb((size_t)c->Np * 8, T(0));
-  for (int64_t i = 0; i < c->N; ++i) vb[i * 8] = (T)y_host[i];
-  CK(cudaMemcpyAsync(c->V, vb.data(), vb.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  k_put_col0<T><<<g, 256, 0, c->stream>>>(c->ybuf, c->N, c->Np, 8, (T*)c->V);
+  c->launches++;
   c->v_colmax_valid = false;
   int ns = 1;
   CKR(bwd_chunk<T>(c, 8, (const T*)c->V, &ns, nullptr));
@@ -1472,13 +1487,10 @@ int compute_aty(cofem_ctx* c, const double* y_host) {
   k_sum_splits<T><<<c->nblk_elem, bsz, bsz * sizeof(double), c->stream>>>(c->Dp, 8, ns, (const T*)c->ppart,
                                                                            (T*)c->tmpD, nullptr, nullptr, nullptr);
   c->launches++;
+  k_get_col0<T><<<g, 256, 0, c->stream>>>((const T*)c->tmpD, c->D, c->Dp, 8, c->aty);
+  c->launches++;
   CK(cudaGetLastError());
-  std::vector<T> out((size_t)c->Dp * 8);
-  CK(cudaMemcpyAsync(out.data(), c->tmpD, out.size() * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  std::vector<double> aty(c->Dp, 0.0);
-  for (int64_t j = 0; j < c->D; ++j) aty[j] = (double)out[j * 8];
-  CK(cudaMemcpy(c->aty, aty.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -1499,7 +1511,7 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   CKR(compute_aty<T>(c, y));
   // alpha = 1 (PrecisionState.initial, cofem.py:65), theta by policy
   std::vector<double> a(c->Dp, 1.0);
-  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h2d_sync(c, c->alpha, a.data(), c->Dp * sizeof(double)));
   if (em->theta_policy == COFEM_THETA_JACOBI) {
     if (c->kind == 2) return fail(COFEM_EINVAL, "jacobi on a DCT dictionary: pass its column norms as custom theta");
     if (c->kind == 0) {
@@ -1510,7 +1522,7 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
     CK(cudaMemcpyAsync(c->theta, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   } else if (em->theta_policy == COFEM_THETA_CUSTOM) {
     if (!theta) return fail(COFEM_EINVAL, "custom theta policy needs a theta vector");
-    CK(cudaMemcpy(c->theta, theta, c->D * sizeof(double), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c, c->theta, theta, c->D * sizeof(double)));
   }
   k_make_minv<<<(int)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->D, c->Dp, beta, c->alpha, c->theta,
                                                                    em->theta_policy, c->minv);
@@ -1630,8 +1642,8 @@ int run_multi_impl(cofem_ctx** cs, int L, const double* const* ys, const double*
     at[3 * L + l] = cs[l]->minv;
     at[4 * L + l] = cs[l]->theta;
   }
-  cudaMemcpy(aptrs, at.data(), at.size() * sizeof(double*), cudaMemcpyHostToDevice);
-  cudaMemcpy(dbeta, betas, L * sizeof(double), cudaMemcpyHostToDevice);
+  h2d_sync(c0, aptrs, at.data(), at.size() * sizeof(double*));
+  h2d_sync(c0, dbeta, betas, L * sizeof(double));
   const int64_t dk = c0->D * K;
   for (int t = 1; t <= em->iterations && !rc; ++t) {
     for (int l = 0; l < L; ++l) {
@@ -1737,14 +1749,14 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
     return bail(fail(COFEM_ECUDA, "stream create failed"));
   if (cudaMalloc(&c->phi, (size_t)c->Np * c->Dp * sizeof(float)) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "dictionary allocation failed"));
-  cudaMemset(c->phi, 0, (size_t)c->Np * c->Dp * sizeof(float));
+  cudaMemsetAsync(c->phi, 0, (size_t)c->Np * c->Dp * sizeof(float), c->stream);
   double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty};
   for (double** p : dvecs) {
     if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
-    cudaMemset(*p, 0, c->Dp * sizeof(double));
+    cudaMemsetAsync(*p, 0, c->Dp * sizeof(double), c->stream);
   }
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
-  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream);
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
   if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
@@ -1754,6 +1766,7 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   cudaEventCreate(&c->t1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+  cudaStreamSynchronize(c->stream);  // zero fills run on the context stream
   *out = c;
   return 0;
 }
@@ -1813,10 +1826,10 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty, &c->colscale, &c->hrows};
   for (double** p : dvecs) {
     if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
-    cudaMemset(*p, 0, c->Dp * sizeof(double));
+    cudaMemsetAsync(*p, 0, c->Dp * sizeof(double), c->stream);
   }
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
-  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream);
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
   if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
@@ -1829,7 +1842,7 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
     std::vector<double> csq(c->Dp, 0.0), cum(ntaps + 1, 0.0);
     for (int64_t m = 0; m < ntaps; ++m) cum[m + 1] = cum[m] + taps[m] * taps[m];
     for (int64_t j = 0; j < dim; ++j) csq[j] = cum[std::min<int64_t>(ntaps, dim - j)];
-    cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+    h2d_sync(c, c->colsq, csq.data(), c->Dp * sizeof(double));
   }
   if (precision == COFEM_FP64) {
     // overlap-save spectra (1024 points, 1/1024 folded in) of h and of reversed h
@@ -1855,14 +1868,15 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
         cudaMalloc(&c->dct_wN, n * sizeof(double2)) ||
         cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess)
       return bail(fail(COFEM_ENOMEM, "FFT tables"));
-    cudaMemcpy(c->cf_H, H.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-    cudaMemcpy(c->cf_Hr, Hr.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-    cudaMemcpy(c->dct_wN, wN.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+    h2d_sync(c, c->cf_H, H.data(), n * sizeof(double2));
+    h2d_sync(c, c->cf_Hr, Hr.data(), n * sizeof(double2));
+    h2d_sync(c, c->dct_wN, wN.data(), n * sizeof(double2));
     cudaMemcpyToSymbol(dctf::c_w64, w64.data(), 64 * sizeof(double2));
     e = cudaGetLastError();
     if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
     c->have_phi = true;
-    *out = c;
+    cudaStreamSynchronize(c->stream);  // zero fills run on the context stream
+  *out = c;
     return 0;
   }
   // operand buffers of the int8 path
@@ -1875,8 +1889,8 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
       cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "operand buffers"));
-  cudaMemset(c->pq_base, 0, (size_t)4 * QCHUNK * c->Dp + lpb);
-  cudaMemset(c->vq, 0, (size_t)4 * QCHUNK * c->Np + lpb);
+  cudaMemsetAsync(c->pq_base, 0, (size_t)4 * QCHUNK * c->Dp + lpb, c->stream);
+  cudaMemsetAsync(c->vq, 0, (size_t)4 * QCHUNK * c->Np + lpb, c->stream);
   c->pq = c->pq_base + lpb;
   // band digit planes: lower band (Phi) and upper band (Phi^T), one scale 2^e >= max |h|
   const double hs = host_pow2_ceil(hmax);
@@ -1897,19 +1911,20 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
     }
   if (cudaMalloc(&c->band_fwd, bf.size()) != cudaSuccess || cudaMalloc(&c->band_adj, ba.size()) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "band planes"));
-  cudaMemcpy(c->band_fwd, bf.data(), bf.size(), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->band_adj, ba.data(), ba.size(), cudaMemcpyHostToDevice);
+  h2d_sync(c, c->band_fwd, bf.data(), bf.size());
+  h2d_sync(c, c->band_adj, ba.data(), ba.size());
   int rc = encode_u8_3d(&c->map_band_fwd, c->band_fwd, nk, oz::BM, 4, oz::KT, oz::BM, 4);
   if (!rc) rc = encode_u8_3d(&c->map_band_adj, c->band_adj, nk, oz::BM, 4, oz::KT, oz::BM, 4);
   if (rc) return bail(rc);
   // scales: output rows carry hs; operands are not pre-scaled (ones)
   std::vector<double> hv(c->Dp, hs), ones(c->Dp, 1.0);
-  cudaMemcpy(c->hrows, hv.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->colscale, ones.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice);
+  h2d_sync(c, c->hrows, hv.data(), c->Dp * sizeof(double));
+  h2d_sync(c, c->colscale, ones.data(), c->Dp * sizeof(double));
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
   c->oz_ready = true;
+  cudaStreamSynchronize(c->stream);  // zero fills run on the context stream
   *out = c;
   return 0;
 }
@@ -1949,10 +1964,10 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty};
   for (double** p : dvecs) {
     if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
-    cudaMemset(*p, 0, c->Dp * sizeof(double));
+    cudaMemsetAsync(*p, 0, c->Dp * sizeof(double), c->stream);
   }
   if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
-  cudaMemset(c->tickets, 0, 8 * sizeof(unsigned));
+  cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream);
   if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
   if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
@@ -1976,22 +1991,23 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
       cudaMalloc(&c->dct_cn, n * sizeof(double)) || cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) ||
       cudaMalloc(&c->dct_grid, grid.size()) || cudaMalloc(&c->dct_gridT, grid.size()))
     return bail(fail(COFEM_ENOMEM, "DCT tables"));
-  cudaMemcpy(c->dct_wN, wN.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dct_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dct_cn, cn.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  h2d_sync(c, c->dct_wN, wN.data(), n * sizeof(double2));
+  h2d_sync(c, c->dct_tw, tw.data(), n * sizeof(double2));
+  h2d_sync(c, c->dct_cn, cn.data(), n * sizeof(double));
   cudaMemcpyToSymbol(dctf::c_w64, w64.data(), 64 * sizeof(double2));
   std::vector<int64_t> sorted(mask, mask + nmask);
   std::sort(sorted.begin(), sorted.end());
-  cudaMemcpy(c->dct_mask, sorted.data(), nmask * sizeof(int64_t), cudaMemcpyHostToDevice);
-  cudaMemcpy(c->dct_grid, grid.data(), grid.size(), cudaMemcpyHostToDevice);
+  h2d_sync(c, c->dct_mask, sorted.data(), nmask * sizeof(int64_t));
+  h2d_sync(c, c->dct_grid, grid.data(), grid.size());
   std::vector<uint8_t> gridT(grid.size());
   for (int64_t k = 0; k < n; ++k)
     for (int64_t l = 0; l < n; ++l) gridT[l * n + k] = grid[k * n + l];
-  cudaMemcpy(c->dct_gridT, gridT.data(), gridT.size(), cudaMemcpyHostToDevice);
+  h2d_sync(c, c->dct_gridT, gridT.data(), gridT.size());
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
   c->oz_ready = true;
+  cudaStreamSynchronize(c->stream);  // zero fills run on the context stream
   *out = c;
   return 0;
 }
@@ -2133,7 +2149,7 @@ int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {
     for (int64_t m = 0; m < L; ++m) cum[m + 1] = cum[m] + c->taps[m] * c->taps[m];
     for (int64_t j = 0; j < c->D; ++j) csq[j] = cum[std::min<int64_t>(L, global_cols - col_offset - j)];
     CKR(set_dev(c));
-    CK(cudaMemcpy(c->colsq, csq.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c, c->colsq, csq.data(), c->Dp * sizeof(double)));
   }
   c->col_offset = col_offset;
   c->global_cols = global_cols;
@@ -2311,7 +2327,7 @@ int pcg_solve_impl(cofem_ctx* c, double beta, const double* alpha, const double*
   CKR(ensure_ws(c, ldq));
   std::vector<double> a(c->Dp, 0.0);
   std::copy(alpha, alpha + c->D, a.begin());
-  CK(cudaMemcpy(c->alpha, a.data(), c->Dp * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h2d_sync(c, c->alpha, a.data(), c->Dp * sizeof(double)));
   // minv: D x ngroups (groups > 1 stored in a dedicated buffer)
   double* minv_dev = c->minv;
   double* minv_tmp = nullptr;
@@ -2321,13 +2337,13 @@ int pcg_solve_impl(cofem_ctx* c, double beta, const double* alpha, const double*
   }
   std::vector<double> m((size_t)c->Dp * ngroups, 0.0);
   std::copy(minv, minv + (size_t)c->D * ngroups, m.begin());
-  CK(cudaMemcpy(minv_dev, m.data(), m.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h2d_sync(c, minv_dev, m.data(), m.size() * sizeof(double)));
   int* gdev = nullptr;
   if (ngroups > 1) {
     std::vector<int> g(ldq, 0);
     for (int64_t k = 0; k < q; ++k) g[k] = group_of_col[k];
     CKR(ensure_groups(c, ldq));
-    CK(cudaMemcpy(c->groups, g.data(), ldq * sizeof(int), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c, c->groups, g.data(), ldq * sizeof(int)));
     gdev = c->groups;
   }
   CKR(upload_block<T>(c, B, c->D, q, c->Dp, ldq, c->R));

@@ -639,6 +639,22 @@ __global__ void k_colsq(const float* phi, int64_t ld, int64_t n_real, int64_t d_
   out[j] = s;
 }
 
+// ---- Phi^T y staging: y (n doubles) -> column 0 of an (rows x ld) block
+// (other columns and the padding rows zero), and column 0 back out
+template <typename T>
+__global__ void k_put_col0(const double* __restrict__ y, int64_t n, int64_t rows, int ld, T* __restrict__ V) {
+  const int64_t total = rows * ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ld;
+    V[e] = (e % ld == 0 && i < n) ? T(y[i]) : T(0);
+  }
+}
+template <typename T>
+__global__ void k_get_col0(const T* __restrict__ src, int64_t n, int64_t rows, int ld, double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = i < n ? (double)src[i * ld] : 0.0;
+}
+
 // ---- in-process shard group (cofem_group): element-wise reduction over the
 // ranks' buffers, in rank order so every rank gets the same bits.  op 0 sum,
 // 1 max (used on non-negative doubles' bit patterns as uint64).

@@ -252,6 +252,28 @@ def test_run_cofem_variants_parity(name, precision):
     np.testing.assert_array_equal(st.alpha < PRUNE, p("alpha") < PRUNE)
 
 
+@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+def test_fresh_context_first_run_equals_repeat(precision):
+    """A context's first run (buffers just allocated and zero-filled, alpha /
+    theta / tables just uploaded) must see exactly the state a repeat run sees:
+    every upload is ordered on the context stream (a legacy-stream copy once
+    raced the preconditioner build and cost 16 extra CG steps)."""
+    c = S.CONFIGS["dense-mid"]
+    prob, _, _ = S.dense_cs_problem(c)
+    cfg = c.cofem_config(precision, iterations=1)
+    runs = []
+    for fresh in (True, False, True):
+        if fresh:
+            prob.op.release()
+        st, est, diag = run_cofem(prob, cfg)
+        runs.append((st.alpha, est.mu, est.s, [d["cg_steps"] for d in diag]))
+    prob.op.release()
+    for r in runs[1:]:
+        assert r[3] == runs[0][3]
+        for a, b in zip(r[:3], runs[0][:3]):
+            np.testing.assert_array_equal(a, b)
+
+
 def test_run_cofem_host_probes_equal_explicit_blocks():
     c = S.CONFIGS["dense-small"]
     prob, _, _ = S.dense_cs_problem(c)
