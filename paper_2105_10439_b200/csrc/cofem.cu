@@ -583,14 +583,28 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
     CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
     CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
   }
+  // column shards agree on the row scales (max over every shard's columns),
+  // so each shard's digit planes are the unsharded dictionary's columns and
+  // every rank quantises the all-reduced V with the same scales
+  const bool shard_rows = c->nranks > 1;
+  auto row_scales = [&](auto* phi_src) -> int {
+    using PT = std::remove_const_t<std::remove_pointer_t<decltype(phi_src)>>;
+    oz::k_phi_rowscale<PT><<<(unsigned)c->Np, 256, 0, c->stream>>>(phi_src, c->Dp, c->N, c->D, c->rowscale,
+                                                                    shard_rows);
+    if (shard_rows) {
+      CKR(allreduce(c, c->rowscale, c->Np, ncclUint64, ncclMax));  // non-negative doubles order as bits
+      oz::k_rows_pow2<<<(unsigned)((c->Np + 255) / 256), 256, 0, c->stream>>>(c->N, c->Np, c->rowscale);
+    }
+    return 0;
+  };
   if (src64) {
-    oz::k_phi_rowscale<double><<<(unsigned)c->Np, 256, 0, c->stream>>>(src64, c->Dp, c->N, c->D, c->rowscale);
+    CKR(row_scales(src64));
     oz::k_phi_colscale<double><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(src64, c->Dp, c->N, c->Dp,
                                                                                         c->rowscale, c->colscale);
     oz::k_phi_planes<double><<<16 * c->sm_count, 256, 0, c->stream>>>(src64, c->Dp, c->Np, c->Dp, c->rowscale,
                                                                       c->colscale, c->phiq);
   } else {
-    oz::k_phi_rowscale<float><<<(unsigned)c->Np, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->rowscale);
+    CKR(row_scales(c->phi));
     oz::k_phi_colscale<float><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->Dp,
                                                                                        c->rowscale, c->colscale);
     oz::k_phi_planes<float><<<16 * c->sm_count, 256, 0, c->stream>>>(c->phi, c->Dp, c->Np, c->Dp, c->rowscale,
@@ -695,7 +709,7 @@ int oz_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, con
   // P's column maxima come fused out of k_direction inside a PCG solve; the
   // quantiser resets the V maxima that k_sum_splits accumulates next
   CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
-                               c->p_colmax_valid, c->vcolmax, st)));
+                               c->p_colmax_valid, c->vcolmax, st, true)));  // shards: the unsharded P scales
   int ns = 1;
   CKR((oz_contract<QW, false>(c, c->map_p[slot], c->Np, c->Dp, c->rowscale, (double*)c->vpart, &ns, st)));
   const int bs = elem_block(QW);
@@ -2168,6 +2182,9 @@ int attach_ranks(cofem_ctx* c, int nranks, int rank) {
   }
   c->nranks = nranks;
   c->rank = rank;
+  // dense shards share the row scales of the whole dictionary: rebuild the
+  // digit planes (collectively, on first use) if they were made before joining
+  if (c->kind == 0 && nranks > 1) c->oz_ready = false;
   // operand maps depend on the neighbours (halo extents): re-encode on next use
   for (int i = 0; i < 5; ++i) c->map_p_ok[i] = c->map_v_ok[i] = false;
   return 0;

@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(256, 3)
 // row scales r_i = 2^ceil(log2 max_j |Phi_ij|)
 template <typename PT>
 __global__ void k_phi_rowscale(const PT* __restrict__ phi, int64_t ld, int64_t n_real, int64_t d_real,
-                               double* __restrict__ rs) {
+                               double* __restrict__ rs, bool raw = false) {
   const int64_t i = blockIdx.x;
   double m = 0.0;
   for (int64_t j = threadIdx.x; j < d_real; j += blockDim.x) m = fmax(m, fabs((double)phi[i * ld + j]));
@@ -819,7 +819,13 @@ __global__ void k_phi_rowscale(const PT* __restrict__ phi, int64_t ld, int64_t n
     if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) rs[i] = (i < n_real && red[0] > 0) ? pow2_ceil(red[0]) : 1.0;
+  if (threadIdx.x == 0) rs[i] = raw ? red[0] : ((i < n_real && red[0] > 0) ? pow2_ceil(red[0]) : 1.0);
+}
+
+// raw row maxima (max-reduced over the column shards) -> power-of-two scales
+__global__ void k_rows_pow2(int64_t n_real, int64_t n_pad, double* __restrict__ rs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (int64_t)gridDim.x * blockDim.x)
+    rs[i] = (i < n_real && rs[i] > 0) ? pow2_ceil(rs[i]) : 1.0;
 }
 
 // column scales c_j = 2^ceil(log2 max_i |Phi_ij| / r_i)

@@ -12,8 +12,9 @@ convolution with halo exchange) is checked on the one available GPU.
   all-reduce, and every output row sees the same operand window);
 * convolution CoFEM: same CG step counts as the unsharded run, mu / alpha
   equal up to the summation order of the PCG dot products (~5e-9);
-* dense CoFEM: column shards (each with its own row scales) against the
-  float64 oracle, with the north_star tolerances.
+* dense CoFEM: column shards (sharing the whole dictionary's row scales and
+  the operand scales) against the float64 oracle / the reference's golden
+  run, and against the one-GPU run (same CG steps, mu / alpha to 1e-7).
 """
 
 import numpy as np
@@ -84,7 +85,8 @@ def test_time_sharded_convolution_cofem_matches_unsharded(world):
 @pytest.mark.parametrize("precision,world", [("ozaki", 2), ("ozaki", 3), ("fp64", 2)])
 def test_column_sharded_dense_cofem_matches_oracle(precision, world):
     """Dense column shards: the partial Phi_r P_r all-reduce, then each rank
-    re-derives the V column maxima for its Phi_r^T quantisation."""
+    re-derives the V column maxima (same row scales everywhere, so the same
+    V scales) for its Phi_r^T quantisation."""
     rng = np.random.default_rng(5)
     n, d = 512, 2048
     phi = (rng.standard_normal((n, d)) / np.sqrt(n)).astype(np.float32)
@@ -123,3 +125,27 @@ def test_group_failure_releases_the_other_ranks():
     finally:
         for c in contexts:
             c.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dense_mid_column_sharded_matches_reference_golden(world):
+    """BASELINE config 2 (N=4096, D=16384, K=20, 2-GPU D-sharded) as 2 / 4
+    column shards against the reference's own float64 run (golden vectors,
+    3 EM iterations): mu, alpha within 1e-5 (the bar is 1e-4), same support."""
+    from conftest import golden
+
+    g = golden("cofem_dense-mid_T3.npz")
+    c = S.CONFIGS["dense-mid"]
+    prob, z, _ = S.dense_cs_problem(c)
+    T = int(g["config"][3])
+    cfg = c.cofem_config("ozaki", iterations=T)
+    st, est, diag = run_cofem_threaded(prob, cfg, devices=[0] * world)
+    assert rel(est.mu, g["mu"]) <= 1e-5 and rel(st.alpha, g["alpha"]) <= 1e-5
+    np.testing.assert_array_equal(st.alpha < PRUNE, g["alpha"] < PRUNE)
+    assert np.all(np.abs(np.array([d["cg_steps"] for d in diag]) - g["cg_steps"]) <= 3)
+    # the shards share the unsharded row / operand scales: they track the
+    # one-GPU run up to the fp64 summation order of the partial products
+    st1, est1, diag1 = run_cofem(prob, cfg)
+    prob.op.release()
+    assert [d["cg_steps"] for d in diag] == [d["cg_steps"] for d in diag1]
+    assert rel(est.mu, est1.mu) <= 1e-7 and rel(st.alpha, st1.alpha) <= 1e-7
