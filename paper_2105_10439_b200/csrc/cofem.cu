@@ -753,7 +753,7 @@ void launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_
       cudaFuncSetAttribute(oz::band_kernel<QW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    oz::band_kernel<QW><<<grid, oz::NTHREADS, sm, c->stream>>>(map_a, map_b, nmb, nk, offset, c->hrows, c->opscale,
+    oz::band_kernel<QW><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(map_a, map_b, nmb, nk, offset, c->hrows, c->opscale,
                                                                 out, rows_real, colmax, st);
   } else {
     oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
@@ -861,7 +861,7 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   }
   Scalars sc = c->sc();
   CK(cudaGetLastError());
-  oz::band_kernel<QW, true><<<grid, oz::NTHREADS, sm, c->stream>>>(
+  oz::band_kernel<QW, true><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
       c->map_band_adj, c->map_v[QW / 8], nmb, nk, 0, c->hrows, c->opscale, (double*)c->Psi + qoff, c->D, nullptr, st,
       (const double*)c->P + qoff, c->ldq, c->alpha, beta, sc.pi + qoff, sc.partials, sc.ticket + 1);
   if (c->time_kernels) {

@@ -288,6 +288,72 @@ __device__ __forceinline__ void epilogue_row_comb(uint32_t tset_lane, double sca
   }
 }
 
+// band_kernel epilogue: 16 warps, warp (quarter, group) owns TMEM lane
+// quarter `quarter` (32 rows) and the 8 columns [q0, q0 + 8) -- twice the
+// warps of the contraction kernels' epilogue, so TMEM-load / global-memory
+// latency of one warp hides behind the others.
+template <int QW, bool TRACK>
+__device__ __forceinline__ void epi8(uint32_t tl, int q0, double scale, const double* __restrict__ op_scale,
+                                     double* o, unsigned long long (&cm)[8]) {
+  uint32_t r[5][8];
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]), "=r"(r[sb][5]),
+                   "=r"(r[sb][6]), "=r"(r[sb][7])
+                 : "r"(tl + sb * QW + q0));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
+                 "r"(0));
+  double v[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                         ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+    v[t] = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * (scale * __ldg(op_scale + q0 + t));
+  }
+  st_v4(o + q0, v[0], v[1], v[2], v[3]);
+  st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
+  if (TRACK) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const unsigned long long m = (unsigned long long)__double_as_longlong(v[t]) & 0x7fffffffffffffffull;
+      cm[t] = m > cm[t] ? m : cm[t];
+    }
+  }
+}
+
+template <int QW>
+__device__ __forceinline__ void epi8_comb(uint32_t tl, int q0, double scale, const double* __restrict__ op_scale,
+                                          double* o, const double (&p)[8], double alpha_j, double beta,
+                                          double (&pacc)[8]) {
+  uint32_t r[5][8];
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]), "=r"(r[sb][5]),
+                   "=r"(r[sb][6]), "=r"(r[sb][7])
+                 : "r"(tl + sb * QW + q0));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
+                 "r"(0));
+  double v[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                         ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+    const double u = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * (scale * __ldg(op_scale + q0 + t));
+    v[t] = beta * u + alpha_j * p[t];
+    pacc[t] += p[t] * v[t];
+  }
+  st_v4(o + q0, v[0], v[1], v[2], v[3]);
+  st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
+}
+
 // the calling epilogue warp's share of one tile row (column groups of parity half)
 template <int QW>
 __device__ __forceinline__ void epilogue_part(int half, bool track, uint32_t tset_lane, double scale,
@@ -498,6 +564,8 @@ constexpr int BAND_SETS = 3;
 constexpr int BAND_SETS = BAND_SETS_OVERRIDE;
 #endif
 constexpr int BAND_SET_COLS = 160;
+constexpr int BAND_EPI_WARPS = 16;                      // 4 lane quarters x 4 column groups of 8
+constexpr int BAND_NTHREADS = 64 + 32 * BAND_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, warps 2..17 epilogue
 template <int QW>
 struct BandCfg {
   static constexpr int B_STAGE = 4 * QW * KT;
@@ -508,7 +576,7 @@ struct BandCfg {
 // (P / out row stride p_ld, column offset of the chunk already applied) and
 // pi_out[q] = <P_q, Psi_q> through fixed-order block partials + last-block fold.
 template <int QW, bool COMB = false>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(BAND_NTHREADS, 1)
     band_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 int n_mblocks, int nk, int band_offset, const double* __restrict__ row_scale,
                 const double* __restrict__ op_scale, double* __restrict__ out, int64_t rows_real,
@@ -529,7 +597,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* tfull = band_full + 1;  // [BAND_SETS]
   uint64_t* tempty = tfull + BAND_SETS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + BAND_SETS);
-  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);  // [EPI_WARPS][QW], after the last tile
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);  // [BAND_EPI_WARPS][QW], after the last tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -540,7 +608,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(band_full, 1);
     for (int b = 0; b < BAND_SETS; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 32 * EPI_WARPS);
+      mbar_init(&tempty[b], 32 * BAND_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&map_a);
@@ -613,66 +681,71 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int quarter = warp & 3, grp = (warp - 2) >> 2;
+    const int q0 = grp * 8;
+    const bool active = q0 < QW;  // QW < 32: the surplus column groups only keep the barrier phases
     const int row_in_tile = quarter * 32 + lane;
-    unsigned long long cm[QW];
-    double pacc[QW];
+    unsigned long long cm[8];
+    double pacc[8];
 #pragma unroll
-    for (int q = 0; q < QW; ++q) {
-      cm[q] = 0ull;
-      pacc[q] = 0.0;
+    for (int t = 0; t < 8; ++t) {
+      cm[t] = 0ull;
+      pacc[t] = 0.0;
     }
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
       const int buf = it % BAND_SETS;
       const int64_t row = (int64_t)mb * BM + row_in_tile;
       const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
-      const double alpha_j = COMB ? alpha[row] : 0.0;
-      double pv[comb_pv<QW>()];
-      if (COMB) {
-        if (half == 0) comb_prefetch<QW, 0>(Pc + row * p_ld, pv);
-        else comb_prefetch<QW, 1>(Pc + row * p_ld, pv);
+      double pv[8];
+      double alpha_j = 0.0;
+      if (COMB && active) {
+        alpha_j = alpha[row];
+        const double* prow = Pc + row * p_ld + q0;
+        ld_v4(prow, pv[0], pv[1], pv[2], pv[3]);
+        ld_v4(prow + 4, pv[4], pv[5], pv[6], pv[7]);
       }
       mbar_wait(&tfull[buf], (it / BAND_SETS) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (OZ_VARIANT == 2) {
-        uint32_t r[5][8];
-        const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
-        for (int q0 = half * 8; q0 < QW; q0 += 16) {
-          for (int sb = 0; sb < 5; ++sb)
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                         : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]),
-                           "=r"(r[sb][5]), "=r"(r[sb][6]), "=r"(r[sb][7])
-                         : "r"(tl + sb * QW + q0));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-          for (int sb = 0; sb < 5; ++sb)
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
-                         "r"(0));
-          if (r[0][0] == 0x12345 && scale == 3.0) out[row] = 1.0;
-        }
-      } else if (COMB) {
-        const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
-        if (half == 0)
-          epilogue_row_comb<QW, 0>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
+      const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
+      if (active && OZ_VARIANT != 3 && OZ_VARIANT != 4) {
+        if (COMB)
+          epi8_comb<QW>(tl, q0, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
+        else if (out_colmax)
+          epi8<QW, true>(tl, q0, scale, op_scale, out + row * QW, cm);
         else
-          epilogue_row_comb<QW, 1>(tl, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
-      } else if (OZ_VARIANT != 3 && OZ_VARIANT != 4)
-        epilogue_part<QW>(half, out_colmax != nullptr, tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16),
-                          scale, op_scale, out + row * QW, cm);
+          epi8<QW, false>(tl, q0, scale, op_scale, out + row * QW, cm);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[buf]);
     }
-    if (out_colmax) warp_fold_max<QW>(cm, cmax + (warp - 2) * QW);
-    if (COMB) {
-      // pi partial of this warp: fixed shuffle tree per column -> smem slice
-      double* psl = reinterpret_cast<double*>(cmax) + (warp - 2) * QW;
+    // per-warp folds of the owned columns into this warp's [QW] smem slice (zeros elsewhere)
+    if (out_colmax) {
+      unsigned long long* slice = cmax + (warp - 2) * QW;
+      for (int q = lane; q < QW; q += 32) slice[q] = 0ull;
+      __syncwarp();
 #pragma unroll
-      for (int q = 0; q < QW; ++q) {
-        double v = pacc[q];
+      for (int t = 0; t < 8; ++t) {
+        unsigned long long m = cm[t];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, off);
+          m = x > m ? x : m;
+        }
+        if (lane == 0 && active) slice[q0 + t] = m;
+      }
+    }
+    if (COMB) {
+      double* psl = reinterpret_cast<double*>(cmax) + (warp - 2) * QW;
+      for (int q = lane; q < QW; q += 32) psl[q] = 0.0;
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        double v = pacc[t];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) psl[q] = v;
+        if (lane == 0 && active) psl[q0 + t] = v;
       }
     }
   }
@@ -680,18 +753,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (out_colmax && threadIdx.x < QW) {
     unsigned long long m = cmax[threadIdx.x];
-    for (int w = 1; w < EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
+    for (int w = 1; w < BAND_EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
     atomicMax(&out_colmax[threadIdx.x], m);
   }
   if (COMB) {
     const double* psl = reinterpret_cast<const double*>(cmax);
     if (threadIdx.x < QW) {
       double v = 0.0;
-      for (int w = 0; w < EPI_WARPS; ++w) v += psl[w * QW + threadIdx.x];  // fixed warp order
+      for (int w = 0; w < BAND_EPI_WARPS; ++w) v += psl[w * QW + threadIdx.x];  // fixed warp order
       partials[(int64_t)blockIdx.x * QW + threadIdx.x] = v;
     }
     double* outs[1] = {pi_out};
-    last_block_reduce(ticket, partials, QW, 1, outs, reinterpret_cast<double*>(cmax) + EPI_WARPS * QW);
+    last_block_reduce(ticket, partials, QW, 1, outs, reinterpret_cast<double*>(cmax) + BAND_EPI_WARPS * QW);
   }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
