@@ -772,8 +772,8 @@ int conv_quantize_v(cofem_ctx* c, const double* v, const Status* st) {
     CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np + (right ? lp : 0), QW, QW));
     c->map_v_ok[slot] = true;
   }
-  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, c->colscale, c->vq, c->vcolmax, c->v_colmax_valid,
-                               nullptr, st, true)));
+  CKR((oz_quantize<double, QW>(c, v, QW, 0, c->N, c->Np, nullptr, c->vq, c->vcolmax, c->v_colmax_valid,
+                               nullptr, st, true)));  // band operands carry no scale (hrows holds it)
   c->v_colmax_valid = false;
   return halo_exchange(c, c->vq, c->vq + c->Np * 4 * QW, (size_t)lp * 4 * QW, -1);
 }
@@ -789,7 +789,7 @@ int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, c
     else CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
     c->map_p_ok[slot] = true;
   }
-  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, c->colscale, c->pq, c->colmax + qoff,
+  CKR((oz_quantize<double, QW>(c, src, lds, qoff, c->D, c->Dp, nullptr, c->pq, c->colmax + qoff,
                                c->p_colmax_valid, c->vcolmax, st, true)));
   // halo: this shard's last lpad operand rows become the right neighbour's
   // first window rows (K-blocked planes: lpad / 64 contiguous blocks)

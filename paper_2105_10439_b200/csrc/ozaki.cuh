@@ -802,7 +802,7 @@ __global__ void k_colmax(int64_t k_real, int ldm, int qoff, int qw, const T* __r
   const int q = threadIdx.x % qw;
   double m = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * rpb + threadIdx.x / qw; k < k_real; k += (int64_t)gridDim.x * rpb) {
-    const double v = fabs((double)M[k * ldm + qoff + q] * pre[k]);
+    const double v = fabs(pre ? (double)M[k * ldm + qoff + q] * pre[k] : (double)M[k * ldm + qoff + q]);
     m = (v > m || v != v) ? v : m;
   }
   sm_cm[threadIdx.x] = m;
@@ -848,10 +848,20 @@ __global__ void __launch_bounds__(256, 3)
   for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
     const int64_t k0 = ch * QCHUNK_K;
     double x[QCHUNK_K];
+    if (k0 + QCHUNK_K <= k_real) {  // full chunk: 16 independent loads in flight
+      const T* mp = M + k0 * ldm + qoff + lane;
 #pragma unroll
-    for (int r = 0; r < QCHUNK_K; ++r) {
-      const int64_t k = k0 + r;
-      x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * __ldg(pre + k) : 0.0;
+      for (int r = 0; r < QCHUNK_K; ++r) x[r] = (double)mp[r * ldm];
+      if (pre) {
+#pragma unroll
+        for (int r = 0; r < QCHUNK_K; ++r) x[r] *= __ldg(pre + k0 + r);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < QCHUNK_K; ++r) {
+        const int64_t k = k0 + r;
+        x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * (pre ? __ldg(pre + k) : 1.0) : 0.0;
+      }
     }
     // |x is| <= 2^30, so v fits int32 and its four balanced base-256 digits
     // (those of digits4) are the bytes of (v + 0x80808080) ^ 0x80808080; a
