@@ -202,6 +202,7 @@ struct cofem_ctx {
   // workspace (T = float or double by precision)
   int ldq = 0;
   void *X = nullptr, *R = nullptr, *P = nullptr, *Psi = nullptr;
+  void* P2 = nullptr;  // the other direction buffer (k_direction writes P(u+1) there; swapped per step)
   void *V = nullptr, *vpart = nullptr, *ppart = nullptr, *tmpD = nullptr;
   size_t vpart_cap = 0, ppart_cap = 0;
   double *alpha = nullptr, *minv = nullptr, *theta = nullptr, *colsq = nullptr;
@@ -209,7 +210,7 @@ struct cofem_ctx {
   int8_t *probes = nullptr, *probe_store = nullptr;
   int* groups = nullptr;
   int groups_cap = 0;
-  double* scal = nullptr;  // rho0 | rho1 | rho_new | rn2 | pi | bn2 (ldq each)
+  double* scal = nullptr;  // rho0 | rho1 | rho_new | rn2 | pi | bn2 | gam0 | gam1 (ldq each)
   int* frozen = nullptr;
   double* partials = nullptr;
   unsigned* tickets = nullptr;
@@ -287,6 +288,8 @@ struct cofem_ctx {
     s.rn2 = scal + 3 * ldq;
     s.pi = scal + 4 * ldq;
     s.bn2 = scal + 5 * ldq;
+    s.gam[0] = scal + 6 * ldq;
+    s.gam[1] = scal + 7 * ldq;
     s.frozen = frozen;
     s.partials = partials;
     s.ticket = tickets;
@@ -323,10 +326,10 @@ cudaEvent_t next_event(cofem_ctx* c) {
 }
 
 void free_ws(cofem_ctx* c) {
-  void* ptrs[] = {c->X, c->R, c->P, c->Psi, c->V, c->vpart, c->ppart, c->tmpD, c->scal, c->frozen, c->partials};
+  void* ptrs[] = {c->X, c->R, c->P, c->P2, c->Psi, c->V, c->vpart, c->ppart, c->tmpD, c->scal, c->frozen, c->partials};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  c->X = c->R = c->P = c->Psi = c->V = c->vpart = c->ppart = c->tmpD = nullptr;
+  c->X = c->R = c->P = c->P2 = c->Psi = c->V = c->vpart = c->ppart = c->tmpD = nullptr;
   c->scal = nullptr;
   c->frozen = nullptr;
   c->partials = nullptr;
@@ -396,6 +399,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->X, dbytes));
   CK(cudaMalloc(&c->R, dbytes));
   CK(cudaMalloc(&c->P, dbytes));
+  CK(cudaMalloc(&c->P2, dbytes));
   CK(cudaMalloc(&c->Psi, dbytes));
   // the DCT passes transform all ldq columns at once; the contractions run
   // 32-column chunks
@@ -411,13 +415,14 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   c->ppart_cap = whole ? 0 : (size_t)max_splits * c->Dp * QCHUNK * ts;
   if (c->vpart_cap) CK(cudaMalloc(&c->vpart, c->vpart_cap));
   if (c->ppart_cap) CK(cudaMalloc(&c->ppart, c->ppart_cap));
-  CK(cudaMalloc(&c->scal, 6 * ldq * sizeof(double)));
+  CK(cudaMalloc(&c->scal, 8 * ldq * sizeof(double)));
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
   c->nblk_elem = 3 * c->sm_count;
   CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
   CK(cudaMemsetAsync(c->X, 0, dbytes, c->stream));
   CK(cudaMemsetAsync(c->R, 0, dbytes, c->stream));
   CK(cudaMemsetAsync(c->P, 0, dbytes, c->stream));
+  CK(cudaMemsetAsync(c->P2, 0, dbytes, c->stream));
   CK(cudaMemsetAsync(c->Psi, 0, dbytes, c->stream));
   if (c->kind == 2) {
     const int64_t n = c->dct_n, nc = n * ldq;
@@ -1216,7 +1221,9 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     // the kernel mirrors the status into the host-mapped slot: no copy in the stream
     k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
-        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot, (T*)c->X);
+        c->minv, ngroups, groups, sc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot, (T*)c->X, (T*)c->P2,
+        (const T*)c->P2);
+    std::swap(c->P, c->P2);  // P(u+1) is the next step's direction
     c->launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[slot], c->stream));
@@ -1324,7 +1331,8 @@ int pcg_multi(cofem_ctx** cs, int L, const double* betas, int q_real, const cofe
       k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c0->stream>>>(
           c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
           c->minv, 1, nullptr, c->sc(), c->colscale, fused ? c->colmax : nullptr, st, agg,
-          l == L - 1 ? c0->d_hst + slot : nullptr, (T*)c->X);
+          l == L - 1 ? c0->d_hst + slot : nullptr, (T*)c->X, (T*)c->P2, (const T*)c->P2);
+      std::swap(c->P, c->P2);
       c->launches++;
     }
     CK(cudaGetLastError());

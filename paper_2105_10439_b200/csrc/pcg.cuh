@@ -20,6 +20,7 @@ struct Scalars {
   double* rn2;      // ||R_q||^2 (contiguous after rho_new: one allreduce)
   double* pi;       // <P_q, A P_q>
   double* bn2;      // ||B_q||^2
+  double* gam[2];   // gamma = rho / pi of the step, by step parity (batched X updates)
   int* frozen;      // breakdown flags
   double* partials; // nblocks x 2 x ldq scratch
   unsigned* ticket; // last-block counters (one per reduction site)
@@ -231,6 +232,7 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
   if (blockIdx.x == 0 && threadIdx.x < ldq) {
     if (q < q_real && pi == 0.0) sc.frozen[q] = 1;
     if (colmax_reset) colmax_reset[threadIdx.x] = 0ull;  // consumed by k_direction below
+    sc.gam[parity][q] = gamma;                           // k_direction's (batched) X update
   }
   const T gm = T(gamma);
   double s_rn = 0.0, s_rho = 0.0;
@@ -276,14 +278,21 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
 // (or R for the printed recursion), rho <- rho_new.  step == 0 is the
 // initialisation pass (no convergence test).  With `colmax` set, also the
 // per-column max of |pre_j P_jq| for the next Phi P quantisation.
-// With X set (step >= 1) the kernel first applies the step's solution update
-// X += P gamma (gamma = rho/pi as k_update derived it), also on the step that
-// stops the solve.
+// With X set (step >= 1) the kernel also applies the solution updates
+// X += P(u) gamma_u (gamma_u = rho/pi as k_update stored it), in pairs: an odd
+// step defers its update, the next (even) step applies both,
+//   X = (X + P(u-1) gamma_{u-1}) + P(u) gamma_u
+// (the order of the one-step-at-a-time recursion, so the bits are the same)
+// with P(u-1) still intact in Pprev -- one read-modify-write of X per two
+// steps.  The stopping step applies whatever is pending.  P(u+1) goes to
+// Pdst (nullptr: in place); the host swaps the two direction buffers, so at
+// an even step Pdst == Pprev (each element read before it is overwritten).
 template <typename T>
 __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
                             T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
                             const double* pre, unsigned long long* colmax, Status* st,
-                            const double* agg = nullptr, Status* mirror = nullptr, T* X = nullptr) {
+                            const double* agg = nullptr, Status* mirror = nullptr, T* X = nullptr,
+                            T* Pdst = nullptr, const T* Pprev = nullptr) {
   // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
   // mirror: host-mapped status slot the host polls (no copy in the stream)
   {
@@ -336,27 +345,35 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
       }
     }
     if (stop) {
-      if (X) {  // the last step's solution update
+      if (X) {  // the pending solution updates
         const ColMap m(ldq);
-        const T gm = T(safe_ratio(sc.rho[cur][m.q], sc.pi[m.q]));
+        const T gm = T(sc.gam[cur][m.q]);
+        const bool pair = (step & 1) == 0 && Pprev;
+        const T gp = pair ? T(sc.gam[nxt][m.q]) : T(0);
         for (int64_t j = m.r0; j < rows; j += m.rstep) {
           const int64_t e = j * ldq + m.q;
-          X[e] = X[e] + P[e] * gm;
+          T x = X[e];
+          if (pair) x = x + Pprev[e] * gp;
+          X[e] = x + P[e] * gm;
         }
       }
       return;
     }
   }
+  if (!Pdst) Pdst = P;
   const ColMap m(ldq);
   const int q = m.q;
   const int g = group_of_col ? group_of_col[q] : 0;
   const double eta = safe_ratio(sc.rho_new[q], sc.rho[cur][q]);
   const T et = T(eta);
-  const bool upd_x = X && step >= 1;
-  const T gm = upd_x ? T(safe_ratio(sc.rho[cur][q], sc.pi[q])) : T(0);
+  // X updates: every step without Pprev (one-step mode), even steps in pairs
+  const bool upd_x = X && step >= 1 && (!Pprev || (step & 1) == 0);
+  const bool pair = upd_x && Pprev;
+  const T gm = upd_x ? T(sc.gam[cur][q]) : T(0);
+  const T gp = pair ? T(sc.gam[nxt][q]) : T(0);
   double pmax = 0.0;
   for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
-    T r[UNR], p[UNR], x[UNR];
+    T r[UNR], p[UNR], x[UNR], pp[UNR];
     double mv[UNR], pr[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -366,6 +383,7 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
         r[u] = R[e];
         p[u] = P[e];
         if (upd_x) x[u] = X[e];
+        if (pair) pp[u] = Pprev[e];
         mv[u] = minv[j * ngroups + g];
         pr[u] = colmax ? pre[j] : 0.0;
       }
@@ -374,7 +392,7 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         const int64_t j = j0 + (int64_t)u * m.rstep;
-        if (j < rows) X[j * ldq + q] = x[u] + p[u] * gm;
+        if (j < rows) X[j * ldq + q] = (pair ? x[u] + pp[u] * gp : x[u]) + p[u] * gm;
       }
     }
 #pragma unroll
@@ -383,7 +401,7 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
       if (j < rows) {
         const T w = (q < q_real) ? T(dd(r[u]) * mv[u]) : T(0);
         const T pn = p[u] * et + (printed ? r[u] : w);
-        P[j * ldq + q] = pn;
+        Pdst[j * ldq + q] = pn;
         if (colmax) {
           const double v = fabs(dd(pn) * pr[u]);
           pmax = (v > pmax || v != v) ? v : pmax;
