@@ -68,9 +68,10 @@ def test_time_sharded_convolution_apply_is_bitwise(dim, ntaps, world, q):
     assert rel(full_f, ref) <= 1e-8
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_time_sharded_convolution_cofem_matches_unsharded(world):
-    c = S.ConvConfig("conv-shard", 8192, 256, 20.0, 0.01, 0.05, 20, 3, 200, 1e-5)
+@pytest.mark.parametrize("world,K", [(2, 20), (3, 20), (2, 40)])
+def test_time_sharded_convolution_cofem_matches_unsharded(world, K):
+    """K = 40: two column chunks per contraction, each with its own halo exchange."""
+    c = S.ConvConfig("conv-shard", 8192, 256, 20.0, 0.01, 0.05, K, 3, 200, 1e-5)
     prob, z = S.conv_problem(c)
     cfg = c.cofem_config("ozaki")
     st1, est1, d1 = run_cofem(prob, cfg)
