@@ -487,6 +487,14 @@ def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return
+    # torchrun pins OMP_NUM_THREADS=1 per rank; the CPU reference (rank 0 alone)
+    # gets every host thread for its BLAS / FFT calls
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        pass
     from paper_2105_10439_b200 import simulate as S
 
     structured = args.config in S.CONV_CONFIGS or args.config in S.DCT_CONFIGS
@@ -540,8 +548,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch_distributed(n):
+    """`python bench.py --gpus N` outside torchrun: relaunch under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:
