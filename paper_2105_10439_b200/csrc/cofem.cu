@@ -224,6 +224,8 @@ struct cofem_ctx {
   // Ozaki (int8 tensor-core) contraction state
   bool oz_ready = false;
   int8_t* phiq = nullptr;        // [4][Np][Dp] signed digit planes
+  int8_t* phiqT = nullptr;       // [4][Dp][Np] the same planes transposed: Phi^T V streams K-major too
+  CUtensorMap map_phiT{};
   double *rowscale = nullptr, *colscale = nullptr;  // Np, Dp powers of two
   int8_t *pq = nullptr, *vq = nullptr;              // operand planes, K-blocked [Dp/64][4][QW][64] / [Np/64][...]
   double* opscale = nullptr;                        // QCHUNK column scales
@@ -587,6 +589,12 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
     CK(cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)));
     CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
     CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
+    if (cudaMalloc(&c->phiqT, (size_t)4 * c->Np * c->Dp) == cudaSuccess) {
+      CKR(encode_u8_3d(&c->map_phiT, c->phiqT, c->Np, c->Dp, 4, oz::KT, oz::BM, 4));
+    } else {
+      cudaGetLastError();  // no room for the transposed copy: Phi^T V reads the planes MN-major
+      c->phiqT = nullptr;
+    }
   }
   // column shards agree on the row scales (max over every shard's columns),
   // so each shard's digit planes are the unsharded dictionary's columns and
@@ -616,6 +624,12 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
                                                                      c->colscale, c->phiq);
   }
   c->launches += 3;
+  if (c->phiqT) {
+    const int64_t tiles = (c->Np / 64) * (c->Dp / 64);
+    oz::k_planes_transpose<<<dim3((unsigned)std::min<int64_t>(tiles, 8 * c->sm_count), 1, 4), 256, 0, c->stream>>>(
+        c->phiq, c->Np, c->Dp, c->phiqT);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
   c->oz_ready = true;
@@ -680,15 +694,23 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
   }
   const int n_items = (int)(n_mblocks * sp.nsplit);
   const int grid = std::min(n_items, c->sm_count);
-  const CUtensorMap& map_a = BWD ? c->map_phi_bwd : c->map_phi_fwd;
+  // Phi^T V: the K-major transposed planes when present (same integers, same
+  // splits -> bitwise the MN-major result, read like Phi P), else MN-major
+  const bool trans = BWD && c->phiqT;
+  const CUtensorMap& map_a = trans ? c->map_phiT : (BWD ? c->map_phi_bwd : c->map_phi_fwd);
   cudaEvent_t e0 = nullptr;
   if (c->time_kernels) {
     e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  oz::contract_kernel<QW, BWD ? oz::MODE_BWD : oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-      map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
-      n_rows_out, nullptr, st, sp.nsplit, QW);
+  if (BWD && !trans)
+    oz::contract_kernel<QW, oz::MODE_BWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+        map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
+        n_rows_out, nullptr, st, sp.nsplit, QW);
+  else
+    oz::contract_kernel<QW, oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+        map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
+        n_rows_out, nullptr, st, sp.nsplit, QW);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -2040,7 +2062,7 @@ int cofem_destroy(cofem_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_ws(c);
   void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
-                  c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->rowscale, c->colscale,
+                  c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
                   c->cf_H, c->cf_Hr, c->lg_tmp};

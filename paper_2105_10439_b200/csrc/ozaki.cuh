@@ -922,6 +922,40 @@ __global__ void k_phi_colscale(const PT* __restrict__ phi, int64_t ld, int64_t n
   cs[j] = m > 0 ? pow2_ceil(m) : 1.0;
 }
 
+// K-major copy of the digit planes for Phi^T V: planesT[a][j][i] = planes[a][i][j]
+// (64 x 64-byte tiles; each thread transposes one 4 x 4 byte block in
+// registers, a padded word tile in smem turns it into 16-B row stores).
+// rows = Np, cols = Dp (multiples of 64); grid.z = plane.
+__global__ void __launch_bounds__(256) k_planes_transpose(const int8_t* __restrict__ planes, int64_t rows,
+                                                          int64_t cols, int8_t* __restrict__ planesT) {
+  __shared__ uint32_t tile[64][17];  // transposed tile: 64 rows (j) x 16 words (64 i-bytes), padded
+  const int64_t plane = blockIdx.z;
+  const int8_t* src = planes + plane * rows * cols;
+  int8_t* dst = planesT + plane * rows * cols;
+  const int t = threadIdx.x;
+  for (int64_t tb = blockIdx.x; tb < (rows / 64) * (cols / 64); tb += gridDim.x) {
+    const int64_t i0 = (tb / (cols / 64)) * 64, j0 = (tb % (cols / 64)) * 64;
+    const int br = t >> 4, bc = t & 15;  // 4 x 4 block (rows 4 br.., bytes 4 bc..)
+    uint32_t w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      w[r] = *reinterpret_cast<const uint32_t*>(src + (i0 + 4 * br + r) * cols + j0 + 4 * bc);
+    // byte transpose: out word c holds byte c of w[0..3]
+    const uint32_t A = __byte_perm(w[0], w[1], 0x5140), B = __byte_perm(w[0], w[1], 0x7362);
+    const uint32_t C = __byte_perm(w[2], w[3], 0x5140), E = __byte_perm(w[2], w[3], 0x7362);
+    __syncthreads();  // the previous tile's reads are done
+    tile[4 * bc + 0][br] = __byte_perm(A, C, 0x5410);
+    tile[4 * bc + 1][br] = __byte_perm(A, C, 0x7632);
+    tile[4 * bc + 2][br] = __byte_perm(B, E, 0x5410);
+    tile[4 * bc + 3][br] = __byte_perm(B, E, 0x7632);
+    __syncthreads();
+    const int jj = t >> 2, part = t & 3;  // row jj of the transposed tile, words 4 part ..
+    const uint4 v = make_uint4(tile[jj][4 * part], tile[jj][4 * part + 1], tile[jj][4 * part + 2],
+                               tile[jj][4 * part + 3]);
+    *reinterpret_cast<uint4*>(dst + (j0 + jj) * rows + i0 + 16 * part) = v;
+  }
+}
+
 // digit planes [4][Np][Dp] of round(Phi / (r c) * 2^30)
 template <typename PT>
 __global__ void k_phi_planes(const PT* __restrict__ phi, int64_t ld, int64_t np, int64_t dp,
