@@ -840,50 +840,60 @@ __global__ void __launch_bounds__(256, 3)
   if (st && st->done) return;
   if (blockIdx.x == 0 && threadIdx.x < QW) scale_out[threadIdx.x] = col_scale(colmax[threadIdx.x]);
   if (blockIdx.x == 0 && reset && threadIdx.x < 32) reset[threadIdx.x] = 0ull;
-  const int lane = threadIdx.x & 31;
-  if (lane >= QW) return;
-  const double is = SCALE30 / col_scale(colmax[lane]);  // NaN for a non-finite column
-  const int64_t nchunks = k_pad / QCHUNK_K;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += nwarps) {
-    const int64_t k0 = ch * QCHUNK_K;
-    double x[QCHUNK_K];
-    if (k0 + QCHUNK_K <= k_real) {  // full chunk: 16 independent loads in flight
-      const T* mp = M + k0 * ldm + qoff + lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool act = lane < QW;
+  const double is = act ? SCALE30 / col_scale(colmax[lane]) : 0.0;  // NaN for a non-finite column
+  // the block's 8 warps cover 128 rows = two K-blocks; their digit words are
+  // staged in smem in the K-blocked layout (64-B rows padded to 80 B) and
+  // leave as whole 64-B lines (a 16-B store per lane leaves half-written
+  // sectors that L2 has to merge or read-modify-write)
+  __shared__ uint4 stage[2 * 4 * QW * 5];
+  const int64_t ngroups = k_pad / 128;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int64_t k0 = g * 128 + warp * QCHUNK_K;
+    if (act) {
+      double x[QCHUNK_K];
+      if (k0 + QCHUNK_K <= k_real) {  // full chunk: 16 independent loads in flight
+        const T* mp = M + k0 * ldm + qoff + lane;
 #pragma unroll
-      for (int r = 0; r < QCHUNK_K; ++r) x[r] = (double)mp[r * ldm];
-      if (pre) {
+        for (int r = 0; r < QCHUNK_K; ++r) x[r] = (double)mp[r * ldm];
+        if (pre) {
 #pragma unroll
-        for (int r = 0; r < QCHUNK_K; ++r) x[r] *= __ldg(pre + k0 + r);
+          for (int r = 0; r < QCHUNK_K; ++r) x[r] *= __ldg(pre + k0 + r);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < QCHUNK_K; ++r) {
+          const int64_t k = k0 + r;
+          x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * (pre ? __ldg(pre + k) : 1.0) : 0.0;
+        }
       }
-    } else {
+      // |x is| <= 2^30, so v fits int32 and its four balanced base-256 digits
+      // (those of digits4) are the bytes of (v + 0x80808080) ^ 0x80808080; a
+      // 4 x 4 byte transpose per 4 rows packs them plane by plane
+      uint32_t w[4][QCHUNK_K / 4];
+      const bool ok = is == is;
 #pragma unroll
-      for (int r = 0; r < QCHUNK_K; ++r) {
-        const int64_t k = k0 + r;
-        x[r] = k < k_real ? (double)M[k * ldm + qoff + lane] * (pre ? __ldg(pre + k) : 1.0) : 0.0;
+      for (int j = 0; j < QCHUNK_K / 4; ++j) {
+        uint32_t u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          u[i] = ok ? (((uint32_t)__double2int_rn(x[4 * j + i] * is) + 0x80808080u) ^ 0x80808080u) : 0u;
+        const uint32_t A = __byte_perm(u[0], u[1], 0x5140), B = __byte_perm(u[0], u[1], 0x7362);
+        const uint32_t C = __byte_perm(u[2], u[3], 0x5140), E = __byte_perm(u[2], u[3], 0x7362);
+        w[3][j] = __byte_perm(A, C, 0x5410);  // byte 0 (least significant digit)
+        w[2][j] = __byte_perm(A, C, 0x7632);
+        w[1][j] = __byte_perm(B, E, 0x5410);
+        w[0][j] = __byte_perm(B, E, 0x7632);  // byte 3 (most significant digit)
       }
+      const int kb = warp >> 2, part = warp & 3;  // K-block of the group, 16-B quarter of its 64-B rows
+#pragma unroll
+      for (int a = 0; a < 4; ++a) stage[((kb * 4 + a) * QW + lane) * 5 + part] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
     }
-    // |x is| <= 2^30, so v fits int32 and its four balanced base-256 digits
-    // (those of digits4) are the bytes of (v + 0x80808080) ^ 0x80808080; a
-    // 4 x 4 byte transpose per 4 rows packs them plane by plane
-    uint32_t w[4][QCHUNK_K / 4];
-    const bool ok = is == is;
-#pragma unroll
-    for (int j = 0; j < QCHUNK_K / 4; ++j) {
-      uint32_t u[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        u[i] = ok ? (((uint32_t)__double2int_rn(x[4 * j + i] * is) + 0x80808080u) ^ 0x80808080u) : 0u;
-      const uint32_t A = __byte_perm(u[0], u[1], 0x5140), B = __byte_perm(u[0], u[1], 0x7362);
-      const uint32_t C = __byte_perm(u[2], u[3], 0x5140), E = __byte_perm(u[2], u[3], 0x7362);
-      w[3][j] = __byte_perm(A, C, 0x5410);  // byte 0 (least significant digit)
-      w[2][j] = __byte_perm(A, C, 0x7632);
-      w[1][j] = __byte_perm(B, E, 0x5410);
-      w[0][j] = __byte_perm(B, E, 0x7632);  // byte 3 (most significant digit)
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-      *reinterpret_cast<uint4*>(planes + kb_offset(QW, a, lane, k0)) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(planes + kb_offset(QW, 0, 0, g * 128));
+    for (int i = threadIdx.x; i < 2 * 4 * QW * 4; i += blockDim.x) dst[i] = stage[(i >> 2) * 5 + (i & 3)];
+    __syncthreads();
   }
 }
 
