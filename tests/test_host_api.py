@@ -184,3 +184,31 @@ def test_ozaki_model_is_close_to_exact():
     U = rng.standard_normal((40, 5))
     assert np.abs(op.apply(V) - phi @ V).max() <= 1e-8 * np.abs(phi @ V).max()
     assert np.abs(op.adjoint(U) - phi.T @ U).max() <= 1e-8 * np.abs(phi.T @ U).max()
+
+
+def _digits4(v):
+    """Balanced base-256 digits (ozaki.cuh digits4): v = sum_a d_a 256^(3-a), d_a in [-128, 127]."""
+    d = np.zeros((4,) + v.shape, np.int64)
+    v = v.copy()
+    for a in range(3, -1, -1):
+        lo = ((v & 0xFF) ^ 0x80) - 0x80
+        d[a] = lo
+        v = (v - lo) >> 8
+    return d
+
+
+def test_quantiser_byte_digits_equal_balanced_digits():
+    """k_quantize packs the digits as the bytes of (v + 0x80808080) ^ 0x80808080
+    (ozaki.cuh); for every |v| <= 2^30 (the fixed-point range) these are the
+    balanced digits, and they reconstruct v exactly."""
+    rng = np.random.default_rng(0)
+    v = np.concatenate([rng.integers(-2**30, 2**30 + 1, 100000),
+                        [2**30, -2**30, 0, -1, 1, 127, 128, -128, -129, 255, 256, -256, 2**24, -2**24]]).astype(np.int64)
+    d = _digits4(v)
+    u = ((v.astype(np.uint64) + 0x80808080) & 0xFFFFFFFF) ^ 0x80808080
+    for a in range(4):
+        byte = (u >> np.uint64(8 * (3 - a))) & np.uint64(0xFF)
+        np.testing.assert_array_equal(((byte ^ np.uint64(0x80)).astype(np.int64) - 0x80), d[a])
+    recon = sum(d[a] * (256 ** (3 - a)) for a in range(4))
+    np.testing.assert_array_equal(recon, v)
+    assert d.min() >= -128 and d.max() <= 127
