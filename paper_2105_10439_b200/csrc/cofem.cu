@@ -589,7 +589,9 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
     CK(cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)));
     CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
     CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
-    if (cudaMalloc(&c->phiqT, (size_t)4 * c->Np * c->Dp) == cudaSuccess) {
+    // COFEM_MN_MAJOR_ONLY: skip the transposed copy (Phi^T V reads the planes
+    // MN-major) -- tests compare the two paths bitwise
+    if (!getenv("COFEM_MN_MAJOR_ONLY") && cudaMalloc(&c->phiqT, (size_t)4 * c->Np * c->Dp) == cudaSuccess) {
       CKR(encode_u8_3d(&c->map_phiT, c->phiqT, c->Np, c->Dp, 4, oz::KT, oz::BM, 4));
     } else {
       cudaGetLastError();  // no room for the transposed copy: Phi^T V reads the planes MN-major

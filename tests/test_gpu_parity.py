@@ -656,3 +656,37 @@ def test_run_cofem_device_probes_equal_host_probes():
     np.testing.assert_array_equal(st1.alpha, st2.alpha)
     np.testing.assert_array_equal(est1.mu, est2.mu)
     assert [d["cg_steps"] for d in d1] == [d["cg_steps"] for d in d2]
+
+
+def test_transposed_planes_equal_mn_major_planes_bitwise():
+    """Phi^T V streams a K-major transposed copy of the digit planes; without it
+    (COFEM_MN_MAJOR_ONLY) the same integers are read MN-major.  Same splits,
+    exact int32 sums: the two CoFEM runs are bitwise equal."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, numpy as np\n"
+        "from paper_2105_10439_b200 import run_cofem\n"
+        "from paper_2105_10439_b200 import simulate as S\n"
+        "c = S.CONFIGS['dense-mid']\n"
+        "prob, z, _ = S.dense_cs_problem(c)\n"
+        "st, est, diag = run_cofem(prob, c.cofem_config('ozaki', iterations=2))\n"
+        "print(json.dumps({'mu': est.mu.tolist(), 'alpha': st.alpha.tolist(), 'steps': [d['cg_steps'] for d in diag]}))\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mn in (False, True):
+        env = dict(os.environ, PYTHONPATH=root)
+        if mn:
+            env["COFEM_MN_MAJOR_ONLY"] = "1"
+        else:
+            env.pop("COFEM_MN_MAJOR_ONLY", None)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["steps"] == outs[1]["steps"]
+    np.testing.assert_array_equal(np.array(outs[0]["mu"]), np.array(outs[1]["mu"]))
+    np.testing.assert_array_equal(np.array(outs[0]["alpha"]), np.array(outs[1]["alpha"]))
