@@ -959,20 +959,20 @@ int conv_fft_system_apply(cofem_ctx* c, double beta, const Status* stt) {
 template <int N1, int N2, int MODE>
 void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
   const int64_t n = c->dct_n, ldq = c->ldq;
-  constexpr int NT = 4 * N2;
-  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
+  constexpr int FPI = DCT_FPI, NT = FPI * N2;
+  constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dctf::k_dct_pass<N1, N2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  const int items = (int)(n * (ldq / 8));
+  const int items = (int)(n * (ldq / (2 * FPI)));
   int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));  // blocks that fit one SM's shared memory
   if (per_sm > 16) per_sm = 16;
   const int grid = std::min(items, per_sm * c->sm_count);
   dctf::k_dct_pass<N1, N2, MODE><<<grid, NT, smem, c->stream>>>(
-      src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / 8), c->dct_wN, c->dct_tw,
+      src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / (2 * FPI)), c->dct_wN, c->dct_tw,
       c->dct_gridT, stt);
   c->launches++;
 }

@@ -173,12 +173,15 @@ __device__ __forceinline__ void inv_pre(double2 xk, double2 xnk, double2 twk, do
 // the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
 //   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(mask .* DCT-II)
 //   with the transposed 0/1 grid gridT[o n + k] (outer index o, coefficient k along m)
-template <int N1, int N2, int MODE>
-__global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
+#ifndef DCT_FPI
+#define DCT_FPI 2  // complex FFTs (column pairs) per item / block: 2 measured best (4: -7 %, 1: -16 %)
+#endif
+template <int N1, int N2, int MODE, int FPI = DCT_FPI>
+__global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
                int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tw,
                const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
-  constexpr int N = N1 * N2, FPI = 4, TPF = N2, NT = FPI * TPF;
+  constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
   constexpr int ZS = N1 * (N2 + 1);  // complex entries per FFT region (padded transpose)
   constexpr int KS = NT / FPI;       // k stride between a thread's loop iterations
   if (stt && stt->done) return;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
   const double c_0 = sqrt(1.0 / N), c_k = sqrt(2.0 / N);
   for (int item = blockIdx.x; item < nouter * ngroups; item += gridDim.x) {
     const int o = item / ngroups, g = item % ngroups;
-    const int64_t base = (int64_t)o * stride_o + g * 8;
+    const int64_t base = (int64_t)o * stride_o + g * (2 * FPI);
     __syncthreads();  // the previous item is done with shared memory
     // ---- load: 4 consecutive threads copy one contiguous 64-B row of the item;
     // cp.async keeps every copy of the thread in flight without registers
