@@ -907,8 +907,8 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
 // ---- convolution, float64 FFT path (dct.cuh k_conv_fft_pass) ----------------
 // dst (D x ldq) = Phi src (adj: Phi^T src) for all ldq columns at once
 int conv_fft_pass(cofem_ctx* c, const double* src, double* dst, bool adj, const Status* stt) {
-  constexpr int N1 = 32, N2 = 32, NT = 4 * N2;
-  constexpr size_t smem = (size_t)4 * N1 * (N2 + 1) * sizeof(double2);
+  constexpr int N1 = 32, N2 = 32, FPI = DCT_FPI, NT = FPI * N2;
+  constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(dctf::k_conv_fft_pass<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -916,10 +916,10 @@ int conv_fft_pass(cofem_ctx* c, const double* src, double* dst, bool adj, const 
   }
   const int L = c->conv_L, valid = CONV_FFT_N - (L - 1);
   const int nblocks = (int)((c->D + valid - 1) / valid);
-  const int items = nblocks * (c->ldq / 8);
-  const int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));
+  const int items = nblocks * (c->ldq / (2 * FPI));
+  const int per_sm = std::min(16, std::max(1, (int)((228 * 1024) / (smem + 1024))));
   const int grid = std::min(items, per_sm * c->sm_count);
-  dctf::k_conv_fft_pass<N1, N2><<<grid, NT, smem, c->stream>>>(src, dst, c->D, c->ldq, c->ldq / 8, nblocks, valid,
+  dctf::k_conv_fft_pass<N1, N2><<<grid, NT, smem, c->stream>>>(src, dst, c->D, c->ldq, c->ldq / (2 * FPI), nblocks, valid,
                                                                 adj ? 0 : L - 1, L - 1, adj ? c->cf_Hr : c->cf_H,
                                                                 c->dct_wN, stt);
   c->launches++;

@@ -309,12 +309,12 @@ __global__ void k_scatter(int64_t nm, int ldq, const int64_t* __restrict__ mask,
 namespace cofem {
 namespace dctf {
 
-template <int N1, int N2>
-__global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
+template <int N1, int N2, int FPI = DCT_FPI>
+__global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     k_conv_fft_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t rows, int ldq, int ngroups,
                     int nblocks, int valid, int in_shift, int keep0, const double2* __restrict__ spec,
                     const double2* __restrict__ wN, const Status* __restrict__ stt) {
-  constexpr int N = N1 * N2, FPI = 4, TPF = N2, NT = FPI * TPF;
+  constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
   constexpr int ZS = N1 * (N2 + 1);
   if (stt && stt->done) return;
   extern __shared__ double2 zsm[];
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
     for (int e = t; e < FPI * N; e += NT) {
       const int f = e % FPI, m = e / FPI;
       const int64_t row = w0 + m;
-      if (row >= 0 && row < rows) cp_async16(zsm + f * ZS + m, src + row * ldq + g * 8 + 2 * f);
+      if (row >= 0 && row < rows) cp_async16(zsm + f * ZS + m, src + row * ldq + g * (2 * FPI) + 2 * f);
       else zsm[f * ZS + m] = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(4 * N2, (N2 >= 32 ? 3 : 4))
     for (int e = t; e < FPI * valid; e += NT) {
       const int f = e % FPI, mm = e / FPI;
       const int64_t row = o0 + mm;
-      if (row < rows) st_out(reinterpret_cast<double2*>(dst + row * ldq + g * 8 + 2 * f), zsm[f * ZS + keep0 + mm]);
+      if (row < rows) st_out(reinterpret_cast<double2*>(dst + row * ldq + g * (2 * FPI) + 2 * f), zsm[f * ZS + keep0 + mm]);
     }
   }
 }
