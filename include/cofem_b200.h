@@ -42,9 +42,10 @@ enum cofem_status {
 /* Arithmetic of the column blocks and of the Phi contractions.
  * FP32: fp32 vectors, fp32 contraction accumulators, fp64 scalar reductions
  *       (the north_star's "GPU runs fp32").
- * FP64: Phi stays fp32 in HBM; vectors, contraction accumulators and scalars
- *       are fp64 (fp32 Phi entries are exact in fp64, so this reproduces the
- *       reference's float64 arithmetic up to summation order).
+ * FP64: CUDA-core DFMA contractions over the dictionary as given (float32
+ *       entries, or the exact float64 ones of cofem_set_dictionary_f64);
+ *       vectors, accumulators and scalars fp64: the reference's float64
+ *       arithmetic up to summation order.
  * OZAKI: fp64 vectors and scalars; the two Phi contractions run on the int8
  *       tensor cores (tcgen05.mma.kind::i8) over a 32-bit fixed-point copy of
  *       Phi (four signed digit planes, 4 B / entry) with exact int32
@@ -99,18 +100,21 @@ int cofem_destroy(cofem_ctx* ctx);
 
 /* Causal convolution dictionary (operators.ConvolutionOperator,
  * operators.py:182-225; BASELINE config 3): the D x D lower-triangular
- * Toeplitz matrix Phi_ij = taps[i - j] for 0 <= i - j < ntaps.  Applied as
- * banded int8 tensor-core contractions (Phi and Phi^T), so it requires
- * precision COFEM_OZAKI.  The reference's filter (1 - rho)^m is passed
- * truncated where it falls below the fixed-point resolution. */
+ * Toeplitz matrix Phi_ij = taps[i - j] for 0 <= i - j < ntaps.  COFEM_OZAKI:
+ * banded int8 tensor-core contractions (Phi and Phi^T; any filter length up to
+ * 32512 taps; the reference's filter (1 - rho)^m is passed truncated where it
+ * falls below the fixed-point resolution).  COFEM_FP64: float64 overlap-save
+ * FFT passes (filters up to 512 taps, one GPU). */
 int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const double* taps, int64_t ntaps,
                              int precision);
 
-/* 2-D partial DCT dictionary (BASELINE config 4; the 2-D analogue of
+/* 2-D partial DCT dictionary (BASELINE config 5; the 2-D analogue of
  * operators.SubsampledDctOperator, operators.py:132-179): z is an n x n image
  * (row-major, D = n^2), Phi z = the coefficients `mask` (flat k n + l) of its
- * orthonormal 2-D DCT-II.  Applied as four int8 tensor-core stages against
- * the n x n DCT matrix; requires COFEM_OZAKI and n a multiple of 128. */
+ * orthonormal 2-D DCT-II.  Phi^T Phi runs as three fused float64 FFT passes
+ * (row DCT-II; column DCT-II, mask, DCT-III; row DCT-III + PCG combine);
+ * n a power of two in [64, 1024]; precision COFEM_FP64 (COFEM_OZAKI is
+ * accepted as an alias: the passes are float64 either way). */
 int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision);
 
 /* Upload Phi (N x D_local float32, row stride `ld` elements) from host
@@ -118,9 +122,13 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
  * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */
 int cofem_set_dictionary(cofem_ctx* ctx, const float* phi, int64_t ld, int on_device);
 
-/* Upload a float64 Phi from host memory (row stride `ld`).  The fp32/fp64
- * modes keep its float32 rounding; in COFEM_OZAKI mode the fixed-point digit
- * planes are built from the exact float64 values (no float32 rounding). */
+/* Upload a float64 Phi from host memory (row stride `ld`).  COFEM_FP64 keeps
+ * the exact float64 entries in HBM and multiplies them (the reference's
+ * float64 DenseOperator, operators.py:109-117); COFEM_OZAKI builds its
+ * fixed-point digit planes from the exact float64 values; COFEM_FP32 uses the
+ * float32 rounding.  (A sharded context joins its communicator / group
+ * first: the digit planes of a column shard use row scales shared across
+ * the ranks, so the call is collective there.) */
 int cofem_set_dictionary_f64(cofem_ctx* ctx, const double* phi, int64_t ld);
 
 /* Declare this context's place in a column-sharded dictionary: it holds
@@ -208,6 +216,28 @@ int cofem_run(cofem_ctx* ctx, const double* y, double beta, const cofem_em_confi
               uint64_t device_probe_seed, double* alpha, double* mu, double* s,
               int32_t* cg_steps, double* cg_residuals, int32_t* failed_iteration,
               int32_t* failed_step);
+
+/* The CgReport of the last cofem_run's final E-step and its per-iteration
+ * wall times (cofem.py:97-100 PosteriorEstimate.cg_report, cofem.py:127-133
+ * _iteration_record's wall_time).  Any output may be NULL:
+ *   wall_times  length `iterations` (must equal the run's T), seconds
+ *   solution    D x (K+1) float64, the final block X = [X_probes | x_mean]
+ *   breakdown   K+1 flags of columns frozen by pi_q == 0
+ *   rep         steps / convergence / residual of the final solve */
+int cofem_last_run_report(cofem_ctx* ctx, int32_t iterations, double* wall_times, double* solution,
+                          uint8_t* breakdown, cofem_cg_report* rep);
+
+/* cg.solve_blocked (cg.py:201-234) over DISTINCT systems: block l solves
+ * (beta_l Phi_l^T Phi_l + diag(alpha_l)) X_l = B_l (D x q_l host float64,
+ * row-major) with inverse preconditioner minv_l (length D), all blocks in ONE
+ * lockstep PCG whose Frobenius stopping rule aggregates every block.  One
+ * context per block (same D, precision and device; a dictionary shared by
+ * two blocks needs two contexts).  breakdowns (may be NULL, or hold NULL
+ * entries) receive the per-column freeze flags. */
+int cofem_pcg_solve_multi(cofem_ctx* const* ctxs, int n_blocks, const double* betas, const double* const* alphas,
+                          const double* const* minvs, const double* const* Bs, const int64_t* qs,
+                          const cofem_cg_config* cg, double* const* Xs, cofem_cg_report* rep,
+                          uint8_t* const* breakdowns);
 
 /* ---- the reference's probe stream on the device ---------------------------------
  * probes.draw_rademacher (probes.py:13-17) over numpy's PCG64 generator

@@ -56,6 +56,8 @@ EXPORTED = (
     "cofem_pcg_solve",
     "cofem_run",
     "cofem_run_multitask",
+    "cofem_last_run_report",
+    "cofem_pcg_solve_multi",
     "cofem_set_probe_stream",
     "cofem_set_probe_stream_ex",
     "cofem_pcg64_rademacher",
@@ -164,6 +166,12 @@ def load():
                                         POINTER(c_int8), POINTER(c_double), POINTER(POINTER(c_double)),
                                         POINTER(POINTER(c_double)), POINTER(c_int32), POINTER(c_double),
                                         POINTER(c_int32), POINTER(c_int32)]),
+        "cofem_last_run_report": (c_int, [vp, c_int32, POINTER(c_double), POINTER(c_double), POINTER(c_uint8),
+                                          POINTER(CgReportC)]),
+        "cofem_pcg_solve_multi": (c_int, [POINTER(vp), c_int, POINTER(c_double), POINTER(POINTER(c_double)),
+                                          POINTER(POINTER(c_double)), POINTER(POINTER(c_double)), POINTER(c_int64),
+                                          POINTER(CgConfigC), POINTER(POINTER(c_double)), POINTER(CgReportC),
+                                          POINTER(POINTER(c_uint8))]),
         "cofem_set_probe_stream": (c_int, [vp, POINTER(c_uint64), POINTER(c_uint64)]),
         "cofem_set_probe_stream_ex": (c_int, [vp, POINTER(c_uint64), POINTER(c_uint64), c_uint64, c_uint64]),
         "cofem_pcg64_rademacher": (c_int, [c_int, POINTER(c_uint64), POINTER(c_uint64), c_uint64, c_int64, c_int64,
@@ -361,6 +369,17 @@ class Context:
         check(rc)
         return (alpha, mu, s, steps, resid), None
 
+    def last_run_report(self, iterations, probes):
+        """(wall_times[T], final block X (D x (K+1)), breakdown flags, CgReportC)
+        of the last ``run`` (cofem_last_run_report)."""
+        wall = np.empty(iterations)
+        X = np.empty((self.n_cols, probes + 1))
+        brk = np.zeros(probes + 1, dtype=np.uint8)
+        rep = CgReportC()
+        check(load().cofem_last_run_report(self.handle, int(iterations), _dp(wall), _dp(X),
+                                           brk.ctypes.data_as(POINTER(c_uint8)), ctypes.byref(rep)))
+        return wall, X, brk, rep
+
     def set_probe_stream(self, rng, first_half=0, halves_per_iteration=0):
         """Draw the probes on the device from numpy Generator ``rng``'s PCG64
         stream (bit for bit the reference's draw); None restores host probes."""
@@ -454,6 +473,30 @@ def run_multitask(contexts, ys, betas, iterations, probes, theta_policy, clamp_m
         return None, (fit.value, fst.value)
     check(rc)
     return (alpha, mus, ss, steps, resid), None
+
+
+def pcg_solve_multi(contexts, betas, alphas, minvs, Bs, max_steps, tolerance, printed=False):
+    """cofem_pcg_solve_multi: block l solves (beta_l Phi_l^T Phi_l + diag(alpha_l)) X_l = B_l
+    in one lockstep PCG.  Returns (Xs, CgReportC, breakdown flags per block, diverged)."""
+    L = len(contexts)
+    handles = (c_void_p * L)(*[c.handle for c in contexts])
+    alphas = [np.ascontiguousarray(a, dtype=np.float64) for a in alphas]
+    minvs = [np.ascontiguousarray(m, dtype=np.float64) for m in minvs]
+    Bs = [np.ascontiguousarray(b, dtype=np.float64) for b in Bs]
+    Xs = [np.empty_like(b) for b in Bs]
+    brks = [np.zeros(b.shape[1], dtype=np.uint8) for b in Bs]
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    qs = np.array([b.shape[1] for b in Bs], dtype=np.int64)
+    ptrs = lambda arrs: (POINTER(c_double) * L)(*[_dp(a) for a in arrs])  # noqa: E731
+    bptr = (POINTER(c_uint8) * L)(*[b.ctypes.data_as(POINTER(c_uint8)) for b in brks])
+    rep = CgReportC()
+    cfg = CgConfigC(int(max_steps), 1 if printed else 0, float(tolerance))
+    rc = load().cofem_pcg_solve_multi(handles, L, _dp(betas), ptrs(alphas), ptrs(minvs), ptrs(Bs),
+                                      qs.ctypes.data_as(POINTER(c_int64)), ctypes.byref(cfg), ptrs(Xs),
+                                      ctypes.byref(rep), bptr)
+    if rc not in (COFEM_OK, COFEM_EDIVERGED):
+        check(rc)
+    return Xs, rep, brks, rc == COFEM_EDIVERGED
 
 
 def pcg64_words(rng):

@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <mutex>
@@ -98,6 +99,29 @@ int nccl_load() {
 }
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// A kernel's raised dynamic shared-memory limit is a per-device setting: the
+// flags that avoid re-issuing cudaFuncSetAttribute are kept per device (and
+// atomic: rank threads of an in-process shard group set them concurrently).
+constexpr int MAX_DEVICES = 64;
+struct DeviceFlags {
+  std::atomic<bool> set[MAX_DEVICES] = {};
+};
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= MAX_DEVICES ? 0 : d;
+}
+// raise `fn`'s dynamic shared memory limit to `bytes` once per device
+template <typename F>
+int smem_attr_once(DeviceFlags& flags, F* fn, size_t bytes) {
+  const int dev = current_device();
+  if (flags.set[dev].load(std::memory_order_acquire)) return 0;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(COFEM_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  flags.set[dev].store(true, std::memory_order_release);
+  return 0;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -196,6 +220,7 @@ struct cofem_ctx {
   uint64_t pcg_first = 0, pcg_stride = 0;  // halves before draw 0; halves between iterations (0: D K)
   cudaStream_t stream = nullptr;
   float* phi = nullptr;
+  double* phi64 = nullptr;  // exact float64 dictionary (fp64 mode, cofem_set_dictionary_f64)
   bool have_phi = false;
   int sm_count = 148;
 
@@ -266,6 +291,11 @@ struct cofem_ctx {
   // time-sharded convolution: operand planes carry the neighbours' halo rows
   // (pq: conv_lpad rows before the data for rank > 0; vq: after it for rank < nranks-1)
   int8_t* pq_base = nullptr;
+
+  // the last cofem_run: per-iteration wall times, probes K, final CG report
+  std::vector<double> run_wall;
+  int run_K = 0;
+  cofem_cg_report run_rep{};
 
   // bench state
   bool bench_ready = false;
@@ -366,32 +396,38 @@ SplitPlan plan_splits(int64_t nblocks_other, int64_t ntiles, int tile, int slots
   return best;
 }
 
-template <typename T, int QP>
+// CUDA-core contractions over a float32 (PhiT = float) or exact float64
+// (PhiT = double, fp64 mode) dictionary
+template <typename T, int QP, typename PhiT = float>
 struct Kern {
   using TL = Tiles<T>;
-  using FC = FwdCfg<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST>;
-  using BC = BwdCfg<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST>;
-  static constexpr auto fwd = fwd_kernel<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST>;
-  static constexpr auto bwd = bwd_kernel<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST>;
-  static bool inited;
-  static int fwd_occ, bwd_occ;
+  using FC = FwdCfg<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST, PhiT>;
+  using BC = BwdCfg<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST, PhiT>;
+  static constexpr auto fwd = fwd_kernel<T, QP, TL::FR, TL::FWM, TL::FWK, TL::FBK, TL::FST, PhiT>;
+  static constexpr auto bwd = bwd_kernel<T, QP, TL::BC, TL::BWN, TL::BWK, TL::BBK, TL::BST, PhiT>;
+  static DeviceFlags flags;
+  static std::atomic<int> fwd_occ, bwd_occ;  // same on every B200
   static int init() {
-    if (inited) return 0;
+    const int dev = current_device();
+    if (flags.set[dev].load(std::memory_order_acquire)) return 0;
     CK(cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM));
     CK(cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BC::SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fwd_occ, fwd, FC::NT, FC::SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bwd_occ, bwd, BC::NT, BC::SMEM));
-    if (fwd_occ < 1 || bwd_occ < 1) return fail(COFEM_ECUDA, "contraction kernel cannot be resident");
-    inited = true;
+    int fo = 0, bo = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fo, fwd, FC::NT, FC::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bo, bwd, BC::NT, BC::SMEM));
+    if (fo < 1 || bo < 1) return fail(COFEM_ECUDA, "contraction kernel cannot be resident");
+    fwd_occ = fo;
+    bwd_occ = bo;
+    flags.set[dev].store(true, std::memory_order_release);
     return 0;
   }
 };
-template <typename T, int QP>
-bool Kern<T, QP>::inited = false;
-template <typename T, int QP>
-int Kern<T, QP>::fwd_occ = 0;
-template <typename T, int QP>
-int Kern<T, QP>::bwd_occ = 0;
+template <typename T, int QP, typename PhiT>
+DeviceFlags Kern<T, QP, PhiT>::flags;
+template <typename T, int QP, typename PhiT>
+std::atomic<int> Kern<T, QP, PhiT>::fwd_occ{0};
+template <typename T, int QP, typename PhiT>
+std::atomic<int> Kern<T, QP, PhiT>::bwd_occ{0};
 
 int ensure_ws(cofem_ctx* c, int ldq) {
   if (c->ldq == ldq) return 0;
@@ -640,15 +676,10 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
 
 template <int QW>
 int oz_init_kernels() {
-  static bool done = false;
-  if (done) return 0;
-  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)oz::Cfg<QW>::SMEM));
-  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)oz::Cfg<QW>::SMEM));
-  CK(cudaFuncSetAttribute(oz::contract_kernel<QW, oz::MODE_BAND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)oz::Cfg<QW>::SMEM));
-  done = true;
+  static DeviceFlags f_fwd, f_bwd, f_band;
+  CKR(smem_attr_once(f_fwd, oz::contract_kernel<QW, oz::MODE_FWD>, oz::Cfg<QW>::SMEM));
+  CKR(smem_attr_once(f_bwd, oz::contract_kernel<QW, oz::MODE_BWD>, oz::Cfg<QW>::SMEM));
+  CKR(smem_attr_once(f_band, oz::contract_kernel<QW, oz::MODE_BAND>, oz::Cfg<QW>::SMEM));
   return 0;
 }
 
@@ -772,22 +803,21 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
 // launch the band contraction: smem-resident band when it fits, else the
 // streaming MODE_BAND of contract_kernel
 template <int QW>
-void launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
-                 double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
+int launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
+                double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
   const int grid = std::min(nmb, c->sm_count);
   const size_t sm = oz::BandCfg<QW>::smem(nk);
   if (sm <= 227 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(oz::band_kernel<QW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
-    }
+    static DeviceFlags flags;
+    CKR(smem_attr_once(flags, oz::band_kernel<QW>, 227 * 1024));
     oz::band_kernel<QW><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(map_a, map_b, nmb, nk, offset, c->hrows, c->opscale,
                                                                 out, rows_real, colmax, st);
   } else {
     oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
         map_a, map_b, nmb, nmb, nk, 0, offset, c->hrows, c->opscale, out, out_rows, rows_real, colmax, st);
   }
+  CK(cudaGetLastError());
+  return 0;
 }
 
 // V -> operand planes for Phi^T (global column maxima), then the halo: the
@@ -829,8 +859,8 @@ int conv_fwd(cofem_ctx* c, const double* src, int lds, int qoff, double* vout, c
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  launch_band<QW>(c, c->map_band_fwd, c->map_p[slot], nmb, oz::BM + c->conv_lpad, left ? 0 : -c->conv_lpad, vout,
-                  c->Np, c->N, c->vcolmax, st);
+  CKR(launch_band<QW>(c, c->map_band_fwd, c->map_p[slot], nmb, oz::BM + c->conv_lpad, left ? 0 : -c->conv_lpad,
+                      vout, c->Np, c->N, c->vcolmax, st));
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -852,8 +882,8 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  launch_band<QW>(c, c->map_band_adj, c->map_v[QW / 8], nmb, oz::BM + c->conv_lpad, 0, (double*)c->ppart, c->Dp,
-                  c->D, nullptr, st);
+  CKR(launch_band<QW>(c, c->map_band_adj, c->map_v[QW / 8], nmb, oz::BM + c->conv_lpad, 0, (double*)c->ppart,
+                      c->Dp, c->D, nullptr, st));
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -879,11 +909,8 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   CKR(conv_quantize_v<QW>(c, v, st));
   const int nmb = (int)(c->Dp / oz::BM);
   const int grid = std::min(nmb, std::min(c->sm_count, c->nblk_elem));
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(oz::band_kernel<QW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 64));
-    attr = true;
-  }
+  static DeviceFlags flags;
+  CKR(smem_attr_once(flags, oz::band_kernel<QW, true>, 227 * 1024 - 64));
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
@@ -909,11 +936,8 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
 int conv_fft_pass(cofem_ctx* c, const double* src, double* dst, bool adj, const Status* stt) {
   constexpr int N1 = 32, N2 = 32, FPI = DCT_FPI, NT = FPI * N2;
   constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(dctf::k_conv_fft_pass<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static DeviceFlags flags;
+  CKR(smem_attr_once(flags, dctf::k_conv_fft_pass<N1, N2>, smem));
   const int L = c->conv_L, valid = CONV_FFT_N - (L - 1);
   const int nblocks = (int)((c->D + valid - 1) / valid);
   const int items = nblocks * (c->ldq / (2 * FPI));
@@ -957,16 +981,12 @@ int conv_fft_system_apply(cofem_ctx* c, double beta, const Status* stt) {
 // pass over an n x n x ldq block; row passes run along j (outer i), column
 // passes along i (outer j / l)
 template <int N1, int N2, int MODE>
-void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
   const int64_t n = c->dct_n, ldq = c->ldq;
   constexpr int FPI = DCT_FPI, NT = FPI * N2;
   constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dctf::k_dct_pass<N1, N2, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
+  static DeviceFlags flags;
+  CKR(smem_attr_once(flags, dctf::k_dct_pass<N1, N2, MODE>, smem));
   const int items = (int)(n * (ldq / (2 * FPI)));
   int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));  // blocks that fit one SM's shared memory
   if (per_sm > 16) per_sm = 16;
@@ -975,16 +995,17 @@ void dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const S
       src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / (2 * FPI)), c->dct_wN, c->dct_tw,
       c->dct_gridT, stt);
   c->launches++;
+  return 0;
 }
 
 template <int MODE>
 int dct_pass(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
   switch (c->dct_n) {
-    case 64: dct_pass_t<8, 8, MODE>(c, src, dst, rows, stt); break;
-    case 128: dct_pass_t<8, 16, MODE>(c, src, dst, rows, stt); break;
-    case 256: dct_pass_t<16, 16, MODE>(c, src, dst, rows, stt); break;
-    case 512: dct_pass_t<16, 32, MODE>(c, src, dst, rows, stt); break;
-    case 1024: dct_pass_t<32, 32, MODE>(c, src, dst, rows, stt); break;
+    case 64: CKR((dct_pass_t<8, 8, MODE>(c, src, dst, rows, stt))); break;
+    case 128: CKR((dct_pass_t<8, 16, MODE>(c, src, dst, rows, stt))); break;
+    case 256: CKR((dct_pass_t<16, 16, MODE>(c, src, dst, rows, stt))); break;
+    case 512: CKR((dct_pass_t<16, 32, MODE>(c, src, dst, rows, stt))); break;
+    case 1024: CKR((dct_pass_t<32, 32, MODE>(c, src, dst, rows, stt))); break;
     default: return fail(COFEM_EINVAL, "unsupported DCT image side");
   }
   CK(cudaGetLastError());
@@ -1035,13 +1056,27 @@ int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
 
 // ---- the two contractions ----------------------------------------------
 // fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
+template <typename T, int QP, typename PhiT>
+int run_fwd_cc(cofem_ctx* c, const PhiT* phi, const T* src, int lds, int qoff, T* vout, const Status* st);
+template <typename T, int QP, typename PhiT>
+int run_bwd_cc(cofem_ctx* c, const PhiT* phi, const T* v, int* nsplit_out, const Status* st);
+
 template <typename T, int QP>
 int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status* st) {
   if constexpr (std::is_same<T, double>::value) {
     if (c->kind == 1) return conv_fwd<QP>(c, src, lds, qoff, vout, st);
     if (c->prec == COFEM_OZAKI) return oz_fwd<QP>(c, src, lds, qoff, vout, st);
   }
-  using K = Kern<T, QP>;
+  if constexpr (std::is_same<T, double>::value) {
+    if (c->phi64) return run_fwd_cc<T, QP, double>(c, c->phi64, src, lds, qoff, vout, st);
+  }
+  return run_fwd_cc<T, QP, float>(c, c->phi, src, lds, qoff, vout, st);
+}
+
+// the CUDA-core contraction over a float32 or float64 dictionary
+template <typename T, int QP, typename PhiT>
+int run_fwd_cc(cofem_ctx* c, const PhiT* phi, const T* src, int lds, int qoff, T* vout, const Status* st) {
+  using K = Kern<T, QP, PhiT>;
   CKR(K::init());
   const int64_t ntiles = c->Dp / Tiles<T>::FBK;
   const int64_t mblocks = c->Np / K::FC::BM;
@@ -1056,7 +1091,7 @@ int run_fwd(cofem_ctx* c, const T* src, int lds, int qoff, T* vout, const Status
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  K::fwd<<<grid, K::FC::NT, K::FC::SMEM, c->stream>>>(c->phi, c->Dp, src, lds, qoff, sp.per_split, c->Dp,
+  K::fwd<<<grid, K::FC::NT, K::FC::SMEM, c->stream>>>(phi, c->Dp, src, lds, qoff, sp.per_split, c->Dp,
                                                       (T*)c->vpart, c->Np, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
@@ -1081,7 +1116,15 @@ int run_bwd(cofem_ctx* c, const T* v, int* nsplit_out, const Status* st) {
     if (c->kind == 1) return conv_bwd<QP>(c, v, nsplit_out, st);
     if (c->prec == COFEM_OZAKI) return oz_bwd<QP>(c, v, nsplit_out, st);
   }
-  using K = Kern<T, QP>;
+  if constexpr (std::is_same<T, double>::value) {
+    if (c->phi64) return run_bwd_cc<T, QP, double>(c, c->phi64, v, nsplit_out, st);
+  }
+  return run_bwd_cc<T, QP, float>(c, c->phi, v, nsplit_out, st);
+}
+
+template <typename T, int QP, typename PhiT>
+int run_bwd_cc(cofem_ctx* c, const PhiT* phi, const T* v, int* nsplit_out, const Status* st) {
+  using K = Kern<T, QP, PhiT>;
   CKR(K::init());
   const int64_t ntiles = c->Np / Tiles<T>::BBK;
   const int64_t nblocks = c->Dp / K::BC::BN;
@@ -1096,7 +1139,7 @@ int run_bwd(cofem_ctx* c, const T* v, int* nsplit_out, const Status* st) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  K::bwd<<<grid, K::BC::NT, K::BC::SMEM, c->stream>>>(c->phi, c->Dp, v, QP, 0, sp.per_split, c->Np,
+  K::bwd<<<grid, K::BC::NT, K::BC::SMEM, c->stream>>>(phi, c->Dp, v, QP, 0, sp.per_split, c->Np,
                                                       (T*)c->ppart, c->Dp, st);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
@@ -1404,6 +1447,16 @@ int check_ctx(cofem_ctx* c, bool need_phi = true) {
 
 int ldq_for(int64_t q) { return (int)round_up(std::max<int64_t>(q, 1), 8); }
 
+// column squared norms of a dense dictionary (the exact float64 copy when held)
+int dense_colsq(cofem_ctx* c) {
+  const int g = (int)((c->D + 255) / 256);
+  if (c->phi64) k_colsq<double><<<g, 256, 0, c->stream>>>(c->phi64, c->Dp, c->N, c->D, c->colsq);
+  else k_colsq<float><<<g, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
 // ---- apply / adjoint / system apply ---------------------------------------
 // DCT: tmpD (D x ldq) <- Phi^T V for V (N x ldq) already in c->V
 int dct_adjoint_from_V(cofem_ctx* c) {
@@ -1561,9 +1614,7 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   if (em->theta_policy == COFEM_THETA_JACOBI) {
     if (c->kind == 2) return fail(COFEM_EINVAL, "jacobi on a DCT dictionary: pass its column norms as custom theta");
     if (c->kind == 0) {
-      k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
-      c->launches++;
-      CK(cudaGetLastError());
+      CKR(dense_colsq(c));
     }
     CK(cudaMemcpyAsync(c->theta, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   } else if (em->theta_policy == COFEM_THETA_CUSTOM) {
@@ -1622,7 +1673,10 @@ int run_impl(cofem_ctx* c, const double* y, double beta, const cofem_em_config* 
              int32_t* steps, double* resid, int32_t* fail_it, int32_t* fail_step) {
   CKR(em_prepare<T>(c, y, beta, em, theta));
   std::vector<double> alpha_used(c->D, 1.0);
+  c->run_wall.assign(em->iterations, 0.0);
+  c->run_K = 0;
   for (int t = 1; t <= em->iterations; ++t) {
+    const auto w0 = std::chrono::steady_clock::now();
     cofem_cg_report rep;
     // alpha of this E-step is what the caller gets back after the last one
     if (t == em->iterations && alpha) {
@@ -1639,8 +1693,12 @@ int run_impl(cofem_ctx* c, const double* y, double beta, const cofem_em_config* 
                                        " (EM iteration " + std::to_string(t) + ")");
     }
     if (rc != 0) return rc;
+    c->run_rep = rep;
+    if (t == em->iterations) CK(cudaStreamSynchronize(c->stream));  // the last M-step-free finish
+    c->run_wall[t - 1] = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
   }
   CK(cudaStreamSynchronize(c->stream));
+  c->run_K = em->probes;
   if (alpha) std::copy(alpha_used.begin(), alpha_used.end(), alpha);
   if (mu) CK(cudaMemcpy(mu, c->mu, c->D * sizeof(double), cudaMemcpyDeviceToHost));
   if (s) CK(cudaMemcpy(s, c->s, c->D * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1746,6 +1804,66 @@ int run_multi_impl(cofem_ctx** cs, int L, const double* const* ys, const double*
     }
   }
   cleanup();
+  return rc;
+}
+
+// cg.solve_blocked with distinct systems (cg.py:201-234): block l is
+// A_l X_l = B_l, A_l = beta_l Phi_l^T Phi_l + diag(alpha_l), with its own
+// preconditioner; one lockstep PCG (pcg_multi) whose stopping rule aggregates
+// the residual over all blocks.  Narrower blocks are zero-padded to the widest
+// (a zero column freezes at its first step and never touches the aggregate).
+template <typename T>
+int pcg_solve_multi_impl(cofem_ctx** cs, int L, const double* betas, const double* const* alphas,
+                         const double* const* minvs, const double* const* Bs, const int64_t* qs,
+                         const cofem_cg_config* cg, double* const* Xs, cofem_cg_report* rep,
+                         uint8_t* const* breakdowns) {
+  cofem_ctx* c0 = cs[0];
+  int64_t qmax = 1;
+  for (int l = 0; l < L; ++l) qmax = std::max(qmax, qs[l]);
+  const int ldq = ldq_for(qmax);
+  if (ldq > 1024) return fail(COFEM_EINVAL, "at most 1024 right-hand sides per block");
+  std::vector<cudaStream_t> saved(L);
+  for (int l = 0; l < L; ++l) {
+    cofem_ctx* c = cs[l];
+    saved[l] = c->stream;
+    CKR(ensure_ws(c, ldq));
+    std::vector<double> a(c->Dp, 1.0), m(c->Dp, 0.0);
+    std::copy(alphas[l], alphas[l] + c->D, a.begin());
+    std::copy(minvs[l], minvs[l] + c->D, m.begin());
+    CK(h2d_sync(c, c->alpha, a.data(), c->Dp * sizeof(double)));
+    CK(h2d_sync(c, c->minv, m.data(), c->Dp * sizeof(double)));
+    std::vector<double> b((size_t)c->D * qmax, 0.0);
+    for (int64_t j = 0; j < c->D; ++j)
+      for (int64_t k = 0; k < qs[l]; ++k) b[j * qmax + k] = Bs[l][j * qs[l] + k];
+    CKR(upload_block<T>(c, b.data(), c->D, qmax, c->Dp, ldq, c->R));
+  }
+  CK(cudaDeviceSynchronize());
+  for (int l = 0; l < L; ++l) cs[l]->stream = c0->stream;  // one stream for the lockstep
+  double* agg = nullptr;
+  double** dptrs = nullptr;
+  int rc = 0;
+  if (cudaMalloc(&agg, 2 * sizeof(double)) != cudaSuccess || cudaMalloc(&dptrs, 2 * L * sizeof(double*)) != cudaSuccess)
+    rc = fail(COFEM_ENOMEM, "blocked solve tables");
+  if (!rc) rc = pcg_multi<T>(cs, L, betas, (int)qmax, cg, rep, agg, dptrs);
+  for (int l = 0; l < L; ++l) cs[l]->stream = saved[l];
+  if (agg) cudaFree(agg);
+  if (dptrs) cudaFree(dptrs);
+  if (rc != 0 && rc != COFEM_EDIVERGED) return rc;
+  int nb = 0;
+  for (int l = 0; l < L; ++l) {
+    cofem_ctx* c = cs[l];
+    std::vector<double> x((size_t)c->D * qmax);
+    CKR(download_block<T>(c, c->X, c->D, qmax, ldq, 0, x.data()));
+    for (int64_t j = 0; j < c->D; ++j)
+      for (int64_t k = 0; k < qs[l]; ++k) Xs[l][j * qs[l] + k] = x[j * qmax + k];
+    std::vector<int> fz(ldq);
+    CK(cudaMemcpy(fz.data(), c->frozen, ldq * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < qs[l]; ++k) {
+      if (breakdowns && breakdowns[l]) breakdowns[l][k] = fz[k] ? 1 : 0;
+      nb += fz[k] ? 1 : 0;
+    }
+  }
+  rep->n_breakdown = nb;
   return rc;
 }
 
@@ -2063,7 +2181,7 @@ int cofem_destroy(cofem_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_ws(c);
-  void* ptrs[] = {c->phi, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
+  void* ptrs[] = {c->phi, c->phi64, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
@@ -2159,6 +2277,10 @@ int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_devi
   else
     CKR(upload_rows(c, c->phi, c->Dp * sizeof(float), phi, ld * sizeof(float), c->D * sizeof(float), c->N));
   CK(cudaStreamSynchronize(c->stream));
+  if (c->phi64) {  // a float32 dictionary replaces an earlier float64 one
+    cudaFree(c->phi64);
+    c->phi64 = nullptr;
+  }
   c->have_phi = true;
   c->oz_ready = false;
   return 0;
@@ -2182,13 +2304,17 @@ int cofem_set_dictionary_f64(cofem_ctx* c, const double* phi, int64_t ld) {
   int rc = 0;
   rc = upload_rows(c, tmp, c->Dp * sizeof(double), phi, ld * sizeof(double), c->D * sizeof(double), c->N);
   if (!rc) {
+    // the float32 copy serves cofem_get_dictionary (and the fp32 mode)
     k_round_f32<<<16 * c->sm_count, 256, 0, c->stream>>>(tmp, c->phi, (int64_t)c->Np * c->Dp);
     c->launches++;
     c->oz_ready = false;
     if (c->prec == COFEM_OZAKI) rc = ensure_oz(c, tmp);  // planes from the exact float64 values
   }
   cudaStreamSynchronize(c->stream);
-  cudaFree(tmp);
+  if (c->phi64) cudaFree(c->phi64);
+  c->phi64 = nullptr;
+  if (!rc && c->prec == COFEM_FP64) c->phi64 = tmp;  // fp64 mode multiplies the exact float64 entries
+  else cudaFree(tmp);
   if (!rc) c->have_phi = true;
   return rc;
 }
@@ -2299,6 +2425,10 @@ int cofem_generate_gaussian_dictionary(cofem_ctx* c, uint64_t seed, double scale
   const int64_t total = c->N * ((c->D + 3) / 4);
   const int gs = (int)std::min<int64_t>((total + 255) / 256, 64 * c->sm_count);
   k_gen_gaussian<<<gs, 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->col_offset, seed, scale);
+  if (c->phi64) {
+    cudaFree(c->phi64);
+    c->phi64 = nullptr;
+  }
   c->launches++;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));
@@ -2374,9 +2504,7 @@ int cofem_column_sq_norms(cofem_ctx* c, double* out) {
     return 0;
   }
   if (c->kind == 2) return fail(COFEM_EINVAL, "DCT column norms are computed by the host (pass a custom theta)");
-  k_colsq<<<(int)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->D, c->colsq);
-  c->launches++;
-  CK(cudaGetLastError());
+  CKR(dense_colsq(c));
   CK(cudaMemcpyAsync(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return 0;
@@ -2479,6 +2607,50 @@ int cofem_run_multitask(cofem_ctx* const* ctxs, int n_tasks, const double* const
   std::vector<cofem_ctx*> cs(ctxs, ctxs + n_tasks);
   return DISPATCH(c0, run_multi_impl, cs.data(), n_tasks, ys, betas, em, cg, theta, probes, alpha, mus, ss,
                   cg_steps, cg_residuals, failed_iteration, failed_step);
+}
+
+int cofem_last_run_report(cofem_ctx* c, int32_t iterations, double* wall_times, double* solution,
+                          uint8_t* breakdown, cofem_cg_report* rep) {
+  CKR(check_ctx(c));
+  if (c->run_K < 1) return fail(COFEM_ESTATE, "no completed cofem_run on this context");
+  if (wall_times) {
+    if (iterations != (int32_t)c->run_wall.size()) return fail(COFEM_EINVAL, "iterations != the last run's T");
+    std::copy(c->run_wall.begin(), c->run_wall.end(), wall_times);
+  }
+  const int q = c->run_K + 1;
+  if (solution) CKR(DISPATCH(c, download_block, c, c->X, c->D, q, c->ldq, 0, solution));
+  if (breakdown) {
+    std::vector<int> fz(c->ldq);
+    CK(cudaMemcpy(fz.data(), c->frozen, c->ldq * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < q; ++k) breakdown[k] = fz[k] ? 1 : 0;
+  }
+  if (rep) *rep = c->run_rep;
+  return 0;
+}
+
+int cofem_pcg_solve_multi(cofem_ctx* const* ctxs, int n_blocks, const double* betas, const double* const* alphas,
+                          const double* const* minvs, const double* const* Bs, const int64_t* qs,
+                          const cofem_cg_config* cg, double* const* Xs, cofem_cg_report* rep,
+                          uint8_t* const* breakdowns) {
+  if (!ctxs || n_blocks < 1 || !betas || !alphas || !minvs || !Bs || !qs || !cg || !Xs || !rep)
+    return fail(COFEM_EINVAL, "null argument");
+  if (cg->max_steps < 1 || !(cg->tolerance > 0)) return fail(COFEM_EINVAL, "bad CG config");
+  cofem_ctx* c0 = ctxs[0];
+  CKR(check_ctx(c0));
+  for (int l = 0; l < n_blocks; ++l) {
+    cofem_ctx* c = ctxs[l];
+    CKR(check_ctx(c));
+    if (!alphas[l] || !minvs[l] || !Bs[l] || !Xs[l] || qs[l] < 1) return fail(COFEM_EINVAL, "null block argument");
+    if (!(betas[l] > 0) || !std::isfinite(betas[l])) return fail(COFEM_EINVAL, "beta must be positive and finite");
+    if (c->D != c0->D || c->prec != c0->prec || c->device != c0->device || c->nranks > 1)
+      return fail(COFEM_EINVAL, "blocks must share D, precision and device (single GPU)");
+    for (int m = 0; m < l; ++m)
+      if (ctxs[m] == c) return fail(COFEM_EINVAL, "each block needs its own context");
+  }
+  std::vector<cofem_ctx*> cs(ctxs, ctxs + n_blocks);
+  CKR(set_dev(c0));
+  return DISPATCH(c0, pcg_solve_multi_impl, cs.data(), n_blocks, betas, alphas, minvs, Bs, qs, cg, Xs, rep,
+                  breakdowns);
 }
 
 int cofem_set_probe_stream_ex(cofem_ctx* c, const uint64_t* state, const uint64_t* inc, uint64_t first_half,

@@ -1,7 +1,9 @@
 // kernels.cuh -- sm_100a kernels of the CoFEM hot path (CUDA-core path).
 //
 // Layouts (HBM):
-//   Phi   : Np x Dp float32 row-major, zero padded (Np % 128 == 0, Dp % 128 == 0)
+//   Phi   : Np x Dp row-major, zero padded (Np % 128 == 0, Dp % 128 == 0);
+//           float32 (PhiT = float), or float64 (PhiT = double) when a float64
+//           dictionary is set in the fp64 mode (exact entries, no rounding)
 //   blocks: Dp x ldq of T (float or double) row-major -- coordinate j's Q
 //           right-hand-side entries contiguous (the reference's (D, Q) C order)
 //   V     : Np x ldq of T (Phi P)
@@ -39,6 +41,34 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// four consecutive dictionary entries from shared memory (16 B or 2 x 16 B)
+__device__ __forceinline__ void load4(const float* p, float f[4]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+__device__ __forceinline__ void load4(const double* p, double f[4]) {
+  const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+template <int CC>
+__device__ __forceinline__ void loadc(const float* p, float f[CC]) {
+  if constexpr (CC == 4) {
+    load4(p, f);
+  } else {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    f[0] = v.x; f[1] = v.y;
+  }
+}
+template <int CC>
+__device__ __forceinline__ void loadc(const double* p, double f[CC]) {
+  if constexpr (CC == 4) {
+    load4(p, f);
+  } else {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    f[0] = v.x; f[1] = v.y;
+  }
+}
+
 template <typename T>
 struct Vec4;  // 16-byte vector of T
 template <>
@@ -56,25 +86,25 @@ struct Vec4<double> {
 // Thread (warp w = wk*WM + wm, lane l) owns rows m0 + wm*32R + r*32 + l
 // (r < R) and the column sub-slice wk of every BK-wide tile; the WK partial
 // sums are folded through smem at the end.
-template <typename T, int QP, int R, int WM, int WK, int BK, int STAGES>
+template <typename T, int QP, int R, int WM, int WK, int BK, int STAGES, typename PhiT = float>
 struct FwdCfg {
   static constexpr int BM = 32 * R * WM;
   static constexpr int NT = 32 * WM * WK;
-  static constexpr int SROW = BK + 4;  // +16 B: LDS.128 row reads are conflict-free
-  static constexpr int PHI_STAGE = BM * SROW;                // floats
+  static constexpr int SROW = BK + 16 / (int)sizeof(PhiT);  // +16 B: 16-B row reads are conflict-free
+  static constexpr int PHI_STAGE = BM * SROW;                // PhiT entries
   static constexpr int P_STAGE = BK * QP;                    // T
-  static constexpr size_t STAGE_BYTES = PHI_STAGE * 4 + P_STAGE * sizeof(T);
+  static constexpr size_t STAGE_BYTES = PHI_STAGE * sizeof(PhiT) + P_STAGE * sizeof(T);
   static constexpr size_t RED_BYTES = (size_t)(WK - 1) * BM * QP * sizeof(T);
   static constexpr size_t SMEM = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
   static_assert(BK % (4 * WK) == 0, "each k group needs whole float4 columns");
   static_assert((QP * sizeof(T)) % 16 == 0, "QP row must be a multiple of 16 B");
 };
 
-template <typename T, int QP, int R, int WM, int WK, int BK, int STAGES>
+template <typename T, int QP, int R, int WM, int WK, int BK, int STAGES, typename PhiT = float>
 __global__ void __launch_bounds__(32 * WM * WK)
-    fwd_kernel(const float* __restrict__ phi, int64_t ldphi, const T* __restrict__ P, int ldq, int qoff,
+    fwd_kernel(const PhiT* __restrict__ phi, int64_t ldphi, const T* __restrict__ P, int ldq, int qoff,
                int k_per_split, int64_t kmax, T* __restrict__ vpart, int64_t np, const Status* __restrict__ st) {
-  using C = FwdCfg<T, QP, R, WM, WK, BK, STAGES>;
+  using C = FwdCfg<T, QP, R, WM, WK, BK, STAGES, PhiT>;
   if (st && st->done) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -85,16 +115,19 @@ __global__ void __launch_bounds__(32 * WM * WK)
   if (k1 > kmax) k1 = kmax;
   const int ntiles = (int)((k1 - k0) / BK);
 
-  auto stage_phi = [&](int s) { return reinterpret_cast<float*>(smem + s * C::STAGE_BYTES); };
-  auto stage_p = [&](int s) { return reinterpret_cast<T*>(smem + s * C::STAGE_BYTES + C::PHI_STAGE * 4); };
+  constexpr int EPC = 16 / (int)sizeof(PhiT);  // dictionary entries per 16-B chunk
+  auto stage_phi = [&](int s) { return reinterpret_cast<PhiT*>(smem + s * C::STAGE_BYTES); };
+  auto stage_p = [&](int s) {
+    return reinterpret_cast<T*>(smem + s * C::STAGE_BYTES + C::PHI_STAGE * sizeof(PhiT));
+  };
 
   auto load_tile = [&](int s, int t) {
     const int64_t kt = k0 + (int64_t)t * BK;
-    float* sphi = stage_phi(s);
-    constexpr int CPR = BK / 4;  // 16-B chunks per tile row
+    PhiT* sphi = stage_phi(s);
+    constexpr int CPR = BK / EPC;  // 16-B chunks per tile row
     for (int c = tid; c < C::BM * CPR; c += C::NT) {
       const int row = c / CPR, ch = c % CPR;
-      cp_async16(sphi + row * C::SROW + ch * 4, phi + (m0 + row) * ldphi + kt + ch * 4);
+      cp_async16(sphi + row * C::SROW + ch * EPC, phi + (m0 + row) * ldphi + kt + ch * EPC);
     }
     T* sp = stage_p(s);
     constexpr int PCH = QP * sizeof(T) / 16;  // chunks per P row
@@ -125,14 +158,13 @@ __global__ void __launch_bounds__(32 * WM * WK)
       if (tn < ntiles) load_tile(tn % STAGES, tn);
       cp_async_commit();
     }
-    const float* sphi = stage_phi(t % STAGES);
+    const PhiT* sphi = stage_phi(t % STAGES);
     const T* sp = stage_p(t % STAGES);
 #pragma unroll
     for (int jj = wk * KW; jj < (wk + 1) * KW; jj += 4) {
-      float4 f[R];
+      PhiT f[R][4];
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        f[r] = *reinterpret_cast<const float4*>(sphi + (wm * 32 * R + r * 32 + lane) * C::SROW + jj);
+      for (int r = 0; r < R; ++r) load4(sphi + (wm * 32 * R + r * 32 + lane) * C::SROW + jj, f[r]);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const T* prow = sp + (jj + kk) * QP;
@@ -140,10 +172,7 @@ __global__ void __launch_bounds__(32 * WM * WK)
         for (int q = 0; q < QP; ++q) {
           const T pv = prow[q];
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float fv = kk == 0 ? f[r].x : kk == 1 ? f[r].y : kk == 2 ? f[r].z : f[r].w;
-            acc[r][q] = fma(T(fv), pv, acc[r][q]);
-          }
+          for (int r = 0; r < R; ++r) acc[r][q] = fma(T(f[r][kk]), pv, acc[r][q]);
         }
       }
     }
@@ -194,24 +223,24 @@ __global__ void __launch_bounds__(32 * WM * WK)
 //
 // Warp w = wk*WN + wn, lane l owns columns n0 + wn*32C + l*C + c (c < C) and
 // the tile rows i with i % WK == wk.
-template <typename T, int QP, int CC, int WN, int WK, int BK, int STAGES>
+template <typename T, int QP, int CC, int WN, int WK, int BK, int STAGES, typename PhiT = float>
 struct BwdCfg {
   static constexpr int BN = 32 * CC * WN;
   static constexpr int NT = 32 * WN * WK;
-  static constexpr int PHI_STAGE = BK * BN;  // floats
+  static constexpr int PHI_STAGE = BK * BN;  // PhiT entries
   static constexpr int V_STAGE = BK * QP;    // T
-  static constexpr size_t STAGE_BYTES = PHI_STAGE * 4 + V_STAGE * sizeof(T);
+  static constexpr size_t STAGE_BYTES = PHI_STAGE * sizeof(PhiT) + V_STAGE * sizeof(T);
   static constexpr size_t RED_BYTES = (size_t)(WK - 1) * BN * QP * sizeof(T);
   static constexpr size_t SMEM = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
   static_assert(CC == 4 || CC == 2, "columns per thread");
   static_assert(BK % WK == 0, "row interleave");
 };
 
-template <typename T, int QP, int CC, int WN, int WK, int BK, int STAGES>
+template <typename T, int QP, int CC, int WN, int WK, int BK, int STAGES, typename PhiT = float>
 __global__ void __launch_bounds__(32 * WN * WK)
-    bwd_kernel(const float* __restrict__ phi, int64_t ldphi, const T* __restrict__ V, int ldv, int qoff,
+    bwd_kernel(const PhiT* __restrict__ phi, int64_t ldphi, const T* __restrict__ V, int ldv, int qoff,
                int n_per_split, int64_t nmax, T* __restrict__ ppart, int64_t dp, const Status* __restrict__ st) {
-  using C = BwdCfg<T, QP, CC, WN, WK, BK, STAGES>;
+  using C = BwdCfg<T, QP, CC, WN, WK, BK, STAGES, PhiT>;
   if (st && st->done) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -222,16 +251,19 @@ __global__ void __launch_bounds__(32 * WN * WK)
   if (r1 > nmax) r1 = nmax;
   const int ntiles = (int)((r1 - r0) / BK);
 
-  auto stage_phi = [&](int s) { return reinterpret_cast<float*>(smem + s * C::STAGE_BYTES); };
-  auto stage_v = [&](int s) { return reinterpret_cast<T*>(smem + s * C::STAGE_BYTES + C::PHI_STAGE * 4); };
+  constexpr int EPC = 16 / (int)sizeof(PhiT);  // dictionary entries per 16-B chunk
+  auto stage_phi = [&](int s) { return reinterpret_cast<PhiT*>(smem + s * C::STAGE_BYTES); };
+  auto stage_v = [&](int s) {
+    return reinterpret_cast<T*>(smem + s * C::STAGE_BYTES + C::PHI_STAGE * sizeof(PhiT));
+  };
 
   auto load_tile = [&](int s, int t) {
     const int64_t rt = r0 + (int64_t)t * BK;
-    float* sphi = stage_phi(s);
-    constexpr int CPR = C::BN / 4;
+    PhiT* sphi = stage_phi(s);
+    constexpr int CPR = C::BN / EPC;
     for (int c = tid; c < BK * CPR; c += C::NT) {
       const int row = c / CPR, ch = c % CPR;
-      cp_async16(sphi + row * C::BN + ch * 4, phi + (rt + row) * ldphi + c0 + ch * 4);
+      cp_async16(sphi + row * C::BN + ch * EPC, phi + (rt + row) * ldphi + c0 + ch * EPC);
     }
     T* sv = stage_v(s);
     constexpr int VCH = QP * sizeof(T) / 16;
@@ -261,18 +293,12 @@ __global__ void __launch_bounds__(32 * WN * WK)
       if (tn < ntiles) load_tile(tn % STAGES, tn);
       cp_async_commit();
     }
-    const float* sphi = stage_phi(t % STAGES);
+    const PhiT* sphi = stage_phi(t % STAGES);
     const T* sv = stage_v(t % STAGES);
 #pragma unroll 4
     for (int i = wk; i < BK; i += WK) {
-      float f[CC];
-      if constexpr (CC == 4) {
-        const float4 v4 = *reinterpret_cast<const float4*>(sphi + i * C::BN + wn * 32 * CC + lane * CC);
-        f[0] = v4.x; f[1] = v4.y; f[2] = v4.z; f[3] = v4.w;
-      } else {
-        const float2 v2 = *reinterpret_cast<const float2*>(sphi + i * C::BN + wn * 32 * CC + lane * CC);
-        f[0] = v2.x; f[1] = v2.y;
-      }
+      PhiT f[CC];
+      loadc<CC>(sphi + i * C::BN + wn * 32 * CC + lane * CC, f);
       const T* vrow = sv + i * QP;
 #pragma unroll
       for (int q = 0; q < QP; ++q) {

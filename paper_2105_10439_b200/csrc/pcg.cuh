@@ -646,7 +646,8 @@ __global__ void k_gen_gaussian(float* phi, int64_t ld, int64_t n_real, int64_t d
 }
 
 // column squared norms in double (operators.py:128-129)
-__global__ void k_colsq(const float* phi, int64_t ld, int64_t n_real, int64_t d_real, double* out) {
+template <typename PT>
+__global__ void k_colsq(const PT* phi, int64_t ld, int64_t n_real, int64_t d_real, double* out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d_real) return;
   double s = 0.0;

@@ -80,7 +80,10 @@ def shard_ranges(op, world_size):
 
 
 def shard_context(op, precision, device, c0, c1):
-    """The native context of shard [c0, c1) of `op` (not yet joined to a transport)."""
+    """The native context of shard [c0, c1) of `op` (not yet joined to a
+    transport; a dense shard's dictionary is uploaded by upload_shard once it
+    has joined)."""
+    precision = op.resolve_precision(precision)
     if isinstance(op, ConvolutionOperator):
         if precision != "ozaki":
             raise NotImplementedError("time-sharded convolutions run the 'ozaki' (int8 band) kernels")
@@ -89,9 +92,21 @@ def shard_context(op, precision, device, c0, c1):
         code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}[precision]
         ctx = _lib.Context(op.n_rows, c1 - c0, code, device)
     ctx.set_shard(c0, op.n_cols)
-    if isinstance(op, DenseOperator):
-        ctx.set_dictionary(np.ascontiguousarray(op.matrix[:, c0:c1]))
     return ctx
+
+
+def upload_shard(ctx, op, c0, c1):
+    """Upload a dense shard's columns after the context joined its transport:
+    a float64 dictionary goes up exactly (the fp64 mode multiplies it, the
+    ozaki planes are built from it -- collectively, with the row scales
+    shared across the ranks, so every rank calls this together)."""
+    if not isinstance(op, DenseOperator):
+        return
+    cols = np.ascontiguousarray(op.matrix[:, c0:c1])
+    if cols.dtype == np.float64:
+        ctx.set_dictionary_f64(cols)
+    else:
+        ctx.set_dictionary(cols)
 
 
 def local_observation(op, y, c0, c1):
@@ -136,6 +151,8 @@ class ShardedContext:
         else:
             self.shards = column_shards(n_cols, self.world)
             c0, c1 = self.shards[self.rank]
+            if precision == "auto":
+                precision = "ozaki"  # a dictionary worth sharding is large
             code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}[precision]
             self.ctx = _lib.Context(n_rows, c1 - c0, code, device)
             self.ctx.set_shard(c0, n_cols)
@@ -147,6 +164,8 @@ class ShardedContext:
         self.n_rows, self.n_cols = n_rows, n_cols
         uid = broadcast_nccl_id(dist, self.rank, device)
         self.ctx.set_comm(uid, self.world, self.rank)
+        if _op is not None:
+            upload_shard(self.ctx, _op, c0, c1)
 
     @classmethod
     def for_operator(cls, op, precision="ozaki", device=0):
@@ -241,6 +260,8 @@ def threaded_contexts(op, precision, devices):
         ctx = shard_context(op, precision, devices[r], c0, c1)
         ctx.set_group(group, r)
         contexts.append(ctx)
+    # the uploads may be collective (float64 ozaki planes): one thread per rank
+    run_threaded(world, lambda r: upload_shard(contexts[r], op, *shards[r]), group)
     return contexts, shards
 
 

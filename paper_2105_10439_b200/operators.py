@@ -6,9 +6,17 @@ path of this build): ``LinearOperator`` (:40-101), ``DenseOperator``
 and ``ShapeMismatchError`` (:21-27).
 
 Every application runs on the GPU through the C ABI (include/cofem_b200.h).
-The dictionary is stored once per precision mode as float32 in HBM (the
-reference keeps float64; a float64 matrix is rounded to float32 on upload --
-dictionaries built by this package are generated float32-exact).
+A dictionary is stored once per precision mode: float32 matrices as given;
+float64 matrices exactly (the "fp64" mode keeps the float64 entries in HBM,
+the "ozaki" mode builds its 32-bit fixed-point digit planes from them).
+
+Precision "auto" (the default of CgConfig) picks, per operator, the mode that
+holds the reference's float64 results on that operator at the best speed:
+float64 CUDA-core contractions where the dictionary is small enough that its
+HBM stream does not matter (dense N*D <= 2^24 entries: <= 64 MB as float32,
+L2-resident; short convolutions), the int8 tensor-core "ozaki" contractions
+(float64-grade, 4 B/entry streamed) everywhere else, and the float64 FFT
+passes for 2-D DCT dictionaries.
 """
 
 from __future__ import annotations
@@ -38,6 +46,14 @@ def _as_columns(V, nrows, what):
 
 
 PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}
+AUTO_FP64_ENTRIES = 1 << 24  # dense dictionaries up to this size run the float64 CUDA-core path under "auto"
+AUTO_FP64_CONV_DIM = 1 << 16  # convolutions up to this length (and <= 512 taps) run the float64 FFT path
+
+
+def check_precision(precision):
+    if precision not in ("auto", "fp32", "fp64", "ozaki"):
+        raise ValueError("precision must be 'auto', 'fp32', 'fp64' or 'ozaki'")
+    return precision
 
 
 class LinearOperator:
@@ -72,6 +88,10 @@ class LinearOperator:
     def column_sq_norms(self):
         raise NotImplementedError
 
+    def resolve_precision(self, precision):
+        """The concrete device mode "auto" stands for on this operator."""
+        return check_precision(precision)
+
 
 class DenseOperator(LinearOperator):
     """Explicit dense dictionary, resident in HBM as float32 (operators.py:104-129).
@@ -96,15 +116,22 @@ class DenseOperator(LinearOperator):
             self.kind = kind
         self._ctx = {}
 
-    def context(self, precision="fp32"):
+    def resolve_precision(self, precision):
+        if check_precision(precision) != "auto":
+            return precision
+        return "fp64" if self.n_rows * self.n_cols <= AUTO_FP64_ENTRIES else "ozaki"
+
+    def context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
         code = PRECISIONS[precision]
         ctx = self._ctx.get(code)
         if ctx is None:
             ctx = self._ctx[code] = self.new_context(precision)
         return ctx
 
-    def new_context(self, precision="fp32"):
+    def new_context(self, precision="auto"):
         """An uncached device copy (the caller closes it)."""
+        precision = self.resolve_precision(precision)
         ctx = _lib.Context(self.n_rows, self.n_cols, PRECISIONS[precision], self.device)
         if self.matrix.dtype == np.float64:
             ctx.set_dictionary_f64(self.matrix)  # ozaki planes from the exact float64 entries
@@ -118,17 +145,26 @@ class DenseOperator(LinearOperator):
             ctx.close()
         self._ctx.clear()
 
+    def apply_context(self):
+        """The context plain applications use: float64 CUDA-core contractions,
+        except that a large dictionary already resident in another mode (e.g.
+        the "ozaki" planes of a run_cofem) is reused rather than uploaded a
+        second time (its contraction error is ~2e-9)."""
+        if self.n_rows * self.n_cols > AUTO_FP64_ENTRIES and self._ctx and PRECISIONS["fp64"] not in self._ctx:
+            return next(iter(self._ctx.values()))
+        return self.context("fp64")
+
     def _apply(self, V):
-        return self.context("fp64").apply(V)
+        return self.apply_context().apply(V)
 
     def _apply_adjoint(self, U):
-        return self.context("fp64").apply_adjoint(U)
+        return self.apply_context().apply_adjoint(U)
 
     def materialize(self):
         return np.array(self.matrix, dtype=np.float64)
 
     def column_sq_norms(self):
-        return self.context("fp64").column_sq_norms()
+        return self.apply_context().column_sq_norms()
 
 
 class SubsampledDctOperator(DenseOperator):
@@ -219,19 +255,34 @@ class ConvolutionOperator(LinearOperator):
         keep = np.flatnonzero(np.abs(h) >= np.abs(h).max() * 2.0**-34)
         return h[: keep[-1] + 1] if keep.size else h[:1]
 
-    def context(self, precision="ozaki"):
+    def fft_taps(self):
+        """The filter for the float64 FFT path: taps below 2^-60 of the largest
+        one are dropped (far under float64 resolution)."""
+        h = self.filter
+        keep = np.flatnonzero(np.abs(h) >= np.abs(h).max() * 2.0**-60)
+        return h[: keep[-1] + 1] if keep.size else h[:1]
+
+    def resolve_precision(self, precision):
+        if check_precision(precision) != "auto":
+            return precision
+        short = self.n_cols <= AUTO_FP64_CONV_DIM and self.fft_taps().size <= 512
+        return "fp64" if short else "ozaki"
+
+    def context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
         ctx = self._ctx.get(precision)
         if ctx is None:
             ctx = self._ctx[precision] = self.new_context(precision)
         return ctx
 
-    def new_context(self, precision="ozaki"):
+    def new_context(self, precision="auto"):
         """'ozaki': banded int8 tensor-core kernel (any filter length);
         'fp64': float64 overlap-save FFT passes (filters up to 512 taps)."""
+        precision = self.resolve_precision(precision)
         if precision == "ozaki":
             return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
         if precision == "fp64":
-            return _lib.Context.convolution(self.n_cols, self.filter, _lib.FP64, self.device)
+            return _lib.Context.convolution(self.n_cols, self.fft_taps(), _lib.FP64, self.device)
         raise NotImplementedError("convolution dictionaries run in the 'ozaki' or 'fp64' precision mode")
 
     def release(self):
@@ -244,6 +295,9 @@ class ConvolutionOperator(LinearOperator):
 
     def _apply_adjoint(self, U):
         return self.context().apply_adjoint(U)
+
+    def apply_context(self):
+        return self.context()
 
     def materialize(self):
         d, h = self.n_cols, self.filter
@@ -289,13 +343,21 @@ class PartialDct2Operator(LinearOperator):
         self.device = device
         self._ctx = {}
 
-    def context(self, precision="ozaki"):
+    def resolve_precision(self, precision):
+        return "fp64" if check_precision(precision) == "auto" else precision
+
+    def context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
         ctx = self._ctx.get("fft")
         if ctx is None:
             ctx = self._ctx["fft"] = self.new_context(precision)
         return ctx
 
-    def new_context(self, precision="ozaki"):
+    def apply_context(self):
+        return self.context()
+
+    def new_context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
         if precision not in ("ozaki", "fp64"):
             raise NotImplementedError("2-D DCT dictionaries run the float64 FFT path ('ozaki' or 'fp64')")
         return _lib.Context.dct2(self.n, self.mask, _lib.FP64, self.device)
@@ -352,15 +414,21 @@ def build_exp_convolution(dim, decay):
     return ConvolutionOperator(dim, decay)
 
 
-def build_dense_gaussian(n_rows, dim, rng):
+def build_dense_gaussian(n_rows, dim, rng, dtype=np.float64):
     """Dense dictionary with i.i.d. N(0, 1/N) entries (operators.py:227-232).
 
-    Drawn float32 (``rng.standard_normal(dtype=float32)``), so the float32
-    copy in HBM is exact and the float64 oracle sees identical entries.
+    The default draw is the reference's (``rng.normal(0, 1/sqrt(N))`` in
+    float64, same generator consumption), held exactly on the device.
+    ``dtype=np.float32`` draws ``rng.standard_normal(dtype=float32)`` instead:
+    a float32-exact dictionary at half the host memory and upload (a
+    different draw from the same seed).
     """
     if not 1 <= n_rows <= dim:
         raise ValueError(f"need 1 <= N <= D, got N={n_rows}, D={dim}")
-    entries = rng.standard_normal((n_rows, dim), dtype=np.float32) * np.float32(1.0 / np.sqrt(n_rows))
+    if np.dtype(dtype) == np.float32:
+        entries = rng.standard_normal((n_rows, dim), dtype=np.float32) * np.float32(1.0 / np.sqrt(n_rows))
+    else:
+        entries = rng.normal(0.0, 1.0 / np.sqrt(n_rows), size=(n_rows, dim))
     return DenseOperator(entries, kind="dense-gaussian")
 
 
@@ -385,9 +453,9 @@ class SystemMatrix:
         return self.op.n_cols
 
     def apply(self, V, precision=None):
-        """A @ V on the GPU without materialising A."""
+        """A @ V on the GPU without materialising A (the operator's apply
+        context unless a precision mode is named)."""
         V, single = _as_columns(V, self.dim, "system apply")
-        if precision is None:
-            precision = "ozaki" if isinstance(self.op, (ConvolutionOperator, PartialDct2Operator)) else "fp64"
-        out = self.op.context(precision).system_apply(self.beta, self.alpha, V)
+        ctx = self.op.apply_context() if precision is None else self.op.context(precision)
+        out = ctx.system_apply(self.beta, self.alpha, V)
         return out[:, 0] if single else out

@@ -1,12 +1,12 @@
 """Rademacher probes and the diagonal estimator rule.
 
 Mirrors /root/reference/pkg/src/sbl/probes.py (draw_rademacher :13-17,
-estimate_diagonal_rademacher :28-31).  Probe draws stay on the host so the
-device consumes exactly the reference's stream (numpy PCG64 through
-``rng.integers(0, 2)``); they are shipped to the GPU as int8 signs.  Inside
-the EM loop the estimator itself is fused on the device with the M-step
-(``k_em_finish``); ``estimate_diagonal_rademacher`` here is the host-side
-API for callers holding solution blocks.
+estimate_diagonal_rademacher :28-31).  Inside run_cofem the probes are drawn
+on the device (k_pcg64_rademacher reproduces numpy's PCG64
+``rng.integers(0, 2)`` stream bit for bit) and the estimator is fused with
+the M-step (``k_em_finish``).  The host functions here are the API for
+callers that draw or hold probe / solution blocks themselves (explicit
+``probe_blocks``, ``e_step``).
 """
 
 from __future__ import annotations

@@ -5,8 +5,11 @@ L2 error of mu and alpha is <= 1e-4, the recovered support (alpha below the
 pruning threshold 1e6 used by the reference's test_cofem.py:347) is identical
 and the NMSE against the ground truth is within 1% relative.
 
-Three device precisions are tested:
-  ozaki -- (default) fp64 blocks; both Phi contractions exact int32 sums of
+Four device precisions are tested:
+  auto  -- (default) per operator: fp64 below 2^24 dictionary entries,
+           ozaki above (the BASELINE bar everywhere, tests/test_baseline_
+           configs_gpu.py holds all five configs to it);
+  ozaki -- fp64 blocks; both Phi contractions exact int32 sums of
            int8 digit products on the tensor cores over a 32-bit fixed-point
            dictionary (relative contraction error ~2e-9): meets the mu,
            support and NMSE bounds everywhere and alpha wherever the reference
@@ -49,7 +52,7 @@ ALPHA_FP32_TOL = 2e-3
 # dense-small is chaotic: its CG solves hit the 100-step cap for ~30 EM
 # iterations, so ANY perturbation (even 2^-48 fixed point, see DESIGN.md
 # "Parity") saturates at ~1e-4 in alpha; the tolerance reflects that.
-ALPHA_SMALL_TOL = {"fp64": 1e-4, "ozaki": 1e-3, "fp32": ALPHA_FP32_TOL}
+ALPHA_SMALL_TOL = {"auto": 1e-4, "fp64": 1e-4, "ozaki": 1e-3, "fp32": ALPHA_FP32_TOL}
 PRECISIONS = ["ozaki", "fp64", "fp32"]
 PRUNE = 1e6
 
@@ -188,7 +191,7 @@ def _check_cofem(st, est, diag, g, precision, alpha_tol):
     assert np.all(steps >= 1)
 
 
-@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("precision", ["auto"] + PRECISIONS)
 def test_run_cofem_dense_small_parity(precision):
     g = golden("cofem_dense-small.npz")
     c = S.CONFIGS["dense-small"]
@@ -199,7 +202,7 @@ def test_run_cofem_dense_small_parity(precision):
     _check_cofem(st, est, diag, g, precision, alpha_tol)
     nmse_ref, nmse = S.nmse(g["mu"], z), S.nmse(est.mu, z)
     assert abs(nmse - nmse_ref) <= 0.01 * nmse_ref
-    if precision == "fp64":
+    if precision in ("fp64", "auto"):
         same = np.mean(np.array([d["cg_steps"] for d in diag]) == g["cg_steps"])
         assert same >= 0.8
 
@@ -379,7 +382,7 @@ def test_run_cofem_convolution_parity(precision):
     st, est, diag = run_cofem(prob, cfg)
     emu, ea = rel(est.mu, g["mu"]), rel(st.alpha, g["alpha"])
     assert emu <= 1e-4 and ea <= 1e-4, (emu, ea, [d["cg_steps"] for d in diag], list(g["cg_steps"]))
-    if precision == "fp64":  # the int8 path adds ~20 % steps on this sensitive workload (scratch/conv_emul.py)
+    if precision == "fp64":  # the int8 path adds ~20 % steps on this sensitive workload (tools/conv_emul.py)
         assert np.all(np.abs(np.array([d["cg_steps"] for d in diag]) - g["cg_steps"]) <= 3)
     np.testing.assert_array_equal(st.alpha < PRUNE, g["alpha"] < PRUNE)
     nref, nour = S.nmse(g["mu"], g["z"]), S.nmse(est.mu, g["z"])
@@ -394,7 +397,7 @@ def test_run_cofem_convolution_config_family(K, precision):
     band epilogue.  (The reference's own D=512, beta=1e4 convolution workload
     is far more sensitive: ANY 1e-9-level arithmetic -- even float rounding
     of the operand to 31 significant bits -- adds ~20 % CG steps there, see
-    scratch/conv_emul.py; its test holds mu / alpha / support only.)"""
+    tools/conv_emul.py; its test holds mu / alpha / support only.)"""
     c = S.ConvConfig("conv-test", 8192, 256, 20.0, 0.01, 0.05, K, 3, 200, 1e-5)
     prob, z = S.conv_problem(c)
     st, est, diag = run_cofem(prob, c.cofem_config(precision))
@@ -442,7 +445,7 @@ def test_run_cofem_dct2_parity_with_oracle():
 
 
 # --------------------------------------------- the reference's own workloads --
-@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+@pytest.mark.parametrize("precision", ["auto", "ozaki", "fp64"])
 def test_reference_dct1d_recovery_parity(precision):
     """test_cofem.py:257-265 workload (SubsampledDctOperator D=1024, N=341, 30 EM
     iterations): parity with the reference and its NRMSE < 2% bar."""
@@ -454,11 +457,14 @@ def test_reference_dct1d_recovery_parity(precision):
     st, est, diag = run_cofem(prob, cfg)
     emu, ea = rel(est.mu, g["dct_mu"]), rel(st.alpha, g["dct_alpha"])
     # the reference's default CG tolerance (1e-4) leaves each E-step converged
-    # only to 1e-4: a 1e-9 operator difference can flip a step count at the
-    # threshold and move the iterate ~1e-4, hence alpha <= 1e-3 here (the
-    # BASELINE configs run at tol 1e-5 and are held to 1e-4)
-    assert emu <= 1e-4 and ea <= 1e-3, (emu, ea)
-    assert_dct_steps_close([d["cg_steps"] for d in diag], g["dct_steps"])
+    # only to 1e-4: a 1e-9 operator difference (ozaki) can flip a step count
+    # at the threshold and move the iterate ~1e-4, hence alpha <= 1e-3 there;
+    # the float64 dictionary in the fp64 / default mode holds the 1e-4 bar
+    assert emu <= 1e-4 and ea <= (1e-3 if precision == "ozaki" else 1e-4), (emu, ea)
+    if precision == "ozaki":
+        assert_dct_steps_close([d["cg_steps"] for d in diag], g["dct_steps"])
+    else:  # float64: a tol-1e-4 stop can still land one or two steps apart
+        assert np.all(np.abs(np.array([d["cg_steps"] for d in diag]) - g["dct_steps"]) <= 2)
     assert S.nrmse(est.mu, g["dct_z"]) < 2.0
     np.testing.assert_array_equal(st.alpha < PRUNE, g["dct_alpha"] < PRUNE)
 
@@ -476,18 +482,23 @@ def assert_dct_steps_close(steps, ref):
     assert abs(steps.sum() - ref.sum()) <= 0.15 * ref.sum(), (steps, ref)
 
 
-@pytest.mark.parametrize("precision", ["ozaki", "fp64"])
+@pytest.mark.parametrize("precision", ["auto", "ozaki", "fp64"])
 def test_reference_dense_float64_parity(precision):
     """A float64 (not float32-exact) dictionary from the reference's conftest
-    generator: the ozaki planes are built from the float64 entries."""
+    generator: the fp64 mode multiplies the exact float64 entries, the ozaki
+    planes are built from them."""
     g = golden("reference_workloads.npz")
     prob = SblProblem(g["d64_y"], DenseOperator(g["d64_phi"]), 1e4)
     cfg = CofemConfig(iterations=30, probes=20, seed=0, cg=CgConfig(precision=precision))
     st, est, diag = run_cofem(prob, cfg)
     emu, ea = rel(est.mu, g["d64_mu"]), rel(st.alpha, g["d64_alpha"])
+    # alpha: this workload (reference default tolerance 1e-4, 30 iterations of
+    # ~100-step solves) is summation-order chaotic -- the reference's own
+    # recursion with only the order of the matmul sums permuted moves alpha by
+    # 1.4e-4 (tests/test_host_api.py::test_float64_workload_alpha_is_
+    # summation_order_sensitive) -- so the float64 modes are held to 5e-4
     assert emu <= 1e-4, (emu, ea)
-    if precision == "ozaki":
-        assert ea <= 1e-3, (emu, ea)
+    assert ea <= (1e-3 if precision == "ozaki" else 5e-4), (emu, ea)
     np.testing.assert_array_equal(st.alpha < PRUNE, g["d64_alpha"] < PRUNE)
 
 
@@ -602,11 +613,13 @@ def test_multitask_shared_support_dct_parity_and_pooling():
     tasks = _multitask_golden_tasks(g, "dct")
     cfg = CofemConfig(iterations=30, probes=20, seed=42)
     st, ests, diag = run_cofem_multitask(MultiTaskProblem(tuple(tasks)), cfg)
-    # reference default tolerance 1e-4 (see test_reference_dct1d_recovery_parity)
+    # default precision (float64 DCT dictionaries multiplied exactly); the
+    # reference's default tolerance 1e-4 makes alpha summation-order
+    # sensitive at the 1e-4 level (see test_reference_dense_float64_parity)
     ea = rel(st.alpha, g["dct_alpha"])
     for l, e in enumerate(ests):
         assert rel(e.mu, g[f"dct_mu{l}"]) <= 1e-4, l
-    assert ea <= 1e-3, ea
+    assert ea <= 5e-4, ea
     assert_dct_steps_close([d["cg_steps"] for d in diag], g["dct_steps"])
     support = g["dct_support"]
 
@@ -690,3 +703,86 @@ def test_transposed_planes_equal_mn_major_planes_bitwise():
     assert outs[0]["steps"] == outs[1]["steps"]
     np.testing.assert_array_equal(np.array(outs[0]["mu"]), np.array(outs[1]["mu"]))
     np.testing.assert_array_equal(np.array(outs[0]["alpha"]), np.array(outs[1]["alpha"]))
+
+
+# ---- float64 dictionaries, API completeness ---------------------------------------
+
+def test_float64_dictionary_is_exact_in_fp64_mode():
+    """A float64 dictionary is multiplied exactly in the fp64 mode (no float32
+    rounding): the reference's contract that a full-mask SubsampledDct is
+    orthonormal -- apply then adjoint returns v -- holds to 1e-10, and a
+    random float64 matrix matches numpy to rounding."""
+    from paper_2105_10439_b200 import SubsampledDctOperator
+
+    rng = np.random.default_rng(4)
+    op = SubsampledDctOperator(512, np.arange(512))
+    v = rng.standard_normal((512, 3))
+    assert rel(op.apply_adjoint(op.apply(v)), v) <= 1e-10
+    phi = rng.standard_normal((300, 700))
+    dop = DenseOperator(phi)
+    V, U = rng.standard_normal((700, 5)), rng.standard_normal((300, 4))
+    assert rel(dop.context("fp64").apply(V), phi @ V) <= 1e-14
+    assert rel(dop.context("fp64").apply_adjoint(U), phi.T @ U) <= 1e-14
+    np.testing.assert_allclose(dop.context("fp64").column_sq_norms(), (phi * phi).sum(axis=0), rtol=1e-13)
+
+
+def test_solve_blocked_distinct_systems_matches_oracle():
+    """cg.solve_blocked (cg.py:201-234) with a different operator, beta and
+    alpha per block: one lockstep device PCG against the oracle's lockstep
+    recursion over the block-diagonal system (aggregate stopping rule)."""
+    rng = np.random.default_rng(17)
+    d = 96
+    phis = [(rng.standard_normal((40, d)) / np.sqrt(40)).astype(np.float32) for _ in range(2)]
+    betas, alphas = [30.0, 80.0], [rng.random(d) + 0.5, rng.random(d) + 0.2]
+    systems = [SystemMatrix(DenseOperator(p), b, a) for p, b, a in zip(phis, betas, alphas)]
+    Bs = [rng.standard_normal((d, 3)), rng.standard_normal((d, 5))]
+    pres = [make_preconditioner("all-ones", s.op, s.beta, s.alpha) for s in systems]
+    rep, slices = solve_blocked(systems, Bs, pres, CgConfig(max_steps=300, tolerance=1e-10, precision="fp64"))
+    assert [(s.start, s.stop) for s in slices] == [(0, 3), (3, 8)]
+    oops = [O.dense_op(p) for p in phis]
+
+    def apply_fn(V):
+        return np.concatenate([O.system_apply(oops[g], betas[g], alphas[g], V[:, sl])
+                               for g, sl in enumerate(slices)], axis=1)
+
+    minv = np.concatenate([np.repeat((1.0 / p.m)[:, None], b.shape[1], 1) for p, b in zip(pres, Bs)], axis=1)
+    oref = O.pcg_solve(apply_fn, np.concatenate(Bs, axis=1), minv, O.CgConfig(max_steps=300, tolerance=1e-10))
+    assert abs(rep.steps_taken - oref.steps_taken) <= 1
+    assert rel(rep.solution, oref.solution) <= 1e-8
+    assert rep.converged and rep.breakdown_columns.size == 0
+
+
+def test_run_cofem_returns_cg_report_and_wall_times():
+    """PosteriorEstimate.cg_report is the final E-step's CgReport (cofem.py:
+    97-100): mu = beta x_{K+1}, s = mean_k p_k x_k over its solution block;
+    diagnostics carry a per-iteration wall_time (cofem.py:127-133)."""
+    from paper_2105_10439_b200 import draw_probe_blocks
+
+    c = S.CONFIGS["dense-small"]
+    prob, _, _ = S.dense_cs_problem(c)
+    T = 4
+    st, est, diag = run_cofem(prob, c.cofem_config(iterations=T))
+    rep = est.cg_report
+    assert rep.solution.shape == (c.D, c.K + 1)
+    assert rep.steps_taken == diag[-1]["cg_steps"] and rep.final_relative_residual == diag[-1]["cg_residual"]
+    np.testing.assert_allclose(est.mu, c.beta * rep.solution[:, c.K], rtol=1e-13, atol=0)
+    probes = draw_probe_blocks(c.D, c.K, T, c.seed)[-1].astype(np.float64)
+    np.testing.assert_allclose(est.s, (probes * rep.solution[:, :c.K]).mean(axis=1), rtol=1e-10, atol=1e-18)
+    walls = [d["wall_time"] for d in diag]
+    assert all(w > 0 for w in walls) and len(set(walls)) > 1
+
+
+def test_two_devices_threaded_shards():
+    """kernels' raised shared-memory limits are per device; shards
+    on two GPUs of one process (in-process group, peer reads) must run."""
+    if _lib.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2105_10439_b200.distributed import run_cofem_threaded
+
+    c = S.CONFIGS["dense-mid"]
+    prob, _, _ = S.dense_cs_problem(c)
+    cfg = c.cofem_config("ozaki", iterations=2)
+    st1, est1, d1 = run_cofem(prob, cfg)
+    st2, est2, d2 = run_cofem_threaded(prob, cfg, devices=(0, 1))
+    assert [d["cg_steps"] for d in d1] == [d["cg_steps"] for d in d2]
+    assert rel(est2.mu, est1.mu) <= 1e-7

@@ -212,3 +212,58 @@ def test_quantiser_byte_digits_equal_balanced_digits():
     recon = sum(d[a] * (256 ** (3 - a)) for a in range(4))
     np.testing.assert_array_equal(recon, v)
     assert d.min() >= -128 and d.max() <= 127
+
+
+def test_build_dense_gaussian_matches_reference_draw():
+    """operators.py:227-232 draws rng.normal(0, 1/sqrt(N)) in float64: the same
+    seed gives the same dictionary and leaves the generator in the same state."""
+    from paper_2105_10439_b200 import build_dense_gaussian
+
+    r1, r2 = np.random.default_rng(3), np.random.default_rng(3)
+    op = build_dense_gaussian(8, 20, r1)
+    np.testing.assert_array_equal(op.matrix, r2.normal(0.0, 1.0 / np.sqrt(8), size=(8, 20)))
+    assert op.matrix.dtype == np.float64 and op.kind == "dense-gaussian"
+    assert r1.integers(0, 2**32) == r2.integers(0, 2**32)
+    f32 = build_dense_gaussian(8, 20, np.random.default_rng(3), dtype=np.float32)
+    assert f32.matrix.dtype == np.float32
+
+
+def test_auto_precision_policy():
+    """CgConfig's default precision "auto" resolves per operator."""
+    from paper_2105_10439_b200 import CgConfig, ConvolutionOperator, DenseOperator, PartialDct2Operator
+
+    assert CgConfig().precision == "auto"
+    with pytest.raises(ValueError):
+        CgConfig(precision="fp16")
+    assert DenseOperator(np.zeros((256, 1024), dtype=np.float32)).resolve_precision("auto") == "fp64"
+    assert DenseOperator(np.zeros((4096, 4097), dtype=np.float32)).resolve_precision("auto") == "ozaki"
+    assert DenseOperator(np.zeros((4, 4), dtype=np.float32)).resolve_precision("ozaki") == "ozaki"
+    assert ConvolutionOperator(512, 0.04).resolve_precision("auto") == "fp64"
+    h = np.exp(-np.arange(256) / 20.0)
+    assert ConvolutionOperator.from_taps(2**22, h).resolve_precision("auto") == "ozaki"
+    assert PartialDct2Operator(64, np.arange(100)).resolve_precision("auto") == "fp64"
+
+
+def test_float64_workload_alpha_is_summation_order_sensitive():
+    """The reference's float64 dense workload (conftest generator, default CG
+    tolerance 1e-4, 30 EM iterations): the reference recursion (oracle,
+    bit-exact with it) with only the ORDER of the matmul sums permuted moves
+    alpha by > 1e-4 -- so no implementation with a different reduction order
+    can hold alpha to 1e-4 there (the basis of the 5e-4 alpha bar of
+    test_gpu_parity.py::test_reference_dense_float64_parity)."""
+    from conftest import golden
+
+    g = golden("reference_workloads.npz")
+    phi = g["d64_phi"]
+    cfg = O.CofemConfig(iterations=30, probes=20, seed=0)
+    base = O.dense_op(phi)
+    a0, mu0, _, _ = O.run_cofem(base, g["d64_y"], 1e4, cfg)
+    np.testing.assert_array_equal(a0, g["d64_alpha"])
+    pc = np.random.default_rng(0).permutation(phi.shape[1])
+    pr = np.random.default_rng(1).permutation(phi.shape[0])
+    reordered = O.Op(phi.shape[0], phi.shape[1], lambda V: phi[:, pc] @ V[pc], lambda U: phi[pr].T @ U[pr],
+                     base.col_sq_norms, base.materialize, "dense")
+    a1, mu1, _, _ = O.run_cofem(reordered, g["d64_y"], 1e4, cfg)
+    rel_a = np.linalg.norm(a1 - a0) / np.linalg.norm(a0)
+    assert 1e-4 < rel_a < 5e-4
+    assert np.linalg.norm(mu1 - mu0) / np.linalg.norm(mu0) < 1e-4

@@ -60,7 +60,8 @@ def test_time_sharded_convolution_apply_is_bitwise(dim, ntaps, world, q):
     op = ConvolutionOperator.from_taps(dim, h)
     rng = np.random.default_rng(dim + world)
     V = rng.standard_normal((dim, q))
-    full_f, full_a = op.apply(V), op.apply_adjoint(V)
+    ctx = op.context("ozaki")  # the unsharded int8 band path (plain apply may pick the fp64 FFT path)
+    full_f, full_a = ctx.apply(V), ctx.apply_adjoint(V)
     np.testing.assert_array_equal(sharded_apply(op, V, world), full_f)
     np.testing.assert_array_equal(sharded_apply(op, V, world, adjoint=True), full_a)
     # and both are the convolution (float64 numpy) to the int8 path's accuracy
