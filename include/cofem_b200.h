@@ -286,6 +286,8 @@ typedef struct {
   int64_t bwd_launches;
   int64_t pcg_steps;        /* PCG steps executed */
   int64_t kernel_launches;  /* all kernels launched by the library */
+  double solve_ms;          /* CUDA-event time of the one-launch PCG solves (dense, one GPU) */
+  int64_t solve_launches;   /* their launches (fwd_ms / bwd_ms then hold their contraction phases) */
 } cofem_timing;
 
 int cofem_bench_prepare(cofem_ctx* ctx, const double* y, double beta, const cofem_em_config* em,

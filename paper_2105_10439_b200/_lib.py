@@ -100,6 +100,8 @@ class TimingC(ctypes.Structure):
         ("bwd_launches", c_int64),
         ("pcg_steps", c_int64),
         ("kernel_launches", c_int64),
+        ("solve_ms", c_double),
+        ("solve_launches", c_int64),
     ]
 
 

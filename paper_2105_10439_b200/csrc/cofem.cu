@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -29,6 +30,7 @@
 #include "dct.cuh"
 #include "ozaki.cuh"
 #include "pcg.cuh"
+#include "persistent.cuh"
 
 using namespace cofem;
 
@@ -304,6 +306,15 @@ struct cofem_ctx {
   cofem_cg_config cg{};
   uint64_t dseed = 0;
   int bench_iter = 0;
+
+  // persistent (one-launch) PCG solves: grid barrier words, phase stamps
+  unsigned* gbar = nullptr;
+  size_t gbar_cap = 0;
+  unsigned long long* ptimes = nullptr;
+  int ptimes_cap = 0;
+  bool persistent_off = false;  // COFEM_NO_PERSISTENT: always the multi-kernel step
+  double ph_fwd_ms = 0, ph_bwd_ms = 0, solve_ms = 0;
+  int64_t solve_launches = 0;
 
   // instrumentation
   bool time_kernels = false;
@@ -1213,6 +1224,167 @@ int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
   return 0;
 }
 
+// ---- one-launch PCG solve (persistent.cuh) --------------------------------
+// dense dictionary, int8 path, one GPU, one column chunk, one preconditioner group
+bool persistent_eligible(cofem_ctx* c, int ngroups) {
+  return c->kind == 0 && c->prec == COFEM_OZAKI && c->nranks <= 1 && c->phiqT && c->ldq <= QCHUNK &&
+         ngroups == 1 && !c->persistent_off;
+}
+
+// split plan of one contraction phase (the constraints of oz_contract)
+SplitPlan persistent_splits(cofem_ctx* c, int64_t rows_out, int64_t k_total, size_t cap, int QW) {
+  SplitPlan sp = plan_splits(rows_out / oz::BM, k_total / oz::KT, oz::KT, c->sm_count, (double)rows_out * QW * 8.0,
+                             (double)c->Np * c->Dp * 4.0);
+  while (sp.per_split > oz::MAX_K_PER_ITEM || (size_t)sp.nsplit * rows_out * QW * 8 > cap) {
+    if (sp.per_split > oz::MAX_K_PER_ITEM) sp.per_split = oz::MAX_K_PER_ITEM;
+    else sp.per_split *= 2;
+    sp.nsplit = (int)((k_total + sp.per_split - 1) / sp.per_split);
+  }
+  return sp;
+}
+
+template <int QW>
+int launch_persistent_t(cofem_ctx* c, double beta, int q_real, const cofem_cg_config* cg) {
+  using PC = oz::PsCfg<QW>;
+  static DeviceFlags flags;
+  CKR(smem_attr_once(flags, oz::pcg_persistent<QW>, PC::SMEM));
+  const int slot = QW / 8;
+  if (!c->map_p_ok[slot]) {
+    CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
+    c->map_p_ok[slot] = true;
+  }
+  if (!c->map_v_ok[slot]) {
+    CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
+    c->map_v_ok[slot] = true;
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oz::pcg_persistent<QW>, oz::PS_THREADS, PC::SMEM));
+  if (occ < 1) return fail(COFEM_ECUDA, "persistent PCG kernel cannot be resident");
+  const int grid = c->sm_count;
+  if ((size_t)grid * 4 * QW > (size_t)c->nblk_elem * 2 * std::max(c->ldq, QCHUNK))
+    return fail(COFEM_ECUDA, "persistent PCG partials do not fit");
+  const SplitPlan fp = persistent_splits(c, c->Np, c->Dp, c->vpart_cap, QW);
+  const SplitPlan bp = persistent_splits(c, c->Dp, c->Np, c->ppart_cap, QW);
+  // grid barrier words
+  const size_t nbar = 2;
+  if (c->gbar_cap < nbar) {
+    if (c->gbar) cudaFree(c->gbar);
+    c->gbar = nullptr;
+    CK(cudaMalloc(&c->gbar, nbar * sizeof(unsigned)));
+    c->gbar_cap = nbar;
+  }
+  CK(cudaMemsetAsync(c->gbar, 0, nbar * sizeof(unsigned), c->stream));
+  unsigned long long* times = nullptr;
+  if (c->time_kernels) {
+    const int need = (cg->max_steps + 1) * oz::PS_TIMES;
+    if (c->ptimes_cap < need) {
+      if (c->ptimes) cudaFree(c->ptimes);
+      c->ptimes = nullptr;
+      CK(cudaMalloc(&c->ptimes, need * sizeof(unsigned long long)));
+      c->ptimes_cap = need;
+    }
+    CK(cudaMemsetAsync(c->ptimes, 0, need * sizeof(unsigned long long), c->stream));
+    times = c->ptimes;
+  }
+  Scalars sc = c->sc();
+  oz::PcgPersistArgs a{};
+  a.Np = c->Np;
+  a.Dp = c->Dp;
+  a.N = c->N;
+  a.D = c->D;
+  a.q_real = q_real;
+  a.f_mblocks = (int)(c->Np / oz::BM);
+  a.f_nsplit = fp.nsplit;
+  a.f_kps = fp.per_split;
+  a.f_items = a.f_mblocks * fp.nsplit;
+  a.b_mblocks = (int)(c->Dp / oz::BM);
+  a.b_nsplit = bp.nsplit;
+  a.b_kps = bp.per_split;
+  a.b_items = a.b_mblocks * bp.nsplit;
+  a.rowscale = c->rowscale;
+  a.colscale = c->colscale;
+  a.P0 = (double*)c->P;
+  a.P1 = (double*)c->P2;
+  a.X = (double*)c->X;
+  a.R = (double*)c->R;
+  a.minv = c->minv;
+  a.alpha = c->alpha;
+  a.vpart = (double*)c->vpart;
+  a.ppart = (double*)c->ppart;
+  a.V = (double*)c->V;
+  a.pq = c->pq;
+  a.vq = c->vq;
+  a.colmax_p = c->colmax;
+  a.colmax_v = c->vcolmax;
+  a.red = c->partials;
+  a.rho1 = sc.rho[1];
+  a.bn2 = sc.bn2;
+  a.frozen = c->frozen;
+  a.beta = beta;
+  a.tol = cg->tolerance;
+  a.max_steps = cg->max_steps;
+  a.printed = cg->printed_recursion;
+  a.st = c->st;
+  a.bar = c->gbar;
+  a.times = times;
+  void* args[] = {&c->map_phi_fwd, &c->map_p[slot], &c->map_phiT, &c->map_v[slot], &a};
+  cudaEvent_t e0 = nullptr;
+  if (c->time_kernels) {
+    e0 = next_event(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  CK(cudaLaunchCooperativeKernel((const void*)oz::pcg_persistent<QW>, dim3(grid), dim3(oz::PS_THREADS), args,
+                                 PC::SMEM, c->stream));
+  if (c->time_kernels) {
+    cudaEvent_t e1 = next_event(c);
+    cudaEventRecord(e1, c->stream);
+    c->timed.push_back({2, c->evnext - 2});
+  }
+  c->launches++;
+  c->solve_launches++;
+  return 0;
+}
+
+int launch_persistent(cofem_ctx* c, double beta, int q_real, const cofem_cg_config* cg) {
+  switch (c->ldq) {
+    case 8: return launch_persistent_t<8>(c, beta, q_real, cg);
+    case 16: return launch_persistent_t<16>(c, beta, q_real, cg);
+    case 24: return launch_persistent_t<24>(c, beta, q_real, cg);
+    case 32: return launch_persistent_t<32>(c, beta, q_real, cg);
+  }
+  return fail(COFEM_EINVAL, "persistent PCG: unsupported column count");
+}
+
+// phase stamps of the last persistent solve -> contraction phase times
+int persistent_phase_times(cofem_ctx* c, int steps) {
+  if (!c->ptimes || steps < 1) return 0;
+  std::vector<unsigned long long> t((size_t)(steps + 1) * oz::PS_TIMES);
+  CK(cudaMemcpy(t.data(), c->ptimes, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  for (int u = 1; u <= steps; ++u) {
+    const unsigned long long* s = &t[(size_t)u * oz::PS_TIMES];
+    if (s[2] > s[1]) c->ph_fwd_ms += (s[2] - s[1]) * 1e-6;  // Phi P phase
+    if (s[5] > s[4]) c->ph_bwd_ms += (s[5] - s[4]) * 1e-6;  // Phi^T V phase
+  }
+  if (getenv("COFEM_PHASE_DUMP") && steps > 1) {  // mean phase durations (us), steps 1..steps-1
+    double ph[7] = {}, wk[7] = {};
+    for (int u = 1; u < steps; ++u) {
+      const unsigned long long* s = &t[(size_t)u * oz::PS_TIMES];
+      const unsigned long long* n = &t[(size_t)(u + 1) * oz::PS_TIMES];
+      for (int p = 0; p < 7; ++p) {
+        ph[p] += ((p < 6 ? s[p + 1] : n[0]) - s[p]) * 1e-3;
+        wk[p] += (s[8 + p] - s[p]) * 1e-3;
+      }
+    }
+    const double m = 1.0 / (steps - 1);
+    fprintf(stderr, "phases(us) A %.1f B %.1f C %.1f D %.1f E %.1f F %.1f H %.1f | CTA0 work A %.1f B %.1f C %.1f "
+            "D %.1f E %.1f F %.1f H %.1f\n", ph[0] * m, ph[1] * m, ph[2] * m, ph[3] * m, ph[4] * m, ph[5] * m,
+            ph[6] * m, wk[0] * m, wk[1] * m, wk[2] * m, wk[3] * m, wk[4] * m, wk[5] * m, wk[6] * m);
+  }
+  c->fwd_launches += steps;
+  c->bwd_launches += steps;
+  return 0;
+}
+
 // the blocked PCG on resident R (= B), minv, groups; result in X
 template <typename T>
 int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* groups, const cofem_cg_config* cg,
@@ -1269,8 +1441,10 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   CK(cudaGetLastError());
   c->p_colmax_valid = oz;
 
+  const bool persistent = std::is_same<T, double>::value && persistent_eligible(c, ngroups);
+  if (persistent) CKR(launch_persistent(c, beta, q_real, cg));
   int u = 1;
-  for (; u <= cg->max_steps; ++u) {
+  for (; !persistent && u <= cg->max_steps; ++u) {
     if (u > LAG) {
       const int slot = (u - LAG) % LAG;
       CK(cudaEventSynchronize(c->ev[slot]));
@@ -1300,6 +1474,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   CK(cudaMemcpyAsync(&fin, c->st, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->pcg_steps += fin.steps;
+  if (persistent && c->time_kernels) CKR(persistent_phase_times(c, fin.steps));
   rep->steps_taken = fin.steps;
   rep->converged = fin.converged;
   rep->diverged = fin.diverged;
@@ -1768,7 +1943,9 @@ int run_multi_impl(cofem_ctx** cs, int L, const double* const* ys, const double*
     }
     if (rc) break;
     cofem_cg_report rep;
-    rc = pcg_multi<T>(cs, L, betas, K + 1, cg, &rep, agg, dptrs);
+    // one task IS the single-task solve (same kernels, same reduction order)
+    rc = L == 1 ? pcg_device<T>(c0, betas[0], K + 1, 1, nullptr, cg, &rep)
+                : pcg_multi<T>(cs, L, betas, K + 1, cg, &rep, agg, dptrs);
     if (steps) steps[t - 1] = rep.steps_taken;
     if (resid) resid[t - 1] = rep.final_relative_residual;
     if (rc == COFEM_EDIVERGED) {
@@ -1897,6 +2074,7 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   cofem_ctx* c = new cofem_ctx();
   c->device = device;
   c->prec = precision;
+  c->persistent_off = getenv("COFEM_NO_PERSISTENT") != nullptr;
   c->N = n_rows;
   c->D = n_cols;
   c->Np = round_up(n_rows, PAD);
@@ -2181,7 +2359,7 @@ int cofem_destroy(cofem_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_ws(c);
-  void* ptrs[] = {c->phi, c->phi64, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
+  void* ptrs[] = {c->gbar, c->ptimes, c->phi, c->phi64, c->alpha, c->minv, c->theta, c->colsq, c->mu, c->s, c->aty, c->ybuf,
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
@@ -2713,6 +2891,8 @@ int cofem_bench_iterations(cofem_ctx* c, int n_iter, int time_kernels, cofem_tim
   c->evnext = 0;
   c->timed.clear();
   c->launches = c->fwd_launches = c->bwd_launches = c->pcg_steps = 0;
+  c->ph_fwd_ms = c->ph_bwd_ms = 0;
+  c->solve_launches = 0;
   CK(cudaEventRecord(c->t0, c->stream));
   for (int i = 0; i < n_iter; ++i) {
     cofem_cg_report rep;
@@ -2732,8 +2912,12 @@ int cofem_bench_iterations(cofem_ctx* c, int n_iter, int time_kernels, cofem_tim
     float d = 0;
     cudaEventElapsedTime(&d, c->evpool[tk.second], c->evpool[tk.second + 1]);
     if (tk.first == 0) out->fwd_ms += d;
-    else out->bwd_ms += d;
+    else if (tk.first == 1) out->bwd_ms += d;
+    else out->solve_ms += d;
   }
+  out->fwd_ms += c->ph_fwd_ms;  // contraction phases of persistent solves (globaltimer stamps)
+  out->bwd_ms += c->ph_bwd_ms;
+  out->solve_launches = c->solve_launches;
   out->fwd_launches = c->fwd_launches;
   out->bwd_launches = c->bwd_launches;
   out->pcg_steps = c->pcg_steps;

@@ -251,6 +251,17 @@ def test_run_cofem_variants_parity(name, precision):
     mu_tol = {"fp64": 1e-6, "ozaki": 1e-6, "fp32": 5e-3}[precision]
     a_tol = {"fp64": 1e-4, "ozaki": 1e-4, "fp32": 5e-3}[precision]
     assert rel(est.mu, p("mu")) <= mu_tol
+    if precision == "ozaki" and name == "nonneg":
+        # tol 1e-6 at beta 1e4 sits at this 64 x 128 system's rounding floor:
+        # the reference recursion on the int8 path's own arithmetic model
+        # (oracle.ozaki_op) already hits the 200-step cap where the float64
+        # run stops at ~170 and moves alpha by 5e-5 -- so the device is held
+        # to that model at 1e-4, and to the float64 golden at 3e-4
+        ocfg = O.CofemConfig(iterations=int(T), probes=int(K), seed=int(seed), variant="nonneg",
+                             cg=O.CgConfig(max_steps=int(U), tolerance=tol))
+        m_alpha, m_mu, _, _ = O.run_cofem(O.ozaki_op(p("phi")), p("y"), beta, ocfg)
+        assert rel(st.alpha, m_alpha) <= 1e-4 and rel(est.mu, m_mu) <= 1e-6
+        a_tol = 3e-4
     assert rel(st.alpha, p("alpha")) <= a_tol
     np.testing.assert_array_equal(st.alpha < PRUNE, p("alpha") < PRUNE)
 
@@ -692,7 +703,8 @@ def test_transposed_planes_equal_mn_major_planes_bitwise():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for mn in (False, True):
-        env = dict(os.environ, PYTHONPATH=root)
+        # both on the multi-kernel step (the one-launch solve needs the transposed copy)
+        env = dict(os.environ, PYTHONPATH=root, COFEM_NO_PERSISTENT="1")
         if mn:
             env["COFEM_MN_MAJOR_ONLY"] = "1"
         else:
@@ -786,3 +798,42 @@ def test_two_devices_threaded_shards():
     st2, est2, d2 = run_cofem_threaded(prob, cfg, devices=(0, 1))
     assert [d["cg_steps"] for d in d1] == [d["cg_steps"] for d in d2]
     assert rel(est2.mu, est1.mu) <= 1e-7
+
+
+def test_one_launch_solve_matches_multikernel_step():
+    """The persistent one-launch PCG solve (dense, one GPU, int8 path) and the
+    multi-kernel step (COFEM_NO_PERSISTENT) run the same recursion; they
+    differ only in reduction order and in pi = beta ||Phi P||^2 + <P, alpha P>
+    (the one-launch form, no A P block) vs <P, A P>: same CG steps, mu /
+    alpha to 1e-7, each bitwise repeatable."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, numpy as np\n"
+        "from paper_2105_10439_b200 import run_cofem\n"
+        "from paper_2105_10439_b200 import simulate as S\n"
+        "c = S.CONFIGS['dense-mid']\n"
+        "prob, z, _ = S.dense_cs_problem(c)\n"
+        "runs = [run_cofem(prob, c.cofem_config('ozaki', iterations=3)) for _ in range(2)]\n"
+        "st, est, diag = runs[0]\n"
+        "same = bool(np.array_equal(st.alpha, runs[1][0].alpha) and np.array_equal(est.mu, runs[1][1].mu))\n"
+        "print(json.dumps({'mu': est.mu.tolist(), 'alpha': st.alpha.tolist(), 'same': same,"
+        " 'steps': [d['cg_steps'] for d in diag]}))\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for multi in (False, True):
+        env = dict(os.environ, PYTHONPATH=root)
+        env.pop("COFEM_NO_PERSISTENT", None)
+        if multi:
+            env["COFEM_NO_PERSISTENT"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["same"] and outs[1]["same"]
+    assert outs[0]["steps"] == outs[1]["steps"], (outs[0]["steps"], outs[1]["steps"])
+    assert rel(np.array(outs[0]["mu"]), np.array(outs[1]["mu"])) <= 1e-7
+    assert rel(np.array(outs[0]["alpha"]), np.array(outs[1]["alpha"])) <= 1e-7
