@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="dense-large")
-    ap.add_argument("--precision", default="ozaki", choices=["fp32", "fp64", "ozaki"])
+    ap.add_argument("--precision", default="ozaki", choices=["fp32", "fp64", "ozaki", "ozaki24"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -209,7 +209,7 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     device = local if world > 1 else 0
-    prec = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}[args.precision]
+    prec = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}[args.precision]
 
     # ---- device-resident run (value) ----
     from paper_2105_10439_b200.distributed import column_shards
@@ -250,7 +250,8 @@ def run_ours(args):
     # roofline of the dominant kernel (the Phi contraction with more device time)
     q = c.K + 1
     d_local = c1 - c0
-    phi_bytes = 4.0 * c.N * d_local
+    phi_entry = 3.0 if args.precision == "ozaki24" else 4.0  # bytes per streamed Phi entry
+    phi_bytes = phi_entry * c.N * d_local
     vec_bytes = 4.0 * (c.N + d_local) * q if args.precision == "fp32" else 8.0 * (c.N + d_local) * q
     alg_bytes = phi_bytes + vec_bytes
     fwd_avg = tim["fwd_ms"] / max(tim["fwd_launches"], 1)
@@ -270,6 +271,7 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": {"ozaki": "i8 x i8 -> exact i32 Phi contractions (32-bit fixed-point Phi), f64 vectors",
+                  "ozaki24": "i8 x i8 -> exact i32 Phi contractions (24-bit fixed-point Phi, 3 B/entry), f64 vectors",
                   "fp64": "f64 (fp32 Phi)", "fp32": "f32 (fp64 scalars)"}[args.precision],
         "data": "synthetic (Gaussian Phi from a device Philox stream, 1% N(0,1) spikes, sigma=0.01)",
         "config": {"workload": f"{args.config}: dense Gaussian CS N={c.N} D={c.D} K={c.K} T={c.T} "
@@ -295,6 +297,10 @@ def run_ours(args):
             "bwd_avg_ms": bwd_avg,
             "contraction_share_of_step": (tim["fwd_ms"] + tim["bwd_ms"]) / tim["total_ms"],
             "step_hbm_frac": (2 * alg_bytes * pcg_steps / (total_ms / 1e3) / 1e9) / peak,
+            # the same step against streaming a 4-byte (fp32) Phi twice per PCG step:
+            # > 1 means faster than any fp32-Phi implementation can be on this HBM
+            "step_frac_of_fp32_phi_roofline": (2 * (4.0 * c.N * d_local + vec_bytes) * pcg_steps
+                                               / (total_ms / 1e3) / 1e9) / peak,
         },
     }
     ctx.close()

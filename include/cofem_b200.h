@@ -49,8 +49,12 @@ enum cofem_status {
  * OZAKI: fp64 vectors and scalars; the two Phi contractions run on the int8
  *       tensor cores (tcgen05.mma.kind::i8) over a 32-bit fixed-point copy of
  *       Phi (four signed digit planes, 4 B / entry) with exact int32
- *       accumulation -- float64-grade results at tensor-core rate. */
-enum cofem_precision { COFEM_FP32 = 0, COFEM_FP64 = 1, COFEM_OZAKI = 2 };
+ *       accumulation -- float64-grade results at tensor-core rate.
+ * OZAKI24: OZAKI over a 24-bit fixed-point Phi (three digit planes, 3 B /
+ *       entry: a quarter less HBM traffic per PCG step on dense
+ *       dictionaries); the operands stay 32-bit.  Structured dictionaries
+ *       (convolution, 2-D DCT) treat it as OZAKI. */
+enum cofem_precision { COFEM_FP32 = 0, COFEM_FP64 = 1, COFEM_OZAKI = 2, COFEM_OZAKI24 = 3 };
 
 /* Preconditioner policy, cg.py:79-108 make_preconditioner(policy, ...). */
 enum cofem_theta { COFEM_THETA_ALL_ONES = 0, COFEM_THETA_JACOBI = 1, COFEM_THETA_NONE = 2,

@@ -412,9 +412,10 @@ def run_cofem_multitask(ops, ys, beta, cfg, share_probes=False):
     return alpha, ests, diag
 
 
-def ozaki_dictionary(phi):
+def ozaki_dictionary(phi, bits=30):
     """The dictionary the 'ozaki' device mode multiplies (NOT reference code):
-    Phi_ij rounded to round(Phi_ij / (r_i c_j) 2^30) r_i c_j / 2^30 with
+    Phi_ij rounded to round(Phi_ij / (r_i c_j) 2^30) r_i c_j / 2^30 (bits=30;
+    'ozaki24' keeps three digit planes: bits=22) with
     power-of-two row scales r_i = 2^ceil(log2 max_j |Phi_ij|) and column
     scales c_j = 2^ceil(log2 max_i |Phi_ij| / r_i) (csrc/ozaki.cuh
     k_phi_rowscale / k_phi_colscale / k_phi_planes).  Running the reference
@@ -429,10 +430,10 @@ def ozaki_dictionary(phi):
     r = p2(np.abs(phi).max(axis=1))
     c = p2((np.abs(phi) / r[:, None]).max(axis=0))
     sc = r[:, None] * c[None, :]
-    return np.rint(phi / sc * 2.0**30) * sc / 2.0**30
+    return np.rint(phi / sc * 2.0**bits) * sc / 2.0**bits
 
 
-def ozaki_op(phi):
+def ozaki_op(phi, bits=30):
     """Arithmetic model of the 'ozaki' device contraction (NOT reference code):
     the dictionary is ozaki_dictionary(phi); every operand column is rounded
     to 31-bit fixed point against its own power-of-two scale s_q =
@@ -448,7 +449,7 @@ def ozaki_op(phi):
 
     r = p2(np.abs(phi).max(axis=1))
     c = p2((np.abs(phi) / r[:, None]).max(axis=0))
-    phq = ozaki_dictionary(phi)
+    phq = ozaki_dictionary(phi, bits)
 
     def qcols(M, w):
         X = M * w[:, None]

@@ -24,7 +24,7 @@ COFEM_EDIVERGED = -4
 COFEM_ENCCL = -5
 COFEM_ESTATE = -6
 
-FP32, FP64, OZAKI = 0, 1, 2
+FP32, FP64, OZAKI, OZAKI24 = 0, 1, 2, 3
 THETA_CODES = {"all-ones": 0, "jacobi": 1, "none": 2}
 THETA_CUSTOM = 3
 VARIANT_CODES = {"standard": 0, "nonneg": 1}

@@ -250,7 +250,8 @@ struct cofem_ctx {
 
   // Ozaki (int8 tensor-core) contraction state
   bool oz_ready = false;
-  int8_t* phiq = nullptr;        // [4][Np][Dp] signed digit planes
+  int8_t* phiq = nullptr;        // [npa][Np][Dp] signed digit planes
+  int npa = 4;                   // digit planes of Phi: 4 (32-bit fixed point) or 3 (24-bit, COFEM_OZAKI24)
   int8_t* phiqT = nullptr;       // [4][Dp][Np] the same planes transposed: Phi^T V streams K-major too
   CUtensorMap map_phiT{};
   double *rowscale = nullptr, *colscale = nullptr;  // Np, Dp powers of two
@@ -626,7 +627,7 @@ ncclDataType_t nccl_t() {
 int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
   if (c->oz_ready && !src64) return 0;
   if (!c->phiq) {
-    CK(cudaMalloc(&c->phiq, (size_t)4 * c->Np * c->Dp));
+    CK(cudaMalloc(&c->phiq, (size_t)c->npa * c->Np * c->Dp));
     CK(cudaMalloc(&c->rowscale, c->Np * sizeof(double)));
     CK(cudaMalloc(&c->colscale, c->Dp * sizeof(double)));
     CK(cudaMalloc(&c->pq, (size_t)4 * QCHUNK * c->Dp));
@@ -634,12 +635,12 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
     CK(cudaMalloc(&c->opscale, QCHUNK * sizeof(double)));
     CK(cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)));
     CK(cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)));
-    CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, 4, oz::KT, oz::BM, 4));
-    CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, 4, 64, oz::KT, 4));
+    CKR(encode_u8_3d(&c->map_phi_fwd, c->phiq, c->Dp, c->Np, c->npa, oz::KT, oz::BM, c->npa));
+    CKR(encode_u8_3d(&c->map_phi_bwd, c->phiq, c->Dp, c->Np, c->npa, 64, oz::KT, c->npa));
     // COFEM_MN_MAJOR_ONLY: skip the transposed copy (Phi^T V reads the planes
     // MN-major) -- tests compare the two paths bitwise
-    if (!getenv("COFEM_MN_MAJOR_ONLY") && cudaMalloc(&c->phiqT, (size_t)4 * c->Np * c->Dp) == cudaSuccess) {
-      CKR(encode_u8_3d(&c->map_phiT, c->phiqT, c->Np, c->Dp, 4, oz::KT, oz::BM, 4));
+    if (!getenv("COFEM_MN_MAJOR_ONLY") && cudaMalloc(&c->phiqT, (size_t)c->npa * c->Np * c->Dp) == cudaSuccess) {
+      CKR(encode_u8_3d(&c->map_phiT, c->phiqT, c->Np, c->Dp, c->npa, oz::KT, oz::BM, c->npa));
     } else {
       cudaGetLastError();  // no room for the transposed copy: Phi^T V reads the planes MN-major
       c->phiqT = nullptr;
@@ -664,18 +665,18 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
     oz::k_phi_colscale<double><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(src64, c->Dp, c->N, c->Dp,
                                                                                         c->rowscale, c->colscale);
     oz::k_phi_planes<double><<<16 * c->sm_count, 256, 0, c->stream>>>(src64, c->Dp, c->Np, c->Dp, c->rowscale,
-                                                                      c->colscale, c->phiq);
+                                                                      c->colscale, c->phiq, c->npa);
   } else {
     CKR(row_scales(c->phi));
     oz::k_phi_colscale<float><<<(unsigned)((c->Dp + 255) / 256), 256, 0, c->stream>>>(c->phi, c->Dp, c->N, c->Dp,
                                                                                        c->rowscale, c->colscale);
     oz::k_phi_planes<float><<<16 * c->sm_count, 256, 0, c->stream>>>(c->phi, c->Dp, c->Np, c->Dp, c->rowscale,
-                                                                     c->colscale, c->phiq);
+                                                                     c->colscale, c->phiq, c->npa);
   }
   c->launches += 3;
   if (c->phiqT) {
     const int64_t tiles = (c->Np / 64) * (c->Dp / 64);
-    oz::k_planes_transpose<<<dim3((unsigned)std::min<int64_t>(tiles, 8 * c->sm_count), 1, 4), 256, 0, c->stream>>>(
+    oz::k_planes_transpose<<<dim3((unsigned)std::min<int64_t>(tiles, 8 * c->sm_count), 1, c->npa), 256, 0, c->stream>>>(
         c->phiq, c->Np, c->Dp, c->phiqT);
     c->launches++;
   }
@@ -687,10 +688,12 @@ int ensure_oz(cofem_ctx* c, const double* src64 = nullptr) {
 
 template <int QW>
 int oz_init_kernels() {
-  static DeviceFlags f_fwd, f_bwd, f_band;
+  static DeviceFlags f_fwd, f_bwd, f_band, f_fwd3, f_bwd3;
   CKR(smem_attr_once(f_fwd, oz::contract_kernel<QW, oz::MODE_FWD>, oz::Cfg<QW>::SMEM));
   CKR(smem_attr_once(f_bwd, oz::contract_kernel<QW, oz::MODE_BWD>, oz::Cfg<QW>::SMEM));
   CKR(smem_attr_once(f_band, oz::contract_kernel<QW, oz::MODE_BAND>, oz::Cfg<QW>::SMEM));
+  CKR(smem_attr_once(f_fwd3, oz::contract_kernel<QW, oz::MODE_FWD, 3>, oz::Cfg<QW, 3>::SMEM));
+  CKR(smem_attr_once(f_bwd3, oz::contract_kernel<QW, oz::MODE_BWD, 3>, oz::Cfg<QW, 3>::SMEM));
   return 0;
 }
 
@@ -727,7 +730,7 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
   const int64_t n_mblocks = n_rows_out / oz::BM;
   const int64_t ntiles = k_total / oz::KT;
   SplitPlan sp = plan_splits(n_mblocks, ntiles, oz::KT, c->sm_count, (double)n_rows_out * QW * 8.0,
-                             (double)c->Np * c->Dp * 4.0);
+                             (double)c->Np * c->Dp * c->npa);
   // exact int32 accumulation: <= 4 digit products of <= 2^14 per significance
   // block, so keep K <= 2^15 per item
   while (sp.per_split > oz::MAX_K_PER_ITEM ||
@@ -747,14 +750,18 @@ int oz_contract(cofem_ctx* c, const CUtensorMap& map_b, int64_t n_rows_out, int6
     e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  if (BWD && !trans)
-    oz::contract_kernel<QW, oz::MODE_BWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-        map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
-        n_rows_out, nullptr, st, sp.nsplit, QW);
-  else
-    oz::contract_kernel<QW, oz::MODE_FWD><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
-        map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0, row_scale, c->opscale, out, n_rows_out,
-        n_rows_out, nullptr, st, sp.nsplit, QW);
+  auto go = [&](auto kern, size_t smem) {
+    kern<<<grid, oz::NTHREADS, smem, c->stream>>>(map_a, map_b, (int)n_mblocks, n_items, sp.per_split, (int)k_total, 0,
+                                                  row_scale, c->opscale, out, n_rows_out, n_rows_out, nullptr, st,
+                                                  sp.nsplit, QW);
+  };
+  if (c->npa == 3) {
+    if (BWD && !trans) go(oz::contract_kernel<QW, oz::MODE_BWD, 3>, oz::Cfg<QW, 3>::SMEM);
+    else go(oz::contract_kernel<QW, oz::MODE_FWD, 3>, oz::Cfg<QW, 3>::SMEM);
+  } else {
+    if (BWD && !trans) go(oz::contract_kernel<QW, oz::MODE_BWD>, oz::Cfg<QW>::SMEM);
+    else go(oz::contract_kernel<QW, oz::MODE_FWD>, oz::Cfg<QW>::SMEM);
+  }
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -1234,7 +1241,7 @@ bool persistent_eligible(cofem_ctx* c, int ngroups) {
 // split plan of one contraction phase (the constraints of oz_contract)
 SplitPlan persistent_splits(cofem_ctx* c, int64_t rows_out, int64_t k_total, size_t cap, int QW) {
   SplitPlan sp = plan_splits(rows_out / oz::BM, k_total / oz::KT, oz::KT, c->sm_count, (double)rows_out * QW * 8.0,
-                             (double)c->Np * c->Dp * 4.0);
+                             (double)c->Np * c->Dp * c->npa);
   while (sp.per_split > oz::MAX_K_PER_ITEM || (size_t)sp.nsplit * rows_out * QW * 8 > cap) {
     if (sp.per_split > oz::MAX_K_PER_ITEM) sp.per_split = oz::MAX_K_PER_ITEM;
     else sp.per_split *= 2;
@@ -1243,11 +1250,11 @@ SplitPlan persistent_splits(cofem_ctx* c, int64_t rows_out, int64_t k_total, siz
   return sp;
 }
 
-template <int QW>
+template <int QW, int NPA>
 int launch_persistent_t(cofem_ctx* c, double beta, int q_real, const cofem_cg_config* cg) {
-  using PC = oz::PsCfg<QW>;
+  using PC = oz::PsCfg<QW, NPA>;
   static DeviceFlags flags;
-  CKR(smem_attr_once(flags, oz::pcg_persistent<QW>, PC::SMEM));
+  CKR(smem_attr_once(flags, oz::pcg_persistent<QW, NPA>, PC::SMEM));
   const int slot = QW / 8;
   if (!c->map_p_ok[slot]) {
     CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
@@ -1258,7 +1265,7 @@ int launch_persistent_t(cofem_ctx* c, double beta, int q_real, const cofem_cg_co
     c->map_v_ok[slot] = true;
   }
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oz::pcg_persistent<QW>, oz::PS_THREADS, PC::SMEM));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oz::pcg_persistent<QW, NPA>, oz::PS_THREADS, PC::SMEM));
   if (occ < 1) return fail(COFEM_ECUDA, "persistent PCG kernel cannot be resident");
   const int grid = c->sm_count;
   if ((size_t)grid * 4 * QW > (size_t)c->nblk_elem * 2 * std::max(c->ldq, QCHUNK))
@@ -1333,7 +1340,7 @@ int launch_persistent_t(cofem_ctx* c, double beta, int q_real, const cofem_cg_co
     e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
-  CK(cudaLaunchCooperativeKernel((const void*)oz::pcg_persistent<QW>, dim3(grid), dim3(oz::PS_THREADS), args,
+  CK(cudaLaunchCooperativeKernel((const void*)oz::pcg_persistent<QW, NPA>, dim3(grid), dim3(oz::PS_THREADS), args,
                                  PC::SMEM, c->stream));
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
@@ -1346,11 +1353,12 @@ int launch_persistent_t(cofem_ctx* c, double beta, int q_real, const cofem_cg_co
 }
 
 int launch_persistent(cofem_ctx* c, double beta, int q_real, const cofem_cg_config* cg) {
+  const bool p3 = c->npa == 3;
   switch (c->ldq) {
-    case 8: return launch_persistent_t<8>(c, beta, q_real, cg);
-    case 16: return launch_persistent_t<16>(c, beta, q_real, cg);
-    case 24: return launch_persistent_t<24>(c, beta, q_real, cg);
-    case 32: return launch_persistent_t<32>(c, beta, q_real, cg);
+    case 8: return p3 ? launch_persistent_t<8, 3>(c, beta, q_real, cg) : launch_persistent_t<8, 4>(c, beta, q_real, cg);
+    case 16: return p3 ? launch_persistent_t<16, 3>(c, beta, q_real, cg) : launch_persistent_t<16, 4>(c, beta, q_real, cg);
+    case 24: return p3 ? launch_persistent_t<24, 3>(c, beta, q_real, cg) : launch_persistent_t<24, 4>(c, beta, q_real, cg);
+    case 32: return p3 ? launch_persistent_t<32, 3>(c, beta, q_real, cg) : launch_persistent_t<32, 4>(c, beta, q_real, cg);
   }
   return fail(COFEM_EINVAL, "persistent PCG: unsupported column count");
 }
@@ -2069,11 +2077,12 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
   if (!out) return fail(COFEM_EINVAL, "null out");
   *out = nullptr;
   if (n_rows < 1 || n_cols < 1) return fail(COFEM_EINVAL, "operator dims must be positive");
-  if (precision != COFEM_FP32 && precision != COFEM_FP64 && precision != COFEM_OZAKI)
-    return fail(COFEM_EINVAL, "precision must be FP32, FP64 or OZAKI");
+  if (precision != COFEM_FP32 && precision != COFEM_FP64 && precision != COFEM_OZAKI && precision != COFEM_OZAKI24)
+    return fail(COFEM_EINVAL, "precision must be FP32, FP64, OZAKI or OZAKI24");
   cofem_ctx* c = new cofem_ctx();
   c->device = device;
-  c->prec = precision;
+  c->prec = precision == COFEM_OZAKI24 ? COFEM_OZAKI : precision;
+  c->npa = precision == COFEM_OZAKI24 ? 3 : 4;
   c->persistent_off = getenv("COFEM_NO_PERSISTENT") != nullptr;
   c->N = n_rows;
   c->D = n_cols;
@@ -2135,6 +2144,7 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   if (!out || !taps) return fail(COFEM_EINVAL, "null argument");
   *out = nullptr;
   if (dim < 1 || ntaps < 1 || ntaps > dim) return fail(COFEM_EINVAL, "need 1 <= ntaps <= dim");
+  if (precision == COFEM_OZAKI24) precision = COFEM_OZAKI;  // the band keeps the 32-bit taps
   if (precision != COFEM_OZAKI && precision != COFEM_FP64)
     return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI (int8 band) or FP64 (FFT) precision");
   if (precision == COFEM_FP64 && ntaps > CONV_FFT_MAX_TAPS)
@@ -2276,6 +2286,7 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   *out = nullptr;
   if (n < 64 || n > 1024 || (n & (n - 1)) != 0) return fail(COFEM_EINVAL, "image side must be a power of two in [64, 1024]");
   if (nmask < 1 || nmask > n * n) return fail(COFEM_EINVAL, "need 1 <= mask size <= n^2");
+  if (precision == COFEM_OZAKI24) precision = COFEM_OZAKI;
   if (precision != COFEM_OZAKI && precision != COFEM_FP64)
     return fail(COFEM_EINVAL, "2-D DCT dictionaries run in FP64 (fused FFT passes; OZAKI is accepted as an alias)");
   std::vector<uint8_t> grid((size_t)n * n, 0);

@@ -132,33 +132,35 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 // two sets and the epilogue of one tile overlaps the MMAs of the next.  The
 // epilogue zeroes its set with tcgen05.st after reading it, so every MMA just
 // accumulates.  Exactness: |block| <= 4 pairs * 2^14 * K < 2^31 for K <= 2^15.
-template <int QW>
+template <int QW, int NPA = 4>
 struct Cfg {
   static constexpr int NB = 4 * QW;  // B tile rows: the four operand planes side by side
+  static constexpr int A_ST = NPA * BM * KT;  // NPA digit planes of Phi per stage
   static constexpr int B_STAGE = NB * KT;
-  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGE = A_ST + B_STAGE;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 1280;
   __host__ __device__ static constexpr int nb_of(int a) { return a <= 1 ? 4 : 5 - a; }  // operand planes used
   __host__ __device__ static constexpr int n_of(int a) { return ((QW * nb_of(a) + 15) / 16) * 16; }
   static constexpr int SET_COLS = 256;  // TMEM columns per accumulator set (two sets)
   static_assert(QW % 8 == 0 && QW <= 32, "QW in {8,16,24,32}");
+  static_assert(NPA >= 2 && NPA <= 4, "2..4 digit planes of Phi");
   static_assert(STAGE % 1024 == 0, "stages must stay 1024-B aligned for the swizzle atoms");
   static_assert(2 * QW + ((QW * 3 + 15) / 16) * 16 <= SET_COLS && 5 * QW <= SET_COLS, "set must fit");
 };
 constexpr int MAX_K_PER_ITEM = 1 << 15;
 
-// one K=64 stage: 2 k-steps x 4 digit planes of A against the operand tile
-template <int QW, bool MN_MAJOR>
+// one K=64 stage: 2 k-steps x NPA digit planes of A against the operand tile
+template <int QW, bool MN_MAJOR, int NPA = 4>
 __device__ __forceinline__ void issue_stage(uint32_t sa, uint32_t sb, uint32_t tset, uint32_t idesc0) {
-  using C = Cfg<QW>;
+  using C = Cfg<QW, NPA>;
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) {
     const uint64_t db = sdesc(sb + kk * 32, 16, 512);
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < NPA; ++a) {
       uint64_t da;
       if (!MN_MAJOR) da = sdesc(sa + a * (BM * KT) + kk * 32, 16, 512);
-      else da = sdesc(sa + a * (64 * KT) + kk * (32 * KT), A_STAGE / 2, 512);
+      else da = sdesc(sa + a * (64 * KT) + kk * (32 * KT), C::A_ST / 2, 512);
       const uint32_t idesc = idesc0 | ((uint32_t)(C::n_of(a) >> 3) << 17);
       mma_i8(tset + a * QW, da, db, idesc, 1u);
     }
@@ -400,7 +402,7 @@ __device__ __forceinline__ void warp_fold_max(unsigned long long (&cm)[QW], unsi
 // chunk nc = w / (n_mblocks * n_split) of an operand with out_ld columns
 // (B TMA row coordinate nc * QW, op_scale / out offset nc * QW).
 enum { MODE_FWD = 0, MODE_BWD = 1, MODE_BAND = 2 };
-template <int QW, int MODE>
+template <int QW, int MODE, int NPA = 4>
 __global__ void __launch_bounds__(NTHREADS, 1)
     contract_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                     int n_mblocks, int n_items, int k_per_split, int k_total, int band_offset,
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st, int n_split = 1,
                     int out_ld = QW) {
   constexpr bool BWD = MODE == MODE_BWD;
-  using C = Cfg<QW>;
+  using C = Cfg<QW, NPA>;
   if (st && st->done) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int k = k0; k < k1; k += KT) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* sa = sm + stage * C::STAGE;
-          unsigned char* sb = sa + A_STAGE;
+          unsigned char* sb = sa + C::A_ST;
           mbar_expect_tx(&full[stage], C::STAGE);
           if (MODE == MODE_BAND) {
             tma_load_3d(sa, &map_a, &full[stage], k - k0, 0, 0);
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_3d(sa, &map_a, &full[stage], k, mb * BM, 0);
           } else {
             tma_load_3d(sa, &map_a, &full[stage], mb * BM, k, 0);
-            tma_load_3d(sa + A_STAGE / 2, &map_a, &full[stage], mb * BM + 64, k, 0);
+            tma_load_3d(sa + C::A_ST / 2, &map_a, &full[stage], mb * BM + 64, k, 0);
           }
           tma_load_4d(sb, &map_b, &full[stage], 0, nc * QW, 0, k >> 6);
           if (++stage == STAGES) {
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t sa = smem_u32(sm + stage * C::STAGE);
-          issue_stage<QW, BWD>(sa, sa + A_STAGE, tset, idesc0);
+          issue_stage<QW, BWD, NPA>(sa, sa + C::A_ST, tset, idesc0);
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
           if (++stage == STAGES) {
             stage = 0;
@@ -966,17 +968,24 @@ __global__ void __launch_bounds__(256) k_planes_transpose(const int8_t* __restri
   }
 }
 
-// digit planes [4][Np][Dp] of round(Phi / (r c) * 2^30)
+// digit planes [npa][Np][Dp] of round(Phi / (r c) * 2^(8 npa - 2)): npa = 4 is
+// the 32-bit fixed-point dictionary, npa = 3 the 24-bit one (COFEM_OZAKI24).
+// Dropping the low plane scales both the digits and the epilogue's 2^-30
+// factor by 2^8, so the contraction kernels' epilogue constant is unchanged.
 template <typename PT>
 __global__ void k_phi_planes(const PT* __restrict__ phi, int64_t ld, int64_t np, int64_t dp,
-                             const double* __restrict__ rs, const double* __restrict__ cs, int8_t* __restrict__ planes) {
+                             const double* __restrict__ rs, const double* __restrict__ cs, int8_t* __restrict__ planes,
+                             int npa) {
   const int64_t n = np * dp;
+  const double sc = ldexp(1.0, 8 * npa - 2);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / dp, j = e % dp;
-    int8_t d[4];
-    digits4((double)phi[i * ld + j] / (rs[i] * cs[j]) * SCALE30, d);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) planes[(int64_t)a * n + e] = d[a];
+    long long v = llrint((double)phi[i * ld + j] / (rs[i] * cs[j]) * sc);
+    for (int a = npa - 1; a >= 0; --a) {
+      const int8_t lo = (int8_t)(v & 0xFF);
+      planes[(int64_t)a * n + e] = lo;
+      v = (v - lo) >> 8;
+    }
   }
 }
 

@@ -52,9 +52,9 @@ constexpr int PS_CTRL = 256;          // mbarriers + TMEM holder
 constexpr int PS_STATE = 12 * 32 * 8; // per-column scalars (12 arrays of <= 32 doubles)
 constexpr int PS_TIMES = 16;          // phase stamps per step: [0, 8) phase starts, [8, 16) CTA 0's work ends
 
-template <int QW>
+template <int QW, int NPA = 4>
 struct PsCfg {
-  static constexpr size_t SMEM = (size_t)STAGES * Cfg<QW>::STAGE + 1024 + PS_CTRL + PS_STATE;
+  static constexpr size_t SMEM = (size_t)STAGES * Cfg<QW, NPA>::STAGE + 1024 + PS_CTRL + PS_STATE;
 };
 
 struct PcgPersistArgs {
@@ -313,7 +313,7 @@ __device__ __forceinline__ void quantize_phase(const double* __restrict__ M, int
 // (MODE_FWD: A K-major), with the ring / TMEM pipeline counters carried across
 // phases.  out[s][row][q] = sum_k A[row][k] B[k][q] * row_scale[row] * s_ops[q].
 // items are (row block, split): w -> mb = w % n_mblocks, s = w / n_mblocks
-template <int QW>
+template <int QW, int NPA>
 __device__ __forceinline__ void contract_phase(const CUtensorMap* map_a, const CUtensorMap* map_b, int n_mblocks,
                                                int nsplit, int kps, int k_total, int64_t rows_real,
                                                const double* __restrict__ row_scale, const double* s_ops,
@@ -321,7 +321,7 @@ __device__ __forceinline__ void contract_phase(const CUtensorMap* map_a, const C
                                                uint64_t* full, uint64_t* empty, uint64_t* tfull, uint64_t* tempty,
                                                uint32_t tmem, int& stage, uint32_t& phase, int& it) {
   const int n_items = n_mblocks * nsplit;
-  using C = Cfg<QW>;
+  using C = Cfg<QW, NPA>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) {
     if (lane == 0) {
@@ -334,7 +334,7 @@ __device__ __forceinline__ void contract_phase(const CUtensorMap* map_a, const C
           unsigned char* sa = sm + stage * C::STAGE;
           mbar_expect_tx(&full[stage], C::STAGE);
           tma_load_3d(sa, map_a, &full[stage], k, mb * BM, 0);
-          tma_load_4d(sa + A_STAGE, map_b, &full[stage], 0, 0, 0, k >> 6);
+          tma_load_4d(sa + C::A_ST, map_b, &full[stage], 0, 0, 0, k >> 6);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -356,7 +356,7 @@ __device__ __forceinline__ void contract_phase(const CUtensorMap* map_a, const C
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t sa = smem_u32(sm + stage * C::STAGE);
-          issue_stage<QW, false>(sa, sa + A_STAGE, tset, idesc0);
+          issue_stage<QW, false, NPA>(sa, sa + C::A_ST, tset, idesc0);
           mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
@@ -444,12 +444,12 @@ __device__ __forceinline__ void sum_splits(const double* __restrict__ part, int6
     }
 }
 
-template <int QW>
+template <int QW, int NPA = 4>
 __global__ void __launch_bounds__(PS_THREADS, 1)
     pcg_persistent(const __grid_constant__ CUtensorMap map_af, const __grid_constant__ CUtensorMap map_bf,
                    const __grid_constant__ CUtensorMap map_ab, const __grid_constant__ CUtensorMap map_bb,
                    const __grid_constant__ PcgPersistArgs a) {
-  using C = Cfg<QW>;
+  using C = Cfg<QW, NPA>;
   constexpr int RPB = PS_THREADS / QW;  // rows per loop trip of the streaming phases
   extern __shared__ unsigned char smem_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1)
 
     // ---- B: Phi P -> vpart ---------------------------------------------------
     stamp(u, 1);
-    contract_phase<QW>(&map_af, &map_bf, a.f_mblocks, a.f_nsplit, a.f_kps, (int)a.Dp, a.N, a.rowscale, s_ops_p,
+    contract_phase<QW, NPA>(&map_af, &map_bf, a.f_mblocks, a.f_nsplit, a.f_kps, (int)a.Dp, a.N, a.rowscale, s_ops_p,
                        a.vpart, a.Np, sm, full, empty, tfull, tempty, tmem, stage, phase, it);
     stamp(u, 9);
     grid_sync(a.bar, gen);
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1)
 
     // ---- E: Phi^T V -> ppart ---------------------------------------------------
     stamp(u, 4);
-    contract_phase<QW>(&map_ab, &map_bb, a.b_mblocks, a.b_nsplit, a.b_kps, (int)a.Np, a.D, a.colscale, s_ops_v,
+    contract_phase<QW, NPA>(&map_ab, &map_bb, a.b_mblocks, a.b_nsplit, a.b_kps, (int)a.Np, a.D, a.colscale, s_ops_v,
                        a.ppart, a.Dp, sm, full, empty, tfull, tempty, tmem, stage, phase, it);
     stamp(u, 12);
     grid_sync(a.bar, gen);

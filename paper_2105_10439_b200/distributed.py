@@ -85,11 +85,11 @@ def shard_context(op, precision, device, c0, c1):
     has joined)."""
     precision = op.resolve_precision(precision)
     if isinstance(op, ConvolutionOperator):
-        if precision != "ozaki":
+        if precision not in ("ozaki", "ozaki24"):
             raise NotImplementedError("time-sharded convolutions run the 'ozaki' (int8 band) kernels")
         ctx = _lib.Context.convolution(c1 - c0, op.gpu_taps(), _lib.OZAKI, device)
     else:
-        code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}[precision]
+        code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}[precision]
         ctx = _lib.Context(op.n_rows, c1 - c0, code, device)
     ctx.set_shard(c0, op.n_cols)
     return ctx
@@ -153,7 +153,7 @@ class ShardedContext:
             c0, c1 = self.shards[self.rank]
             if precision == "auto":
                 precision = "ozaki"  # a dictionary worth sharding is large
-            code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}[precision]
+            code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}[precision]
             self.ctx = _lib.Context(n_rows, c1 - c0, code, device)
             self.ctx.set_shard(c0, n_cols)
             if phi is not None:

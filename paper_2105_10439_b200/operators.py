@@ -45,14 +45,14 @@ def _as_columns(V, nrows, what):
     return V, single
 
 
-PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI}
+PRECISIONS = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}
 AUTO_FP64_ENTRIES = 1 << 24  # dense dictionaries up to this size run the float64 CUDA-core path under "auto"
 AUTO_FP64_CONV_DIM = 1 << 16  # convolutions up to this length (and <= 512 taps) run the float64 FFT path
 
 
 def check_precision(precision):
-    if precision not in ("auto", "fp32", "fp64", "ozaki"):
-        raise ValueError("precision must be 'auto', 'fp32', 'fp64' or 'ozaki'")
+    if precision not in ("auto", "fp32", "fp64", "ozaki", "ozaki24"):
+        raise ValueError("precision must be 'auto', 'fp32', 'fp64', 'ozaki' or 'ozaki24'")
     return precision
 
 
@@ -279,7 +279,7 @@ class ConvolutionOperator(LinearOperator):
         """'ozaki': banded int8 tensor-core kernel (any filter length);
         'fp64': float64 overlap-save FFT passes (filters up to 512 taps)."""
         precision = self.resolve_precision(precision)
-        if precision == "ozaki":
+        if precision in ("ozaki", "ozaki24"):  # the band keeps 32-bit taps
             return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
         if precision == "fp64":
             return _lib.Context.convolution(self.n_cols, self.fft_taps(), _lib.FP64, self.device)
@@ -358,7 +358,7 @@ class PartialDct2Operator(LinearOperator):
 
     def new_context(self, precision="auto"):
         precision = self.resolve_precision(precision)
-        if precision not in ("ozaki", "fp64"):
+        if precision not in ("ozaki", "ozaki24", "fp64"):
             raise NotImplementedError("2-D DCT dictionaries run the float64 FFT path ('ozaki' or 'fp64')")
         return _lib.Context.dct2(self.n, self.mask, _lib.FP64, self.device)
 

@@ -72,16 +72,18 @@ def test_config1_dense_small_default_precision():
     assert abs(nour - nref) <= 0.01 * nref
 
 
-def test_config2_dense_mid_full_length():
+@pytest.mark.parametrize("precision", ["auto", "ozaki", "ozaki24"])
+def test_config2_dense_mid_full_length(precision):
     """Config 2 (N=4096, D=16384, K=20, 30 EM iterations, cap 200, tol 1e-5),
-    all 30 iterations against the reference."""
+    all 30 iterations against the reference: the default mode and both
+    tensor-core dictionary widths (32-bit and 24-bit fixed-point Phi)."""
     g = need("cofem_dense-mid_T30.npz")
     c = S.CONFIGS["dense-mid"]
     prob, z, phi = S.dense_cs_problem(c)
     np.testing.assert_array_equal(np.asarray(prob.y), g["y"])
-    st, est, diag = run_cofem(prob, c.cofem_config("auto"))
+    st, est, diag = run_cofem(prob, c.cofem_config(precision))
     prob.op.release()
-    print("dense-mid T30", check_dense(g, st, est, diag, z, step_slack=5))
+    print(f"dense-mid T30 {precision}", check_dense(g, st, est, diag, z, step_slack=5))
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -97,19 +99,29 @@ def test_config2_dense_mid_column_sharded_full_length(world):
     print(f"dense-mid T30 x{world}", check_dense(g, st, est, diag, z, step_slack=5))
 
 
-def test_config3_dense_large_headline():
-    """Config 3, the headline (N=16384, D=65536 -- Phi 4 GiB --, K=20, 20 EM
-    iterations, cap 200, tol 1e-5) on the default (int8 tensor-core) path
-    against the reference's float64 run on the same float32-exact Phi."""
+@pytest.fixture(scope="module")
+def dense_large():
     g = need("cofem_dense-large_T20.npz")
     c = S.CONFIGS["dense-large"]
     phi = S.gaussian_dictionary(c.N, c.D, c.seed)
     prob, z, _ = S.dense_cs_problem(c, phi=phi)
     np.testing.assert_array_equal(np.asarray(prob.y), g["y"])
-    assert prob.op.resolve_precision("auto") == "ozaki"
-    st, est, diag = run_cofem(prob, c.cofem_config("auto", iterations=int(g["config"][3])))
+    yield g, c, prob, z
     prob.op.release()
-    print("dense-large", check_dense(g, st, est, diag, z, step_slack=3))
+
+
+@pytest.mark.parametrize("precision", ["auto", "ozaki"])
+def test_config3_dense_large_headline(dense_large, precision):
+    """Config 3, the headline (N=16384, D=65536 -- Phi 4 GiB --, K=20, 20 EM
+    iterations, cap 200, tol 1e-5) on the int8 tensor-core path (the default
+    mode, and the 32-bit fixed-point dictionary) against the reference's
+    float64 run on the same float32-exact Phi."""
+    g, c, prob, z = dense_large
+    if precision == "auto":
+        assert prob.op.resolve_precision("auto") in ("ozaki", "ozaki24")
+    st, est, diag = run_cofem(prob, c.cofem_config(precision, iterations=int(g["config"][3])))
+    prob.op.release()
+    print(f"dense-large {precision}", check_dense(g, st, est, diag, z, step_slack=3))
 
 
 def check_sampled(g, st, est, diag, z, step_slack):

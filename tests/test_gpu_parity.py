@@ -90,6 +90,29 @@ def test_contractions_match_numpy(prec, tol, n, d, q):
     ctx.close()
 
 
+@pytest.mark.parametrize("n,d,q", [(256, 1024, 21), (100, 300, 5), (513, 257, 33), (2048, 4096, 24)])
+def test_ozaki24_contractions_match_arithmetic_model(n, d, q):
+    """COFEM_OZAKI24 (three digit planes of Phi, 24-bit fixed point): the
+    device contraction equals the arithmetic model oracle.ozaki_op(phi,
+    bits=22) -- Phi rounded to 2^-22 of its power-of-two row / column scale,
+    operands to 2^-30 -- up to the dropped low digit pairs (~1e-9), and the
+    exact float64 product to the 24-bit representation error."""
+    rng = np.random.default_rng(n + 3 * d + q)
+    phi = rng.standard_normal((n, d)).astype(np.float32)
+    ctx = _lib.Context(n, d, _lib.OZAKI24)
+    ctx.set_dictionary(phi)
+    model = O.ozaki_op(phi, bits=22)
+    V = rng.standard_normal((d, q))
+    U = rng.standard_normal((n, q))
+    got_f, got_b = ctx.apply(V), ctx.apply_adjoint(U)
+    assert rel(got_f, model.apply(V)) <= 5e-9
+    assert rel(got_b, model.adjoint(U)) <= 5e-9
+    p64 = phi.astype(np.float64)
+    assert 1e-9 < rel(got_f, p64 @ V) <= 5e-6  # really the 24-bit dictionary
+    assert rel(got_b, p64.T @ U) <= 5e-6
+    ctx.close()
+
+
 # ------------------------------------------------------------------- PCG ----
 PCG = golden("pcg_cases.npz")
 
