@@ -359,7 +359,7 @@ def run_ours_conv(args):
         raise SystemExit("2-D DCT dictionaries run on one GPU (their transposes are not sharded)")
     c = S.CONV_CONFIGS[args.config] if is_conv else S.DCT_CONFIGS[args.config]
     prob, z = S.conv_problem(c) if is_conv else S.dct2_problem(c)
-    prec = args.precision if args.precision in ("ozaki", "fp64") else "ozaki"
+    prec = args.precision if args.precision in ("ozaki", "ozaki24", "fp64") else "ozaki"
     dist, device, y_local = None, 0, np.asarray(prob.y)
     if world > 1:
         # time shards: each rank holds its samples; halo send/recv + scalar all-reduces over NCCL
@@ -399,14 +399,23 @@ def run_ours_conv(args):
     q = c.K + 1  # real right-hand sides (the kernels pad to 24 / 32 columns; padding is not algorithmic)
     fwd_avg = tim["fwd_ms"] / max(tim["fwd_launches"], 1)
     bwd_avg = tim["bwd_ms"] / max(tim["bwd_launches"], 1)
+    # the fused convolution step (one GPU, K + 1 <= 32)
+    fused = is_conv and world == 1 and q <= 32 and not os.environ.get("COFEM_CONV_UNFUSED")
     if is_conv:
         d_loc = c.D // world  # per-rank launch (balanced time shards)
         # Phi P band: operand digit planes in (4 B / entry), fp64 V out; Phi^T V
-        # band with the PCG combine fused: planes in, P in, Psi out
+        # band with the PCG combine fused: planes in, P in, Psi out -- or, in
+        # the fused step, planes in, P in, R in and out (no Psi)
         if tim["bwd_ms"] >= tim["fwd_ms"]:
-            dom, avg_ms = ("bwd (Phi^T V band + fused combine: Psi = beta Phi^T V + alpha P; MMA-issue bound, "
-                           "see DESIGN.md)", bwd_avg)
-            alg_bytes = (4.0 + 8.0 + 8.0) * q * d_loc
+            if fused:
+                dom = ("bwd (Phi^T V band + fused residual update: R -= gamma (beta Phi^T V + alpha P); "
+                       "MMA-issue bound, see DESIGN.md)")
+                alg_bytes = (4.0 + 8.0 + 8.0 + 8.0) * q * d_loc
+            else:
+                dom = ("bwd (Phi^T V band + fused combine: Psi = beta Phi^T V + alpha P; MMA-issue bound, "
+                       "see DESIGN.md)")
+                alg_bytes = (4.0 + 8.0 + 8.0) * q * d_loc
+            avg_ms = bwd_avg
         else:
             dom, avg_ms = "fwd (Phi P band)", fwd_avg
             alg_bytes = (4.0 + 8.0) * q * d_loc
@@ -418,14 +427,17 @@ def run_ours_conv(args):
     line = {
         "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "i8 x i8 -> exact i32 (ozaki) / f64" if is_conv else "f64 (FFT passes)",
+        "vs_baseline": None,
+        "dtype": (("i8 x i8 -> exact i32, 24-bit taps (ozaki24) / f64" if prec == "ozaki24" else
+                   "i8 x i8 -> exact i32 (ozaki) / f64") if is_conv else "f64 (FFT passes)"),
         "data": ("synthetic (Bernoulli(0.01) x Exp(1) spikes, exp(-t/20) filter, sigma=0.05)" if is_conv else
                  "synthetic (3% N(0,1) pixels, variable-density 25% DCT mask, sigma=0.01)"),
         "config": {"workload": (f"{args.config}: causal convolution N=D={c.D}, {c.ntaps} taps, K={c.K}, "
                                 f"PCG cap {c.U} tol {c.tol}" if is_conv else
                                 f"{args.config}: 2-D partial DCT n={c.n} (D={c.D}, N={prob.op.n_rows}), K={c.K}, "
                                 f"PCG cap {c.U} tol {c.tol}"), "D": c.D, "K": c.K,
-                   "parallelism": f"time-shard x{world}" if is_conv else "single GPU"},
+                   "parallelism": f"time-shard x{world}" if is_conv else "single GPU",
+                   "precision": prec, "fused_step": fused},
         "pcg_steps_per_sec": pcg_steps / (total_ms / 1e3), "pcg_steps_per_em_iteration": pcg_steps / args.steps,
         "gpu_launches": int(tim["kernel_launches"]), "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -237,7 +237,7 @@ struct cofem_ctx {
   int8_t *probes = nullptr, *probe_store = nullptr;
   int* groups = nullptr;
   int groups_cap = 0;
-  double* scal = nullptr;  // rho0 | rho1 | rho_new | rn2 | pi | bn2 | gam0 | gam1 (ldq each)
+  double* scal = nullptr;  // rho0 | rho1 | rho_new | rn2 | pi | bn2 | gam0 | gam1 | vv | pap (ldq each)
   int* frozen = nullptr;
   double* partials = nullptr;
   unsigned* tickets = nullptr;
@@ -314,6 +314,8 @@ struct cofem_ctx {
   unsigned long long* ptimes = nullptr;
   int ptimes_cap = 0;
   bool persistent_off = false;  // COFEM_NO_PERSISTENT: always the multi-kernel step
+  bool conv_fused_off = false;  // COFEM_CONV_UNFUSED: the convolution step as separate quantise / update launches
+  unsigned long long* fz_max = nullptr;  // fused convolution step: |P| maxima [2][32] (by step parity), |M^-1 R| [32]
   double ph_fwd_ms = 0, ph_bwd_ms = 0, solve_ms = 0;
   int64_t solve_launches = 0;
 
@@ -465,7 +467,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   c->ppart_cap = whole ? 0 : (size_t)max_splits * c->Dp * QCHUNK * ts;
   if (c->vpart_cap) CK(cudaMalloc(&c->vpart, c->vpart_cap));
   if (c->ppart_cap) CK(cudaMalloc(&c->ppart, c->ppart_cap));
-  CK(cudaMalloc(&c->scal, 8 * ldq * sizeof(double)));
+  CK(cudaMalloc(&c->scal, 10 * ldq * sizeof(double)));  // + vv | pap (fused convolution step)
   CK(cudaMalloc(&c->frozen, ldq * sizeof(int)));
   c->nblk_elem = 3 * c->sm_count;
   CK(cudaMalloc(&c->partials, (size_t)c->nblk_elem * 2 * std::max(ldq, QCHUNK) * sizeof(double)));
@@ -820,22 +822,30 @@ int oz_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
 // starting at the tile.  Ends of the sequence arrive as TMA zero fill.
 // launch the band contraction: smem-resident band when it fits, else the
 // streaming MODE_BAND of contract_kernel
-template <int QW>
-int launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
-                double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
+template <int QW, int NPA>
+int launch_band_t(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
+                  double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
   const int grid = std::min(nmb, c->sm_count);
-  const size_t sm = oz::BandCfg<QW>::smem(nk);
+  const size_t sm = oz::BandCfg<QW, NPA>::smem(nk);
   if (sm <= 227 * 1024) {
     static DeviceFlags flags;
-    CKR(smem_attr_once(flags, oz::band_kernel<QW>, 227 * 1024));
-    oz::band_kernel<QW><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(map_a, map_b, nmb, nk, offset, c->hrows, c->opscale,
-                                                                out, rows_real, colmax, st);
+    CKR(smem_attr_once(flags, oz::band_kernel<QW, oz::EPI_PLAIN, NPA>, 227 * 1024));
+    oz::band_kernel<QW, oz::EPI_PLAIN, NPA><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
+        map_a, map_b, nmb, nk, offset, c->hrows, c->opscale, out, rows_real, colmax, st, oz::BandStep{});
   } else {
-    oz::contract_kernel<QW, oz::MODE_BAND><<<grid, oz::NTHREADS, oz::Cfg<QW>::SMEM, c->stream>>>(
+    static DeviceFlags flags;
+    CKR(smem_attr_once(flags, oz::contract_kernel<QW, oz::MODE_BAND, NPA>, oz::Cfg<QW, NPA>::SMEM));
+    oz::contract_kernel<QW, oz::MODE_BAND, NPA><<<grid, oz::NTHREADS, oz::Cfg<QW, NPA>::SMEM, c->stream>>>(
         map_a, map_b, nmb, nmb, nk, 0, offset, c->hrows, c->opscale, out, out_rows, rows_real, colmax, st);
   }
   CK(cudaGetLastError());
   return 0;
+}
+template <int QW>
+int launch_band(cofem_ctx* c, const CUtensorMap& map_a, const CUtensorMap& map_b, int nmb, int nk, int offset,
+                double* out, int64_t out_rows, int64_t rows_real, unsigned long long* colmax, const Status* st) {
+  if (c->npa == 3) return launch_band_t<QW, 3>(c, map_a, map_b, nmb, nk, offset, out, out_rows, rows_real, colmax, st);
+  return launch_band_t<QW, 4>(c, map_a, map_b, nmb, nk, offset, out, out_rows, rows_real, colmax, st);
 }
 
 // V -> operand planes for Phi^T (global column maxima), then the halo: the
@@ -918,26 +928,34 @@ int conv_bwd(cofem_ctx* c, const double* v, int* nsplit_out, const Status* st) {
 // Psi[:, qoff:qoff+QW] = beta Phi^T V + alpha .* P and pi[qoff:...] directly
 // (no U round trip, no k_combine).  Returns 1 when the band does not fit the
 // smem-resident kernel (caller falls back to conv_bwd + k_combine).
-template <int QW>
-int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const Status* st) {
+template <int QW, int NPA>
+int conv_bwd_comb_t(cofem_ctx* c, const double* v, int qoff, double beta, const Status* st) {
   const int nk = oz::BM + c->conv_lpad;
-  const size_t sm = oz::BandCfg<QW>::smem(nk);
+  const size_t sm = oz::BandCfg<QW, NPA>::smem(nk);
   if (sm > 227 * 1024 - 64) return 1;  // (the last-block fold adds a little static smem)
   CKR(oz_init_kernels<QW>());
   CKR(conv_quantize_v<QW>(c, v, st));
   const int nmb = (int)(c->Dp / oz::BM);
   const int grid = std::min(nmb, std::min(c->sm_count, c->nblk_elem));
   static DeviceFlags flags;
-  CKR(smem_attr_once(flags, oz::band_kernel<QW, true>, 227 * 1024 - 64));
+  CKR(smem_attr_once(flags, oz::band_kernel<QW, oz::EPI_COMB, NPA>, 227 * 1024 - 64));
   if (c->time_kernels) {
     cudaEvent_t e0 = next_event(c);
     cudaEventRecord(e0, c->stream);
   }
   Scalars sc = c->sc();
   CK(cudaGetLastError());
-  oz::band_kernel<QW, true><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
+  oz::BandStep bs{};
+  bs.P = (const double*)c->P + qoff;
+  bs.ld = c->ldq;
+  bs.alpha = c->alpha;
+  bs.beta = beta;
+  bs.out0 = sc.pi + qoff;
+  bs.partials = sc.partials;
+  bs.ticket = sc.ticket + 1;
+  oz::band_kernel<QW, oz::EPI_COMB, NPA><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
       c->map_band_adj, c->map_v[QW / 8], nmb, nk, 0, c->hrows, c->opscale, (double*)c->Psi + qoff, c->D, nullptr, st,
-      (const double*)c->P + qoff, c->ldq, c->alpha, beta, sc.pi + qoff, sc.partials, sc.ticket + 1);
+      bs);
   if (c->time_kernels) {
     cudaEvent_t e1 = next_event(c);
     cudaEventRecord(e1, c->stream);
@@ -947,6 +965,11 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
   c->bwd_launches++;
   CK(cudaGetLastError());
   return 0;
+}
+
+template <int QW>
+int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const Status* st) {
+  return c->npa == 3 ? conv_bwd_comb_t<QW, 3>(c, v, qoff, beta, st) : conv_bwd_comb_t<QW, 4>(c, v, qoff, beta, st);
 }
 
 // ---- convolution, float64 FFT path (dct.cuh k_conv_fft_pass) ----------------
@@ -1231,6 +1254,129 @@ int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
   return 0;
 }
 
+// ---- fused convolution PCG step ---------------------------------------------
+// One GPU, one column chunk (K + 1 <= 32), one preconditioner group, the
+// smem-resident band: per PCG step four launches instead of six and no Psi
+// block:
+//   K1 band Phi P (EPI_FWD): V, column maxima of |V|, vv = ||V||^2
+//   K2 k_quantize(V) (the exact maxima from K1; zeroes the |M^-1 R| maxima)
+//   K3 band Phi^T V (EPI_UPD): gamma = rho / (beta vv + pap), R -= gamma Psi
+//      on the fly, rho_new, ||R||^2, maxima of |M^-1 R|
+//   K4 k_direction_q: stopping test, X, P(u+1) and its digit planes against
+//      the bound scale, maxima of |P(u+1)|, pap = <P(u+1), alpha P(u+1)>
+bool conv_fused_eligible(cofem_ctx* c, int ngroups) {
+  if (!(c->kind == 1 && c->prec == COFEM_OZAKI && !c->conv_fft && c->nranks <= 1 && c->ldq <= QCHUNK &&
+        ngroups == 1 && !c->conv_fused_off && c->fz_max))
+    return false;
+  const int nk = oz::BM + c->conv_lpad;
+  return oz::BandCfg<32, 4>::smem(nk) <= 227 * 1024 - 64 - 512;
+}
+
+template <int QW, int NPA>
+int conv_fused_launch(cofem_ctx* c, int which, int step, double beta, int q_real, const cofem_cg_config* cg,
+                      Status* mirror) {
+  const int slot = QW / 8;
+  const int nk = oz::BM + c->conv_lpad;
+  const int nmb = (int)(c->Np / oz::BM);
+  const size_t sm = oz::BandCfg<QW, NPA>::smem(nk);
+  const int ldq = c->ldq;
+  Scalars sc = c->sc();
+  double* vv = c->scal + 8 * ldq;
+  double* pap = c->scal + 9 * ldq;
+  unsigned long long* pmax[2] = {c->fz_max, c->fz_max + 32};
+  unsigned long long* wmax = c->fz_max + 64;
+  if (which == 0 || which == 2) {  // the band launches
+    static DeviceFlags f1, f3;
+    CKR(smem_attr_once(f1, oz::band_kernel<QW, oz::EPI_FWD, NPA>, 227 * 1024 - 64));
+    CKR(smem_attr_once(f3, oz::band_kernel<QW, oz::EPI_UPD, NPA>, 227 * 1024 - 64));
+    const int grid = std::min(nmb, std::min(c->sm_count, c->nblk_elem));
+    oz::BandStep bs{};
+    bs.ld = ldq;
+    bs.q_real = q_real;
+    bs.printed = cg->printed_recursion;
+    bs.alpha = c->alpha;
+    bs.minv = c->minv;
+    bs.ngroups = 1;
+    bs.beta = beta;
+    bs.partials = sc.partials;
+    cudaEvent_t e0 = nullptr;
+    if (c->time_kernels) {
+      e0 = next_event(c);
+      cudaEventRecord(e0, c->stream);
+    }
+    if (which == 0) {
+      if (!c->map_p_ok[slot]) {
+        CKR(encode_u8_kblocked(&c->map_p[slot], c->pq, c->Dp, QW, QW));
+        c->map_p_ok[slot] = true;
+      }
+      bs.out0 = vv;
+      bs.ticket = sc.ticket + 3;
+      oz::band_kernel<QW, oz::EPI_FWD, NPA><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
+          c->map_band_fwd, c->map_p[slot], nmb, nk, -c->conv_lpad, c->hrows, c->opscale, (double*)c->V, c->N,
+          c->vcolmax, c->st, bs);
+      c->fwd_launches++;
+    } else {
+      if (!c->map_v_ok[slot]) {
+        CKR(encode_u8_kblocked(&c->map_v[slot], c->vq, c->Np, QW, QW));
+        c->map_v_ok[slot] = true;
+      }
+      bs.P = (const double*)c->P;
+      bs.R = (double*)c->R;
+      bs.rho = sc.rho[step & 1];
+      bs.vv = vv;
+      bs.pap = pap;
+      bs.gam_out = sc.gam[step & 1];
+      bs.frozen = sc.frozen;
+      bs.wmax = wmax;
+      bs.reset = pmax[(step + 1) & 1];
+      bs.out0 = sc.rho_new;
+      bs.out1 = sc.rn2;
+      bs.ticket = sc.ticket + 4;
+      oz::band_kernel<QW, oz::EPI_UPD, NPA><<<grid, oz::BAND_NTHREADS, sm, c->stream>>>(
+          c->map_band_adj, c->map_v[slot], nmb, nk, 0, c->hrows, c->opscale, nullptr, c->D, nullptr, c->st, bs);
+      c->bwd_launches++;
+    }
+    if (c->time_kernels) {
+      cudaEvent_t e1 = next_event(c);
+      cudaEventRecord(e1, c->stream);
+      c->timed.push_back({which == 0 ? 0 : 1, c->evnext - 2});
+    }
+    (void)e0;
+  } else if (which == 1) {  // K2
+    CKR((oz_quantize<double, QW>(c, (const double*)c->V, QW, 0, c->N, c->Np, nullptr, c->vq, c->vcolmax, true, wmax,
+                                 c->st)));
+    return 0;
+  } else {  // K4 (step 0: the first direction; P in place, no X)
+    const int64_t ngrp = c->Dp / 128;
+    const unsigned grid = (unsigned)std::min<int64_t>(ngrp, 2 * c->sm_count);  // 2 blocks / SM resident
+    const bool first = step == 0;
+    oz::k_direction_q<QW><<<grid, 256, 0, c->stream>>>(
+        c->Dp, q_real, step, cg->max_steps, cg->tolerance, cg->printed_recursion, (double*)c->P, (const double*)c->R,
+        c->minv, c->alpha, sc, pmax[step & 1], pmax[(step + 1) & 1], wmax, c->vcolmax, c->opscale, c->pq, pap,
+        sc.ticket + 5, c->st, mirror, first ? nullptr : (double*)c->X, first ? nullptr : (double*)c->P2,
+        first ? nullptr : (const double*)c->P2);
+  }
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int conv_fused(cofem_ctx* c, int which, int step, double beta, int q_real, const cofem_cg_config* cg,
+               Status* mirror = nullptr) {
+  const bool p3 = c->npa == 3;
+  switch (c->ldq) {
+    case 8: return p3 ? conv_fused_launch<8, 3>(c, which, step, beta, q_real, cg, mirror)
+                      : conv_fused_launch<8, 4>(c, which, step, beta, q_real, cg, mirror);
+    case 16: return p3 ? conv_fused_launch<16, 3>(c, which, step, beta, q_real, cg, mirror)
+                       : conv_fused_launch<16, 4>(c, which, step, beta, q_real, cg, mirror);
+    case 24: return p3 ? conv_fused_launch<24, 3>(c, which, step, beta, q_real, cg, mirror)
+                       : conv_fused_launch<24, 4>(c, which, step, beta, q_real, cg, mirror);
+    case 32: return p3 ? conv_fused_launch<32, 3>(c, which, step, beta, q_real, cg, mirror)
+                       : conv_fused_launch<32, 4>(c, which, step, beta, q_real, cg, mirror);
+  }
+  return fail(COFEM_EINVAL, "fused convolution step: unsupported column count");
+}
+
 // ---- one-launch PCG solve (persistent.cuh) --------------------------------
 // dense dictionary, int8 path, one GPU, one column chunk, one preconditioner group
 bool persistent_eligible(cofem_ctx* c, int ngroups) {
@@ -1442,10 +1588,22 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     CK(cudaMemsetAsync(c->colmax, 0, ldq * sizeof(unsigned long long), c->stream));
   }
   unsigned long long* pmax = (oz && c->kind != 2) ? c->colmax : nullptr;
-  k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
-      c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
-      ngroups, groups, sc, c->colscale, pmax, c->st);
-  c->launches++;
+  const bool fused = std::is_same<T, double>::value && conv_fused_eligible(c, ngroups);
+  if (fused) {
+    // first direction P(1) = M^-1 B with its planes: the bound is max |M^-1 B| (max |P(0)| = 0)
+    CK(cudaMemsetAsync(c->fz_max, 0, 4 * 32 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->vcolmax, 0, QCHUNK * sizeof(unsigned long long), c->stream));
+    const int cbs = ldq * (256 / ldq);
+    oz::k_colmax<double><<<2 * c->sm_count, cbs, cbs * sizeof(double), c->stream>>>(
+        c->D, ldq, 0, ldq, (const double*)c->R, cg->printed_recursion ? nullptr : c->minv, c->fz_max + 64, c->st);
+    c->launches++;
+    CKR(conv_fused(c, 3, 0, beta, q_real, cg));
+  } else {
+    k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+        c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
+        ngroups, groups, sc, c->colscale, pmax, c->st);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   c->p_colmax_valid = oz;
 
@@ -1457,6 +1615,16 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
       const int slot = (u - LAG) % LAG;
       CK(cudaEventSynchronize(c->ev[slot]));
       if (c->h_st[slot].done) break;
+    }
+    if (fused) {
+      const int slot = u % LAG;
+      CKR(conv_fused(c, 0, u, beta, q_real, cg));
+      CKR(conv_fused(c, 1, u, beta, q_real, cg));
+      CKR(conv_fused(c, 2, u, beta, q_real, cg));
+      CKR(conv_fused(c, 3, u, beta, q_real, cg, c->d_hst + slot));
+      std::swap(c->P, c->P2);
+      CK(cudaEventRecord(c->ev[slot], c->stream));
+      continue;
     }
     CKR(system_apply_dev<T>(c, beta, c->st));
     CKR(allreduce(c, sc.pi, ldq, ncclFloat64));
@@ -2124,9 +2292,9 @@ int cofem_create(cofem_ctx** out, int device, int64_t n_rows, int64_t n_cols, in
 
 namespace {
 // signed base-256 digits of round(x), host side (same decomposition as oz::digits4)
-void host_digits4(double x, int8_t d[4]) {
+void host_digits(double x, int8_t* d, int n) {
   long long v = llrint(x);
-  for (int a = 3; a >= 0; --a) {
+  for (int a = n - 1; a >= 0; --a) {
     const int8_t lo = (int8_t)(v & 0xFF);
     d[a] = lo;
     v = (v - lo) >> 8;
@@ -2144,7 +2312,8 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   if (!out || !taps) return fail(COFEM_EINVAL, "null argument");
   *out = nullptr;
   if (dim < 1 || ntaps < 1 || ntaps > dim) return fail(COFEM_EINVAL, "need 1 <= ntaps <= dim");
-  if (precision == COFEM_OZAKI24) precision = COFEM_OZAKI;  // the band keeps the 32-bit taps
+  const int npa = precision == COFEM_OZAKI24 ? 3 : 4;  // 24-bit taps: three band digit planes
+  if (precision == COFEM_OZAKI24) precision = COFEM_OZAKI;
   if (precision != COFEM_OZAKI && precision != COFEM_FP64)
     return fail(COFEM_EINVAL, "convolution dictionaries run in OZAKI (int8 band) or FP64 (FFT) precision");
   if (precision == COFEM_FP64 && ntaps > CONV_FFT_MAX_TAPS)
@@ -2160,6 +2329,7 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   c->kind = 1;
   c->device = device;
   c->prec = precision;
+  c->npa = npa;
   c->N = c->D = dim;
   c->Np = c->Dp = round_up(dim, PAD);
   c->global_cols = dim;
@@ -2239,34 +2409,38 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
       cudaMalloc(&c->vq, (size_t)4 * QCHUNK * c->Np + lpb) != cudaSuccess ||
       cudaMalloc(&c->opscale, QCHUNK * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)) != cudaSuccess)
+      cudaMalloc(&c->vcolmax, QCHUNK * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->fz_max, 4 * 32 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "operand buffers"));
+  c->conv_fused_off = getenv("COFEM_CONV_UNFUSED") != nullptr;
   cudaMemsetAsync(c->pq_base, 0, (size_t)4 * QCHUNK * c->Dp + lpb, c->stream);
   cudaMemsetAsync(c->vq, 0, (size_t)4 * QCHUNK * c->Np + lpb, c->stream);
   c->pq = c->pq_base + lpb;
-  // band digit planes: lower band (Phi) and upper band (Phi^T), one scale 2^e >= max |h|
+  // band digit planes: lower band (Phi) and upper band (Phi^T), one scale 2^e >= max |h|;
+  // npa planes of round(h / hs * 2^(8 npa - 2)) (the epilogue constant is the same for 3 and 4)
   const double hs = host_pow2_ceil(hmax);
+  const double tsc = std::ldexp(1.0, 8 * npa - 2);
   const int nk = oz::BM + c->conv_lpad;
-  std::vector<int8_t> bf((size_t)4 * oz::BM * nk, 0), ba((size_t)4 * oz::BM * nk, 0);
+  std::vector<int8_t> bf((size_t)npa * oz::BM * nk, 0), ba((size_t)npa * oz::BM * nk, 0);
   for (int r = 0; r < oz::BM; ++r)
     for (int col = 0; col < nk; ++col) {
       const int mf = r + c->conv_lpad - col, ma = col - r;
       int8_t d[4];
       if (mf >= 0 && mf < ntaps) {
-        host_digits4(taps[mf] / hs * 1073741824.0, d);
-        for (int a = 0; a < 4; ++a) bf[((size_t)a * oz::BM + r) * nk + col] = d[a];
+        host_digits(taps[mf] / hs * tsc, d, npa);
+        for (int a = 0; a < npa; ++a) bf[((size_t)a * oz::BM + r) * nk + col] = d[a];
       }
       if (ma >= 0 && ma < ntaps) {
-        host_digits4(taps[ma] / hs * 1073741824.0, d);
-        for (int a = 0; a < 4; ++a) ba[((size_t)a * oz::BM + r) * nk + col] = d[a];
+        host_digits(taps[ma] / hs * tsc, d, npa);
+        for (int a = 0; a < npa; ++a) ba[((size_t)a * oz::BM + r) * nk + col] = d[a];
       }
     }
   if (cudaMalloc(&c->band_fwd, bf.size()) != cudaSuccess || cudaMalloc(&c->band_adj, ba.size()) != cudaSuccess)
     return bail(fail(COFEM_ENOMEM, "band planes"));
   h2d_sync(c, c->band_fwd, bf.data(), bf.size());
   h2d_sync(c, c->band_adj, ba.data(), ba.size());
-  int rc = encode_u8_3d(&c->map_band_fwd, c->band_fwd, nk, oz::BM, 4, oz::KT, oz::BM, 4);
-  if (!rc) rc = encode_u8_3d(&c->map_band_adj, c->band_adj, nk, oz::BM, 4, oz::KT, oz::BM, 4);
+  int rc = encode_u8_3d(&c->map_band_fwd, c->band_fwd, nk, oz::BM, npa, oz::KT, oz::BM, npa);
+  if (!rc) rc = encode_u8_3d(&c->map_band_adj, c->band_adj, nk, oz::BM, npa, oz::KT, oz::BM, npa);
   if (rc) return bail(rc);
   // scales: output rows carry hs; operands are not pre-scaled (ones)
   std::vector<double> hv(c->Dp, hs), ones(c->Dp, 1.0);
@@ -2374,7 +2548,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

@@ -236,126 +236,6 @@ __device__ __forceinline__ void epilogue_row(uint32_t tset_lane, double scale, c
   }
 }
 
-// Epilogue with the PCG combine fused in (the conv Phi^T V launch): instead of
-// U = Phi^T V the row writes Psi = beta U + alpha_j P_j (k_combine's formula)
-// and accumulates p * psi per column for pi = <P, Psi>.
-// P values of the row's column groups (group g of this half at pv[8 g ..]),
-// loaded before the accumulator wait
-template <int QW>
-__host__ __device__ constexpr int comb_pv() { return (QW + 15) / 16 * 8; }
-template <int QW, int HALF>
-__device__ __forceinline__ void comb_prefetch(const double* __restrict__ prow, double (&pv)[comb_pv<QW>()]) {
-#pragma unroll
-  for (int q0 = HALF * 8, g = 0; q0 < QW; q0 += 16, ++g)
-#pragma unroll
-    for (int t = 0; t < 8; t += 4) ld_v4(prow + q0 + t, pv[8 * g + t], pv[8 * g + t + 1], pv[8 * g + t + 2], pv[8 * g + t + 3]);
-}
-
-template <int QW, int HALF>
-__device__ __forceinline__ void epilogue_row_comb(uint32_t tset_lane, double scale, const double* __restrict__ op_scale,
-                                                  double* o, const double (&pv)[comb_pv<QW>()], double alpha_j,
-                                                  double beta, double (&pacc)[QW]) {
-#pragma unroll
-  for (int q0 = HALF * 8, g = 0; q0 < QW; q0 += 16, ++g) {
-    double f[8], p[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      f[t] = scale * __ldg(op_scale + q0 + t);
-      p[t] = pv[8 * g + t];
-    }
-    uint32_t r[5][8];
-#pragma unroll
-    for (int sb = 0; sb < 5; ++sb)
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]),
-                     "=r"(r[sb][5]), "=r"(r[sb][6]), "=r"(r[sb][7])
-                   : "r"(tset_lane + sb * QW + q0));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-    for (int sb = 0; sb < 5; ++sb)
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                       tset_lane + sb * QW + q0),
-                   "r"(0));
-    double v[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
-                           ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
-      const double u = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * f[t];
-      v[t] = beta * u + alpha_j * p[t];
-      pacc[q0 + t] += p[t] * v[t];
-    }
-    st_v4(o + q0, v[0], v[1], v[2], v[3]);
-    st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
-  }
-}
-
-// band_kernel epilogue: 16 warps, warp (quarter, group) owns TMEM lane
-// quarter `quarter` (32 rows) and the 8 columns [q0, q0 + 8) -- twice the
-// warps of the contraction kernels' epilogue, so TMEM-load / global-memory
-// latency of one warp hides behind the others.
-template <int QW, bool TRACK>
-__device__ __forceinline__ void epi8(uint32_t tl, int q0, double scale, const double* __restrict__ op_scale,
-                                     double* o, unsigned long long (&cm)[8]) {
-  uint32_t r[5][8];
-#pragma unroll
-  for (int sb = 0; sb < 5; ++sb)
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]), "=r"(r[sb][5]),
-                   "=r"(r[sb][6]), "=r"(r[sb][7])
-                 : "r"(tl + sb * QW + q0));
-  asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-  for (int sb = 0; sb < 5; ++sb)
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
-                 "r"(0));
-  double v[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
-                         ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
-    v[t] = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * (scale * __ldg(op_scale + q0 + t));
-  }
-  st_v4(o + q0, v[0], v[1], v[2], v[3]);
-  st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
-  if (TRACK) {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const unsigned long long m = (unsigned long long)__double_as_longlong(v[t]) & 0x7fffffffffffffffull;
-      cm[t] = m > cm[t] ? m : cm[t];
-    }
-  }
-}
-
-template <int QW>
-__device__ __forceinline__ void epi8_comb(uint32_t tl, int q0, double scale, const double* __restrict__ op_scale,
-                                          double* o, const double (&p)[8], double alpha_j, double beta,
-                                          double (&pacc)[8]) {
-  uint32_t r[5][8];
-#pragma unroll
-  for (int sb = 0; sb < 5; ++sb)
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]), "=r"(r[sb][5]),
-                   "=r"(r[sb][6]), "=r"(r[sb][7])
-                 : "r"(tl + sb * QW + q0));
-  asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-  for (int sb = 0; sb < 5; ++sb)
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
-                 "r"(0));
-  double v[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
-                         ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
-    const double u = fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo) * (scale * __ldg(op_scale + q0 + t));
-    v[t] = beta * u + alpha_j * p[t];
-    pacc[t] += p[t] * v[t];
-  }
-  st_v4(o + q0, v[0], v[1], v[2], v[3]);
-  st_v4(o + q0 + 4, v[4], v[5], v[6], v[7]);
-}
-
 // the calling epilogue warp's share of one tile row (column groups of parity half)
 template <int QW>
 __device__ __forceinline__ void epilogue_part(int half, bool track, uint32_t tset_lane, double scale,
@@ -551,14 +431,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // Band-resident Toeplitz contraction (convolution dictionaries).  The whole
-// 128 x nk band (4 digit planes, nk = 128 + lpad bytes per row) is loaded into
-// shared memory ONCE per CTA; the TMA ring then carries only the operand
+// 128 x nk band (NPA digit planes, nk = 128 + lpad bytes per row) is loaded
+// into shared memory ONCE per CTA; the TMA ring then carries only the operand
 // windows (4 QW x 64 B per stage), so the L2 -> SM traffic per output tile is
-// the window alone.  Same significance-aligned, double-buffered accumulation
-// and epilogue as contract_kernel.
+// the window alone.  Same significance-aligned accumulation as
+// contract_kernel (NPA = 3: the 24-bit taps of COFEM_OZAKI24, one MMA per
+// k-step less -- the kernel is MMA-issue bound).
 constexpr int BSTAGES = 4;
 // band_kernel accumulator sets: 5 significance blocks of QW <= 32 columns
-// (160 TMEM columns), three sets in the 512-column allocation so the MMA
+// (160 TMEM columns); three sets in the 512-column allocation, so the MMA
 // issuer can run two tiles ahead of a slow epilogue
 #ifndef BAND_SETS_OVERRIDE
 constexpr int BAND_SETS = 3;
@@ -568,38 +449,152 @@ constexpr int BAND_SETS = BAND_SETS_OVERRIDE;
 constexpr int BAND_SET_COLS = 160;
 constexpr int BAND_EPI_WARPS = 16;                      // 4 lane quarters x 4 column groups of 8
 constexpr int BAND_NTHREADS = 64 + 32 * BAND_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, warps 2..17 epilogue
-template <int QW>
+template <int QW, int NPA = 4>
 struct BandCfg {
   static constexpr int B_STAGE = 4 * QW * KT;
-  static size_t smem(int nk) { return (size_t)nk * 4 * BM + (size_t)BSTAGES * B_STAGE + 1024 + 1280; }
+  static size_t smem(int nk) { return (size_t)nk * NPA * BM + (size_t)BSTAGES * B_STAGE + 1024 + 1280; }
 };
 
-// COMB (the Phi^T V launch of a PCG step): out = Psi = beta Phi^T V + alpha .* P
-// (P / out row stride p_ld, column offset of the chunk already applied) and
-// pi_out[q] = <P_q, Psi_q> through fixed-order block partials + last-block fold.
-template <int QW, bool COMB = false>
+// band_kernel epilogues
+//   EPI_PLAIN: out = Phi(.) op, optional column maxima of |out|
+//   EPI_COMB : the Phi^T V launch of a PCG step: out = Psi = beta Phi^T V +
+//              alpha .* P and pi = <P, Psi> (k_combine fused)
+//   EPI_FWD  : the Phi P launch of the fused convolution step: out = V, the
+//              column maxima of |V| and vv = ||V||^2 per column (block
+//              partials + last-block fold), so pi = beta ||V||^2 + <P, alpha P>
+//              is known before Phi^T V runs
+//   EPI_UPD  : the Phi^T V launch of the fused convolution step: no Psi block
+//              and no k_update -- each row applies R -= gamma (beta Phi^T V +
+//              alpha .* P) (gamma = rho / pi, pi from EPI_FWD's vv and the
+//              direction kernel's <P, alpha P>) and accumulates <R, M^-1 R>,
+//              ||R||^2 (block partials + last-block fold) and the column
+//              maxima of |M^-1 R| (the next direction's quantisation bound)
+enum { EPI_PLAIN = 0, EPI_COMB = 1, EPI_FWD = 2, EPI_UPD = 3 };
+
+// extra arguments of the fused-step epilogues
+struct BandStep {
+  const double* P;         // [rows][ld] current direction (EPI_COMB / EPI_UPD)
+  double* R;               // [rows][ld] residual, updated in place (EPI_UPD)
+  int ld;
+  int q_real;
+  int printed;             // printed recursion: the bound tracks |R| instead of |M^-1 R|
+  const double* alpha;     // [rows]
+  const double* minv;      // [rows * ngroups]
+  const int* groups;       // column -> preconditioner group (nullptr: one group)
+  int ngroups;
+  double beta;
+  const double* rho;       // rho of P(u) (EPI_UPD)
+  const double* vv;        // ||Phi P||^2 (EPI_UPD)
+  const double* pap;       // <P, alpha P> (EPI_UPD)
+  double* gam_out;         // gamma per column, for the direction kernel's X update (EPI_UPD)
+  int* frozen;             // breakdown flags (EPI_UPD)
+  unsigned long long* wmax;   // column maxima of |M^-1 R| (EPI_UPD, atomicMax)
+  unsigned long long* reset;  // zeroed by block 0 (the next direction's |P| maxima)
+  double* out0;            // fold outputs: pi (COMB) / vv (FWD) / rho_new (UPD)
+  double* out1;            // rn2 (UPD)
+  double* partials;        // [grid][2][QW]
+  unsigned* ticket;
+};
+
+template <int QW>
+__device__ __forceinline__ void tmem_rows4(uint32_t tl, int q0, uint32_t (&r)[5][4]) {
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3])
+                 : "r"(tl + sb * QW + q0));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0), "r"(0));
+}
+template <int NC>
+__device__ __forceinline__ double combine5n(const uint32_t (&r)[5][NC], int t) {
+  const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                       ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+  return fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo);
+}
+template <int QW>
+__device__ __forceinline__ void tmem_rows8(uint32_t tl, int q0, uint32_t (&r)[5][8]) {
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[sb][0]), "=r"(r[sb][1]), "=r"(r[sb][2]), "=r"(r[sb][3]), "=r"(r[sb][4]), "=r"(r[sb][5]),
+                   "=r"(r[sb][6]), "=r"(r[sb][7])
+                 : "r"(tl + sb * QW + q0));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+  for (int sb = 0; sb < 5; ++sb)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tl + sb * QW + q0),
+                 "r"(0));
+}
+__device__ __forceinline__ double combine5(const uint32_t (&r)[5][8], int t) {
+  const long long lo = ((long long)(int32_t)r[1][t] << 24) + ((long long)(int32_t)r[2][t] << 16) +
+                       ((long long)(int32_t)r[3][t] << 8) + (long long)(int32_t)r[4][t];
+  return fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo);
+}
+__device__ __forceinline__ void ld_v4_rw(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+// L2 prefetch of a contiguous global range (bulk, no registers / smem)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Transposed warp reduction of 8 per-lane values (8 columns): 9 shuffles
+// instead of 40; the result for column c = 4 b4 + 2 b3 + b2 (bits of the
+// lane index) ends up in the four lanes of that group.  Fixed pattern, so
+// deterministic.
+template <bool MAX>
+__device__ __forceinline__ double treduce8(const double (&v)[8]) {
+  const int l = threadIdx.x & 31;
+  const bool b4 = l & 16, b3 = l & 8, b2 = l & 4;
+  auto op = [](double a, double b) { return MAX ? fmax(a, b) : a + b; };
+  double w[4], x[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b4 ? v[i] : v[i + 4], keep = b4 ? v[i + 4] : v[i];
+    w[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b3 ? w[i] : w[i + 2], keep = b3 ? w[i + 2] : w[i];
+    x[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+  }
+  double y = op(b2 ? x[1] : x[0], __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4));
+  y = op(y, __shfl_xor_sync(0xffffffffu, y, 2));
+  return op(y, __shfl_xor_sync(0xffffffffu, y, 1));
+}
+__device__ __forceinline__ int treduce8_col() {
+  const int l = threadIdx.x & 31;
+  return ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1);
+}
+
+template <int QW, int EPI = EPI_PLAIN, int NPA = 4>
 __global__ void __launch_bounds__(BAND_NTHREADS, 1)
     band_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 int n_mblocks, int nk, int band_offset, const double* __restrict__ row_scale,
                 const double* __restrict__ op_scale, double* __restrict__ out, int64_t rows_real,
                 unsigned long long* __restrict__ out_colmax, const Status* __restrict__ st,
-                const double* __restrict__ Pc = nullptr, int p_ld = 0, const double* __restrict__ alpha = nullptr,
-                double beta = 0.0, double* pi_out = nullptr, double* partials = nullptr, unsigned* ticket = nullptr) {
-  using C = Cfg<QW>;
-  using BC = BandCfg<QW>;
+                const __grid_constant__ BandStep bs) {
+  using BC = BandCfg<QW, NPA>;
+  constexpr int A_ST = NPA * BM * KT;
   if (st && st->done) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int nst = nk / KT;                          // band stages
-  unsigned char* band = sm;                         // [nst][4 planes][128][64]
-  unsigned char* ring = sm + (size_t)nst * A_STAGE; // [BSTAGES][4 QW][64]
+  unsigned char* band = sm;                         // [nst][NPA planes][128][64]
+  unsigned char* ring = sm + (size_t)nst * A_ST;    // [BSTAGES][4 QW][64]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + BSTAGES * BC::B_STAGE);
   uint64_t* empty = full + BSTAGES;
   uint64_t* band_full = empty + BSTAGES;
   uint64_t* tfull = band_full + 1;  // [BAND_SETS]
   uint64_t* tempty = tfull + BAND_SETS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + BAND_SETS);
-  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);  // [BAND_EPI_WARPS][QW], after the last tile
+  double* gam_s = reinterpret_cast<double*>(tempty + BAND_SETS + 1);  // [QW] gamma (EPI_UPD)
+  // after the last tile: [BAND_EPI_WARPS][2][QW] per-warp folds (the ring is idle by then)
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ring);
+  double* fold = reinterpret_cast<double*>(ring) + BAND_EPI_WARPS * QW;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -616,7 +611,17 @@ __global__ void __launch_bounds__(BAND_NTHREADS, 1)
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
   }
-  (void)0;
+  if (EPI == EPI_UPD && threadIdx.x >= 64 && threadIdx.x < 64 + QW) {
+    const int q = threadIdx.x - 64;
+    const double pi = bs.beta * bs.vv[q] + bs.pap[q];
+    const double g = pi != 0.0 ? bs.rho[q] / pi : 0.0;  // safe_ratio
+    gam_s[q] = g;
+    if (blockIdx.x == 0) {
+      bs.gam_out[q] = g;
+      if (q < bs.q_real && pi == 0.0) bs.frozen[q] = 1;
+      bs.reset[q] = 0ull;
+    }
+  }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(512));
@@ -634,12 +639,18 @@ __global__ void __launch_bounds__(BAND_NTHREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       // band once, then the operand windows of every tile
-      mbar_expect_tx(band_full, (uint32_t)(nst * A_STAGE));
-      for (int s = 0; s < nst; ++s) tma_load_3d(band + (size_t)s * A_STAGE, &map_a, band_full, s * KT, 0, 0);
+      mbar_expect_tx(band_full, (uint32_t)(nst * A_ST));
+      for (int s = 0; s < nst; ++s) tma_load_3d(band + (size_t)s * A_ST, &map_a, band_full, s * KT, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x) {
         const int k0 = mb * BM + band_offset;
+        if (EPI == EPI_COMB || EPI == EPI_UPD) {
+          // the tile's P (and R) rows are one contiguous block: pull them into L2
+          // now, a tile or more before the epilogue loads them
+          prefetch_l2(bs.P + (int64_t)mb * BM * bs.ld, (uint32_t)(BM * bs.ld * sizeof(double)));
+          if (EPI == EPI_UPD) prefetch_l2(bs.R + (int64_t)mb * BM * bs.ld, (uint32_t)(BM * bs.ld * sizeof(double)));
+        }
         for (int s = 0; s < nst; ++s) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (OZ_VARIANT >= 4) {
@@ -671,8 +682,8 @@ __global__ void __launch_bounds__(BAND_NTHREADS, 1)
           mbar_wait(&full[stage], phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (OZ_VARIANT != 1)
-            issue_stage<QW, false>(smem_u32(band + (size_t)s * A_STAGE), smem_u32(ring + stage * BC::B_STAGE), tset,
-                                   idesc0);
+            issue_stage<QW, false, NPA>(smem_u32(band + (size_t)s * A_ST), smem_u32(ring + stage * BC::B_STAGE),
+                                        tset, idesc0);
           mma_commit(&empty[stage]);
           if (++stage == BSTAGES) {
             stage = 0;
@@ -688,85 +699,153 @@ __global__ void __launch_bounds__(BAND_NTHREADS, 1)
     const bool active = q0 < QW;  // QW < 32: the surplus column groups only keep the barrier phases
     const int row_in_tile = quarter * 32 + lane;
     unsigned long long cm[8];
-    double pacc[8];
+    double acc0[8], acc1[8];
+    // EPI_UPD: running per-column values of this lane's column treduce8_col()
+    // (a NaN residual stops the solve through ||R||^2 before the bound is used)
+    double acc_rho = 0.0, acc_rn = 0.0, acc_w = 0.0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       cm[t] = 0ull;
-      pacc[t] = 0.0;
+      acc0[t] = 0.0;
+      acc1[t] = 0.0;
     }
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
       const int buf = it % BAND_SETS;
       const int64_t row = (int64_t)mb * BM + row_in_tile;
       const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
-      double pv[8];
-      double alpha_j = 0.0;
-      if (COMB && active) {
-        alpha_j = alpha[row];
-        const double* prow = Pc + row * p_ld + q0;
+      double pv[8], rr[8];
+      double alpha_j = 0.0, mv = 0.0;
+      if ((EPI == EPI_COMB || EPI == EPI_UPD) && active) {
+        alpha_j = bs.alpha[row];
+        const double* prow = bs.P + row * bs.ld + q0;
         ld_v4(prow, pv[0], pv[1], pv[2], pv[3]);
         ld_v4(prow + 4, pv[4], pv[5], pv[6], pv[7]);
+      }
+      if (EPI == EPI_UPD && active) {
+        mv = bs.minv[row * bs.ngroups];
+        const double* rrow = bs.R + row * bs.ld + q0;
+        ld_v4_rw(rrow, rr[0], rr[1], rr[2], rr[3]);
+        ld_v4_rw(rrow + 4, rr[4], rr[5], rr[6], rr[7]);
       }
       mbar_wait(&tfull[buf], (it / BAND_SETS) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tl = tmem + buf * BAND_SET_COLS + ((uint32_t)(quarter * 32) << 16);
-      if (active && OZ_VARIANT != 3 && OZ_VARIANT != 4) {
-        if (COMB)
-          epi8_comb<QW>(tl, q0, scale, op_scale, out + row * p_ld, pv, alpha_j, beta, pacc);
-        else if (out_colmax)
-          epi8<QW, true>(tl, q0, scale, op_scale, out + row * QW, cm);
-        else
-          epi8<QW, false>(tl, q0, scale, op_scale, out + row * QW, cm);
+      if (EPI == EPI_UPD && active && OZ_VARIANT != 3 && OZ_VARIANT != 4) {
+        // two passes of 4 columns (register budget: 18 warps -> 96 per thread)
+        double wm[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t r4[5][4];
+          tmem_rows4<QW>(tl, q0 + 4 * h, r4);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int q = q0 + 4 * h + t;
+            const double u = combine5n<4>(r4, t) * (scale * __ldg(op_scale + q));
+            const double psi = bs.beta * u + alpha_j * pv[4 * h + t];
+            const double rn = rr[4 * h + t] - psi * gam_s[q];
+            rr[4 * h + t] = rn;
+            wm[4 * h + t] = fabs(bs.printed ? rn : (q < bs.q_real ? rn * mv : 0.0));
+          }
+        }
+        double* rrow = bs.R + row * bs.ld + q0;
+        st_v4(rrow, rr[0], rr[1], rr[2], rr[3]);
+        st_v4(rrow + 4, rr[4], rr[5], rr[6], rr[7]);
+        // per-tile column reductions, transposed across the warp; one lane per
+        // 4 keeps the running value of its column (c = treduce8_col())
+        const double m8 = treduce8<true>(wm);
+        acc_w = fmax(acc_w, m8);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) rr[t] = rr[t] * rr[t];
+        acc_rn += treduce8<false>(rr);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) rr[t] = (q0 + t < bs.q_real) ? rr[t] * mv : 0.0;
+        acc_rho += treduce8<false>(rr);
+      } else if (active && OZ_VARIANT != 3 && OZ_VARIANT != 4) {
+        uint32_t r[5][8];
+        tmem_rows8<QW>(tl, q0, r);
+        double v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const double u = combine5(r, t) * (scale * __ldg(op_scale + q0 + t));
+          if (EPI == EPI_COMB) {
+            v[t] = bs.beta * u + alpha_j * pv[t];
+            acc0[t] += pv[t] * v[t];
+          } else {
+            v[t] = u;
+            if (EPI == EPI_FWD) acc0[t] += u * u;
+            if (EPI == EPI_FWD || out_colmax) {
+              const unsigned long long m = (unsigned long long)__double_as_longlong(u) & 0x7fffffffffffffffull;
+              cm[t] = m > cm[t] ? m : cm[t];
+            }
+          }
+        }
+        double* o = out + row * (EPI == EPI_COMB ? bs.ld : QW) + q0;
+        st_v4(o, v[0], v[1], v[2], v[3]);
+        st_v4(o + 4, v[4], v[5], v[6], v[7]);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
       mbar_arrive(&tempty[buf]);
     }
-    // per-warp folds of the owned columns into this warp's [QW] smem slice (zeros elsewhere)
-    if (out_colmax) {
-      unsigned long long* slice = cmax + (warp - 2) * QW;
-      for (int q = lane; q < QW; q += 32) slice[q] = 0ull;
-      __syncwarp();
+    // per-warp folds of the owned columns into this warp's smem slices (zeros elsewhere)
+    const bool want_max = out_colmax || EPI == EPI_FWD || EPI == EPI_UPD;
+    const int nsum = EPI == EPI_UPD ? 2 : (EPI == EPI_PLAIN ? 0 : 1);
+    unsigned long long* slice = cmax + (warp - 2) * QW;
+    double* fsl = fold + (warp - 2) * 2 * QW;
+    for (int q = lane; q < QW; q += 32) {
+      slice[q] = 0ull;
+      fsl[q] = 0.0;
+      fsl[QW + q] = 0.0;
+    }
+    __syncwarp();
+    if (EPI == EPI_UPD) {  // lanes 4 c hold column c of this warp's group
+      const int cc = treduce8_col();
+      if ((lane & 3) == 0 && active) {
+        slice[q0 + cc] = (unsigned long long)__double_as_longlong(acc_w);
+        fsl[q0 + cc] = acc_rho;
+        fsl[QW + q0 + cc] = acc_rn;
+      }
+    }
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        unsigned long long m = cm[t];
+    for (int t = 0; t < 8 && EPI != EPI_UPD; ++t) {
+      unsigned long long m = cm[t];
+      double a = acc0[t], b = acc1[t];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+      for (int off = 16; off > 0; off >>= 1) {
+        if (want_max) {
           const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, off);
           m = x > m ? x : m;
         }
-        if (lane == 0 && active) slice[q0 + t] = m;
+        if (nsum >= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        if (nsum >= 2) b += __shfl_xor_sync(0xffffffffu, b, off);
       }
-    }
-    if (COMB) {
-      double* psl = reinterpret_cast<double*>(cmax) + (warp - 2) * QW;
-      for (int q = lane; q < QW; q += 32) psl[q] = 0.0;
-      __syncwarp();
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        double v = pacc[t];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0 && active) psl[q0 + t] = v;
+      if (lane == 0 && active) {
+        slice[q0 + t] = m;
+        fsl[q0 + t] = a;
+        fsl[QW + q0 + t] = b;
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (out_colmax && threadIdx.x < QW) {
+  unsigned long long* maxout = EPI == EPI_UPD ? bs.wmax : out_colmax;
+  if (maxout && threadIdx.x < QW) {
     unsigned long long m = cmax[threadIdx.x];
     for (int w = 1; w < BAND_EPI_WARPS; ++w) m = cmax[w * QW + threadIdx.x] > m ? cmax[w * QW + threadIdx.x] : m;
-    atomicMax(&out_colmax[threadIdx.x], m);
+    atomicMax(&maxout[threadIdx.x], m);
   }
-  if (COMB) {
-    const double* psl = reinterpret_cast<const double*>(cmax);
-    if (threadIdx.x < QW) {
-      double v = 0.0;
-      for (int w = 0; w < BAND_EPI_WARPS; ++w) v += psl[w * QW + threadIdx.x];  // fixed warp order
-      partials[(int64_t)blockIdx.x * QW + threadIdx.x] = v;
+  if (EPI != EPI_PLAIN) {
+    const int nsum = EPI == EPI_UPD ? 2 : 1;
+    if (threadIdx.x < nsum * QW) {
+      const int v = threadIdx.x / QW, q = threadIdx.x % QW;
+      double a = 0.0;
+      for (int w = 0; w < BAND_EPI_WARPS; ++w) a += fold[w * 2 * QW + v * QW + q];  // fixed warp order
+      bs.partials[((int64_t)blockIdx.x * nsum + v) * QW + q] = a;
     }
-    double* outs[1] = {pi_out};
-    last_block_reduce(ticket, partials, QW, 1, outs, reinterpret_cast<double*>(cmax) + BAND_EPI_WARPS * QW);
+    double* outs[2] = {bs.out0, bs.out1};
+    // fold scratch after the per-warp slices (the ring is idle)
+    last_block_reduce(bs.ticket, bs.partials, QW, nsum, outs, fold + BAND_EPI_WARPS * 2 * QW);
   }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -897,6 +976,173 @@ __global__ void __launch_bounds__(256, 3)
     for (int i = threadIdx.x; i < 2 * 4 * QW * 4; i += blockDim.x) dst[i] = stage[(i >> 2) * 5 + (i & 3)];
     __syncthreads();
   }
+}
+
+// Direction update of the fused convolution step (one column chunk, ldq ==
+// QW, one preconditioner group) with the NEXT Phi P operand quantised on the
+// fly: the stopping test, the paired X updates and P(u+1) = eta P(u) + M^-1 R
+// exactly as k_direction, and P(u+1)'s K-blocked digit planes, written
+// through a smem stage as whole 64-B lines like k_quantize -- so the separate
+// quantiser launch and its 1 GB re-read of P per convolution step are gone.
+// The column scale must be known before any P(u+1) value exists: it is the
+// power of two above the bound |eta| max|P(u)| + max|M^-1 R(u+1)| (max|P(u)|
+// from the previous launch, max|M^-1 R| from the EPI_UPD band epilogue), at
+// most one bit coarser than the exact column maximum.  Also emitted: the
+// exact column maxima of |P(u+1)| (the next bound) and <P(u+1), alpha
+// P(u+1)> (fixed-order block partials + last-block fold) for pi of the next
+// step.  Each warp owns 16 rows of a 128-row group, lane = column.
+template <int QW>
+__global__ void __launch_bounds__(256, 2)
+    k_direction_q(int64_t rows, int q_real, int step, int max_steps, double tol, int printed,
+                  double* __restrict__ P, const double* __restrict__ R, const double* __restrict__ minv,
+                  const double* __restrict__ alpha, Scalars sc, const unsigned long long* __restrict__ pmax_cur,
+                  unsigned long long* __restrict__ pmax_next, const unsigned long long* __restrict__ wmax,
+                  unsigned long long* __restrict__ reset, double* __restrict__ scale_out,
+                  int8_t* __restrict__ planes, double* __restrict__ pap, unsigned* ticket, Status* st,
+                  Status* mirror, double* X, double* Pdst, const double* Pprev) {
+  {
+    // finished by an EARLIER step: nothing to do (see k_direction)
+    const volatile Status* vs = st;
+    const int done = vs->done;
+    __threadfence();
+    const int sdone = vs->steps;
+    if (done && !(step >= 1 && sdone == step)) {
+      if (mirror && blockIdx.x == 0 && threadIdx.x == 0) {
+        *mirror = *st;
+        __threadfence_system();
+      }
+      return;
+    }
+  }
+  __shared__ uint4 stage[2 * 4 * QW * 5];
+  __shared__ double red[8][2][QW];
+  __shared__ double fold_sm[256];
+  const int cur = step & 1, nxt = (step + 1) & 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool act = lane < QW;
+  const int q = lane;
+  if (step == 0) {
+    double b2 = 0.0;
+    for (int c = 0; c < QW; ++c) b2 += sc.bn2[c];
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->bnorm = sqrt(b2);
+  } else {
+    double r2 = 0.0, b2 = 0.0;
+    for (int c = 0; c < QW; ++c) r2 += sc.rn2[c];
+    for (int c = 0; c < QW; ++c) b2 += sc.bn2[c];
+    const double delta = sqrt(r2) / sqrt(b2);
+    const bool finite = isfinite(delta);
+    const bool conv = finite && delta <= tol;
+    const bool stop = !finite || conv || step >= max_steps;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      volatile Status* vs = st;
+      vs->steps = step;
+      vs->delta = delta;
+      vs->converged = conv ? 1 : 0;
+      vs->diverged = finite ? 0 : 1;
+      __threadfence();
+      if (stop) vs->done = 1;
+      if (mirror) {
+        *mirror = *st;
+        __threadfence_system();
+      }
+    }
+    if (stop) {  // the pending solution updates
+      const bool pair = (step & 1) == 0 && Pprev;
+      for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * QW;
+           e += (int64_t)gridDim.x * blockDim.x) {
+        const int qq = (int)(e % QW);
+        double x = X[e];
+        if (pair) x = x + Pprev[e] * sc.gam[nxt][qq];
+        X[e] = x + P[e] * sc.gam[cur][qq];
+      }
+      return;
+    }
+  }
+  double eta = 0.0, is = 0.0, gm = 0.0, gp = 0.0;
+  const bool upd_x = X && step >= 1 && (!Pprev || (step & 1) == 0);
+  const bool pair = upd_x && Pprev;
+  if (act) {
+    eta = safe_ratio(sc.rho_new[q], sc.rho[cur][q]);
+    const double bound = fabs(eta) * __longlong_as_double((long long)pmax_cur[q]) +
+                         __longlong_as_double((long long)wmax[q]);
+    const double s = !(bound <= 1.7976931348623157e308) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                         : (bound == 0.0 ? 1.0 : pow2_ceil(bound));
+    is = SCALE30 / s;
+    if (blockIdx.x == 0) scale_out[q] = s;
+    if (upd_x) gm = sc.gam[cur][q];
+    if (pair) gp = sc.gam[nxt][q];
+  }
+  if (!Pdst) Pdst = P;
+  const bool ok = is == is;
+  double pmx = 0.0, pacc = 0.0;
+  const int64_t ngrp = rows / 128;
+  for (int64_t g = blockIdx.x; g < ngrp; g += gridDim.x) {
+    const int64_t k0 = g * 128 + warp * QCHUNK_K;
+    if (act) {
+      uint32_t w[4][QCHUNK_K / 4];
+#pragma unroll
+      for (int sub = 0; sub < QCHUNK_K / 4; ++sub) {
+        double r[4], p[4], x[4], pp[4], mv[4], al[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t j = k0 + 4 * sub + i, e = j * QW + q;
+          r[i] = R[e];
+          p[i] = P[e];
+          if (upd_x) x[i] = X[e];
+          if (pair) pp[i] = Pprev[e];
+          mv[i] = __ldg(minv + j);
+          al[i] = __ldg(alpha + j);
+        }
+        uint32_t u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t j = k0 + 4 * sub + i, e = j * QW + q;
+          if (upd_x) X[e] = (pair ? x[i] + pp[i] * gp : x[i]) + p[i] * gm;
+          const double wv = (q < q_real) ? r[i] * mv[i] : 0.0;
+          const double pn = p[i] * eta + (printed ? r[i] : wv);
+          Pdst[e] = pn;
+          const double a = fabs(pn);
+          pmx = (a > pmx || a != a) ? a : pmx;
+          pacc += pn * (al[i] * pn);
+          u[i] = ok ? (((uint32_t)__double2int_rn(pn * is) + 0x80808080u) ^ 0x80808080u) : 0u;
+        }
+        const uint32_t A = __byte_perm(u[0], u[1], 0x5140), B = __byte_perm(u[0], u[1], 0x7362);
+        const uint32_t C = __byte_perm(u[2], u[3], 0x5140), E = __byte_perm(u[2], u[3], 0x7362);
+        w[3][sub] = __byte_perm(A, C, 0x5410);
+        w[2][sub] = __byte_perm(A, C, 0x7632);
+        w[1][sub] = __byte_perm(B, E, 0x5410);
+        w[0][sub] = __byte_perm(B, E, 0x7632);
+      }
+      const int kb = warp >> 2, part = warp & 3;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) stage[((kb * 4 + a) * QW + lane) * 5 + part] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+    }
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(planes + kb_offset(QW, 0, 0, g * 128));
+    for (int i = threadIdx.x; i < 2 * 4 * QW * 4; i += blockDim.x) dst[i] = stage[(i >> 2) * 5 + (i & 3)];
+    __syncthreads();
+  }
+  if (act) {
+    red[warp][0][q] = pmx;
+    red[warp][1][q] = pacc;
+  }
+  __syncthreads();
+  if (threadIdx.x < QW) {
+    double m = 0.0, a = 0.0;
+    for (int ww = 0; ww < 8; ++ww) {
+      const double x = red[ww][0][threadIdx.x];
+      m = (x > m || x != x) ? x : m;
+      a += red[ww][1][threadIdx.x];  // fixed warp order
+    }
+    atomicMax(&pmax_next[threadIdx.x], (unsigned long long)__double_as_longlong(m));
+    sc.partials[(int64_t)blockIdx.x * QW + threadIdx.x] = a;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < QW) {
+    sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
+    if (reset) reset[threadIdx.x] = 0ull;
+  }
+  double* outs[1] = {pap};
+  last_block_reduce(ticket, sc.partials, QW, 1, outs, fold_sm);
 }
 
 // ---- dictionary conversion (once per dictionary) ---------------------------

@@ -87,7 +87,8 @@ def shard_context(op, precision, device, c0, c1):
     if isinstance(op, ConvolutionOperator):
         if precision not in ("ozaki", "ozaki24"):
             raise NotImplementedError("time-sharded convolutions run the 'ozaki' (int8 band) kernels")
-        ctx = _lib.Context.convolution(c1 - c0, op.gpu_taps(), _lib.OZAKI, device)
+        ctx = _lib.Context.convolution(c1 - c0, op.gpu_taps(), _lib.OZAKI24 if precision == "ozaki24" else _lib.OZAKI,
+                                       device)
     else:
         code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}[precision]
         ctx = _lib.Context(op.n_rows, c1 - c0, code, device)

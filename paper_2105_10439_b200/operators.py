@@ -276,11 +276,14 @@ class ConvolutionOperator(LinearOperator):
         return ctx
 
     def new_context(self, precision="auto"):
-        """'ozaki': banded int8 tensor-core kernel (any filter length);
-        'fp64': float64 overlap-save FFT passes (filters up to 512 taps)."""
+        """'ozaki': banded int8 tensor-core kernel (any filter length; 32-bit
+        fixed-point taps), 'ozaki24': the same with 24-bit taps (three band
+        digit planes, a quarter fewer MMAs); 'fp64': float64 overlap-save FFT
+        passes (filters up to 512 taps)."""
         precision = self.resolve_precision(precision)
-        if precision in ("ozaki", "ozaki24"):  # the band keeps 32-bit taps
-            return _lib.Context.convolution(self.n_cols, self.gpu_taps(), _lib.OZAKI, self.device)
+        if precision in ("ozaki", "ozaki24"):
+            code = _lib.OZAKI24 if precision == "ozaki24" else _lib.OZAKI
+            return _lib.Context.convolution(self.n_cols, self.gpu_taps(), code, self.device)
         if precision == "fp64":
             return _lib.Context.convolution(self.n_cols, self.fft_taps(), _lib.FP64, self.device)
         raise NotImplementedError("convolution dictionaries run in the 'ozaki' or 'fp64' precision mode")

@@ -423,7 +423,8 @@ def test_run_cofem_convolution_parity(precision):
     assert abs(nour - nref) <= 0.01 * nref
 
 
-@pytest.mark.parametrize("K,precision", [(20, "ozaki"), (40, "ozaki"), (20, "fp64"), (40, "fp64")])
+@pytest.mark.parametrize("K,precision", [(20, "ozaki"), (40, "ozaki"), (20, "fp64"), (40, "fp64"), (20, "ozaki24"),
+                                         (30, "ozaki")])
 def test_run_cofem_convolution_config_family(K, precision):
     """BASELINE config 3's problem family at D = 8192 (256 taps, sigma 0.05),
     3 EM iterations, against the float64 oracle step for step.  K = 40 runs the
@@ -860,3 +861,44 @@ def test_one_launch_solve_matches_multikernel_step():
     assert outs[0]["steps"] == outs[1]["steps"], (outs[0]["steps"], outs[1]["steps"])
     assert rel(np.array(outs[0]["mu"]), np.array(outs[1]["mu"])) <= 1e-7
     assert rel(np.array(outs[0]["alpha"]), np.array(outs[1]["alpha"])) <= 1e-7
+
+
+def test_fused_convolution_step_matches_separate_launches():
+    """The fused convolution PCG step (band Phi P with ||V||^2, quantise V,
+    band Phi^T V with the residual update in its epilogue, direction with the
+    next operand's digit planes against the bound scale; no Psi block) and
+    the six-launch step (COFEM_CONV_UNFUSED) run the same recursion up to
+    rounding and the one-bit coarser P scale: same CG steps within 1, mu /
+    alpha to 1e-6, each bitwise repeatable."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, numpy as np\n"
+        "from paper_2105_10439_b200 import run_cofem\n"
+        "from paper_2105_10439_b200 import simulate as S\n"
+        "c = S.ConvConfig('conv-test', 16384, 256, 20.0, 0.01, 0.05, 30, 3, 200, 1e-5)\n"
+        "prob, z = S.conv_problem(c)\n"
+        "runs = [run_cofem(prob, c.cofem_config('ozaki')) for _ in range(2)]\n"
+        "st, est, diag = runs[0]\n"
+        "same = bool(np.array_equal(st.alpha, runs[1][0].alpha) and np.array_equal(est.mu, runs[1][1].mu))\n"
+        "print(json.dumps({'mu': est.mu.tolist(), 'alpha': st.alpha.tolist(), 'same': same,"
+        " 'steps': [d['cg_steps'] for d in diag]}))\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for unfused in (False, True):
+        env = dict(os.environ, PYTHONPATH=root)
+        env.pop("COFEM_CONV_UNFUSED", None)
+        if unfused:
+            env["COFEM_CONV_UNFUSED"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = outs
+    assert a["same"] and b["same"]
+    assert all(abs(x - y) <= 1 for x, y in zip(a["steps"], b["steps"])), (a["steps"], b["steps"])
+    assert rel(np.array(a["mu"]), np.array(b["mu"])) <= 1e-6
+    assert rel(np.array(a["alpha"]), np.array(b["alpha"])) <= 1e-6
