@@ -534,7 +534,12 @@ __device__ __forceinline__ double combine5(const uint32_t (&r)[5][8], int t) {
   return fma((double)(int32_t)r[0][t], 4294967296.0, (double)lo);
 }
 __device__ __forceinline__ void ld_v4_rw(const double* p, double& a, double& b, double& c, double& d) {
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+// streamed read-only rows: no L1 allocation (the stream would evict the few
+// spilled registers of a 96-register epilogue from L1)
+__device__ __forceinline__ void ld_v4_stream(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
 // L2 prefetch of a contiguous global range (bulk, no registers / smem)
@@ -709,18 +714,22 @@ __global__ void __launch_bounds__(BAND_NTHREADS, 1)
       acc0[t] = 0.0;
       acc1[t] = 0.0;
     }
+    // the band's output rows all carry the same power-of-two scale (hrows holds
+    // copies): one load before the loop, not a dependent load per tile (ncu:
+    // a quarter of the Phi P launch's stall samples sat on that load)
+    const double band_scale = row_scale[0] * (65536.0 / (SCALE30 * SCALE30));
     int it = 0;
     for (int mb = blockIdx.x; mb < n_mblocks; mb += gridDim.x, ++it) {
       const int buf = it % BAND_SETS;
       const int64_t row = (int64_t)mb * BM + row_in_tile;
-      const double scale = row < rows_real ? row_scale[row] * (65536.0 / (SCALE30 * SCALE30)) : 0.0;
+      const double scale = row < rows_real ? band_scale : 0.0;
       double pv[8], rr[8];
       double alpha_j = 0.0, mv = 0.0;
       if ((EPI == EPI_COMB || EPI == EPI_UPD) && active) {
         alpha_j = bs.alpha[row];
         const double* prow = bs.P + row * bs.ld + q0;
-        ld_v4(prow, pv[0], pv[1], pv[2], pv[3]);
-        ld_v4(prow + 4, pv[4], pv[5], pv[6], pv[7]);
+        ld_v4_stream(prow, pv[0], pv[1], pv[2], pv[3]);
+        ld_v4_stream(prow + 4, pv[4], pv[5], pv[6], pv[7]);
       }
       if (EPI == EPI_UPD && active) {
         mv = bs.minv[row * bs.ngroups];
