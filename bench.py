@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="dense-large")
-    ap.add_argument("--precision", default="ozaki", choices=["fp32", "fp64", "ozaki", "ozaki24"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp32", "fp64", "ozaki", "ozaki24"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -614,8 +614,26 @@ def relaunch_distributed(n):
     os.execv(sys.executable, cmd)
 
 
+def resolve_precision(args):
+    """--precision auto: the mode the library's CgConfig(precision="auto")
+    picks for this config's operator (operators.py resolve_precision)."""
+    if args.precision != "auto":
+        return args.precision
+    from paper_2105_10439_b200 import simulate as S
+    from paper_2105_10439_b200.operators import AUTO_FP64_ENTRIES, ConvolutionOperator
+
+    if args.config in S.CONFIGS:
+        c = S.CONFIGS[args.config]
+        return "fp64" if c.N * c.D <= AUTO_FP64_ENTRIES else "ozaki24"
+    if args.config in S.CONV_CONFIGS:
+        c = S.CONV_CONFIGS[args.config]
+        return ConvolutionOperator.from_taps(c.D, c.taps()).resolve_precision("auto")
+    return "fp64"
+
+
 def main():
     args = parse()
+    args.precision = resolve_precision(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_distributed(args.gpus)
     if args.impl == "reference":

@@ -153,7 +153,7 @@ class ShardedContext:
             self.shards = column_shards(n_cols, self.world)
             c0, c1 = self.shards[self.rank]
             if precision == "auto":
-                precision = "ozaki"  # a dictionary worth sharding is large
+                precision = "ozaki24"  # a dictionary worth sharding is large
             code = {"fp32": _lib.FP32, "fp64": _lib.FP64, "ozaki": _lib.OZAKI, "ozaki24": _lib.OZAKI24}[precision]
             self.ctx = _lib.Context(n_rows, c1 - c0, code, device)
             self.ctx.set_shard(c0, n_cols)

@@ -110,12 +110,12 @@ def dense_large():
     prob.op.release()
 
 
-@pytest.mark.parametrize("precision", ["auto", "ozaki"])
+@pytest.mark.parametrize("precision", ["auto", "ozaki", "ozaki24"])
 def test_config3_dense_large_headline(dense_large, precision):
     """Config 3, the headline (N=16384, D=65536 -- Phi 4 GiB --, K=20, 20 EM
     iterations, cap 200, tol 1e-5) on the int8 tensor-core path (the default
-    mode, and the 32-bit fixed-point dictionary) against the reference's
-    float64 run on the same float32-exact Phi."""
+    mode, the 32-bit and the 24-bit fixed-point dictionary) against the
+    reference's float64 run on the same float32-exact Phi."""
     g, c, prob, z = dense_large
     if precision == "auto":
         assert prob.op.resolve_precision("auto") in ("ozaki", "ozaki24")

@@ -236,7 +236,7 @@ def test_auto_precision_policy():
     with pytest.raises(ValueError):
         CgConfig(precision="fp16")
     assert DenseOperator(np.zeros((256, 1024), dtype=np.float32)).resolve_precision("auto") == "fp64"
-    assert DenseOperator(np.zeros((4096, 4097), dtype=np.float32)).resolve_precision("auto") == "ozaki"
+    assert DenseOperator(np.zeros((4096, 4097), dtype=np.float32)).resolve_precision("auto") == "ozaki24"
     assert DenseOperator(np.zeros((4, 4), dtype=np.float32)).resolve_precision("ozaki") == "ozaki"
     assert ConvolutionOperator(512, 0.04).resolve_precision("auto") == "fp64"
     h = np.exp(-np.arange(256) / 20.0)
