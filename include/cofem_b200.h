@@ -121,6 +121,15 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
  * accepted as an alias: the passes are float64 either way). */
 int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision);
 
+/* 1-D subsampled DCT dictionary: operators.SubsampledDctOperator
+ * (operators.py:132-179), Phi = the rows `mask` of the orthonormal inverse
+ * DCT-II (DCT-III) of length `dim` (any dim >= 2).  O(D log D): Makhoul's
+ * reduction, two real columns per complex length-D FFT (cuFFT double
+ * complex, loaded at run time), fused float64 pre / mask / post passes;
+ * Phi^T Phi = DCT-II(mask .* DCT-III(.)).  Precision COFEM_FP64 (the int8
+ * modes are accepted as aliases). */
+int cofem_create_dct1(cofem_ctx** out, int device, int64_t dim, const int64_t* mask, int64_t nmask, int precision);
+
 /* Upload Phi (N x D_local float32, row stride `ld` elements) from host
  * memory (or adopt a device pointer when `on_device` != 0; the caller keeps
  * it alive).  operators.DenseOperator.__init__, operators.py:109-117. */

@@ -38,6 +38,7 @@ EXPORTED = (
     "cofem_destroy",
     "cofem_create_convolution",
     "cofem_create_dct2",
+    "cofem_create_dct1",
     "cofem_set_dictionary",
     "cofem_set_dictionary_f64",
     "cofem_set_shard",
@@ -140,6 +141,7 @@ def load():
         "cofem_destroy": (c_int, [vp]),
         "cofem_create_convolution": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_double), c_int64, c_int]),
         "cofem_create_dct2": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_int64), c_int64, c_int]),
+        "cofem_create_dct1": (c_int, [POINTER(vp), c_int, c_int64, POINTER(c_int64), c_int64, c_int]),
         "cofem_set_dictionary": (c_int, [vp, vp, c_int64, c_int]),
         "cofem_set_dictionary_f64": (c_int, [vp, POINTER(c_double), c_int64]),
         "cofem_set_shard": (c_int, [vp, c_int64, c_int64]),
@@ -230,6 +232,15 @@ class Context:
         check(load().cofem_create_dct2(ctypes.byref(handle), int(device), int(n), mask.ctypes.data_as(POINTER(c_int64)),
                                        mask.size, int(precision)))
         return cls(mask.size, n * n, precision, device, _handle=handle)
+
+    @classmethod
+    def dct1(cls, dim, mask, precision=FP64, device=0):
+        """1-D subsampled DCT dictionary: rows `mask` of the orthonormal inverse DCT-II of length dim."""
+        mask = np.ascontiguousarray(mask, dtype=np.int64)
+        handle = c_void_p()
+        check(load().cofem_create_dct1(ctypes.byref(handle), int(device), int(dim), mask.ctypes.data_as(POINTER(c_int64)),
+                                       mask.size, int(precision)))
+        return cls(mask.size, dim, precision, device, _handle=handle)
 
     @classmethod
     def convolution(cls, dim, taps, precision=OZAKI, device=0):

@@ -28,6 +28,8 @@
 #include "kernels.cuh"
 #include "nccl.h"
 #include "dct.cuh"
+#include "dct1.cuh"
+#include <cufft.h>
 #include "ozaki.cuh"
 #include "pcg.cuh"
 #include "persistent.cuh"
@@ -78,6 +80,32 @@ struct NcclApi {
   ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi g_nccl;
+
+// ---- cuFFT, bound at run time (only the 1-D subsampled DCT uses it) --------
+struct CufftApi {
+  bool tried = false, ok = false;
+  cufftResult (*planMany)(cufftHandle*, int, int*, int*, int, int, int*, int, int, cufftType, int) = nullptr;
+  cufftResult (*execZ2Z)(cufftHandle, cufftDoubleComplex*, cufftDoubleComplex*, int) = nullptr;
+  cufftResult (*setStream)(cufftHandle, cudaStream_t) = nullptr;
+  cufftResult (*destroy)(cufftHandle) = nullptr;
+};
+CufftApi g_cufft;
+
+int cufft_load() {
+  if (g_cufft.tried) return g_cufft.ok ? 0 : fail(COFEM_ECUDA, "libcufft.so.11 not loadable");
+  g_cufft.tried = true;
+  const char* names[] = {"libcufft.so.11", "libcufft.so", "/usr/local/cuda/lib64/libcufft.so.11"};
+  void* h = nullptr;
+  for (const char* n : names)
+    if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return fail(COFEM_ECUDA, std::string("dlopen libcufft.so.11 failed: ") + dlerror());
+  g_cufft.planMany = (decltype(g_cufft.planMany))dlsym(h, "cufftPlanMany");
+  g_cufft.execZ2Z = (decltype(g_cufft.execZ2Z))dlsym(h, "cufftExecZ2Z");
+  g_cufft.setStream = (decltype(g_cufft.setStream))dlsym(h, "cufftSetStream");
+  g_cufft.destroy = (decltype(g_cufft.destroy))dlsym(h, "cufftDestroy");
+  g_cufft.ok = g_cufft.planMany && g_cufft.execZ2Z && g_cufft.setStream && g_cufft.destroy;
+  return g_cufft.ok ? 0 : fail(COFEM_ECUDA, "libcufft missing symbols");
+}
 
 int nccl_load() {
   if (g_nccl.tried) return g_nccl.ok ? 0 : fail(COFEM_ENCCL, "libnccl.so.2 not loadable");
@@ -285,6 +313,12 @@ struct cofem_ctx {
   double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n}
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
+  // 1-D subsampled DCT (kind 3, dct1.cuh): length D = N_cols, N = mask size;
+  // dct_mask holds the sorted mask, bufA the complex [D][ldq / 2] work block
+  uint8_t* dct1_mv = nullptr;  // the mask in Makhoul (v) order: mask[sigma(m)]
+  cufftHandle fft_plan = 0;
+  int fft_plan_hc = 0;         // column pairs the plan was made for (0: none)
+
   // multi-GPU
   ncclComm_t comm = nullptr;
   cofem_group* lgroup = nullptr;  // in-process shard group (instead of comm)
@@ -455,7 +489,7 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMalloc(&c->Psi, dbytes));
   // the DCT passes transform all ldq columns at once; the contractions run
   // 32-column chunks
-  const bool whole = c->kind == 2 || c->conv_fft;  // passes over all ldq columns at once
+  const bool whole = c->kind == 2 || c->kind == 3 || c->conv_fft;  // passes over all ldq columns at once
   const int vcols = whole ? std::max(ldq, QCHUNK) : QCHUNK;
   CK(cudaMalloc(&c->tmpD, (size_t)c->Dp * vcols * ts));
   CK(cudaMalloc(&c->V, (size_t)c->Np * vcols * ts));
@@ -476,6 +510,10 @@ int ensure_ws(cofem_ctx* c, int ldq) {
   CK(cudaMemsetAsync(c->P, 0, dbytes, c->stream));
   CK(cudaMemsetAsync(c->P2, 0, dbytes, c->stream));
   CK(cudaMemsetAsync(c->Psi, 0, dbytes, c->stream));
+  if (c->kind == 3) {  // the complex [D][ldq / 2] work block
+    if (c->bufA) cudaFree(c->bufA);
+    CK(cudaMalloc(&c->bufA, (size_t)c->D * ldq * sizeof(double)));
+  }
   if (c->kind == 2) {
     const int64_t n = c->dct_n, nc = n * ldq;
     for (double** b : {&c->bufA, &c->bufB}) {
@@ -1095,6 +1133,76 @@ int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
   return 0;
 }
 
+// ---- 1-D subsampled DCT (kind 3; dct1.cuh) ----------------------------------
+int dct1_plan(cofem_ctx* c) {
+  const int hc = c->ldq / 2;
+  if (c->fft_plan_hc == hc) return 0;
+  CKR(cufft_load());
+  if (c->fft_plan_hc) g_cufft.destroy(c->fft_plan);
+  c->fft_plan_hc = 0;
+  int n = (int)c->D, emb = (int)c->D;
+  if (g_cufft.planMany(&c->fft_plan, 1, &n, &emb, hc, 1, &emb, hc, 1, CUFFT_Z2Z, hc) != CUFFT_SUCCESS)
+    return fail(COFEM_ECUDA, "cufftPlanMany failed");
+  if (g_cufft.setStream(c->fft_plan, c->stream) != CUFFT_SUCCESS) return fail(COFEM_ECUDA, "cufftSetStream failed");
+  c->fft_plan_hc = hc;
+  return 0;
+}
+
+int dct1_fft(cofem_ctx* c, int dir) {
+  CKR(dct1_plan(c));
+  cufftDoubleComplex* z = reinterpret_cast<cufftDoubleComplex*>(c->bufA);
+  if (g_cufft.execZ2Z(c->fft_plan, z, z, dir) != CUFFT_SUCCESS) return fail(COFEM_ECUDA, "cufftExecZ2Z failed");
+  c->launches++;
+  return 0;
+}
+
+// bufA <- DCT-III of the real block X (all ldq columns), in v order
+int dct1_inverse(cofem_ctx* c, const double* X) {
+  dct1::k_pre<<<8 * c->sm_count, 256, 0, c->stream>>>(c->D, c->ldq, X, reinterpret_cast<double2*>(c->bufA));
+  c->launches++;
+  CK(cudaGetLastError());
+  return dct1_fft(c, CUFFT_INVERSE);
+}
+
+// out (real [Dp][ldq]) <- orthonormal DCT-II of the v-order vectors in bufA
+int dct1_forward_post(cofem_ctx* c, double* out) {
+  CKR(dct1_fft(c, CUFFT_FORWARD));
+  dct1::k_post<<<8 * c->sm_count, 256, 0, c->stream>>>(c->D, c->Dp, c->ldq, reinterpret_cast<const double2*>(c->bufA),
+                                                       out);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// Psi = beta Phi^T Phi P + alpha .* P for all ldq columns, pi on the fly:
+// DCT-III, mask (v order), DCT-II, then the streaming PCG combine
+int dct1_system_apply(cofem_ctx* c, double beta, const Status* stt) {
+  CKR(dct1_inverse(c, (const double*)c->P));
+  dct1::k_vmask<<<8 * c->sm_count, 256, 0, c->stream>>>(c->D, c->ldq / 2, reinterpret_cast<double2*>(c->bufA),
+                                                        c->dct1_mv);
+  c->launches++;
+  CK(cudaGetLastError());
+  CKR(dct1_forward_post(c, (double*)c->tmpD));
+  Scalars sc = c->sc();
+  const int bs = elem_block(c->ldq);
+  k_combine<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->tmpD, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
+      stt);
+  c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// tmpD <- Phi^T of the N x ldq block in V
+int dct1_adjoint_from_V(cofem_ctx* c) {
+  CK(cudaMemsetAsync(c->bufA, 0, (size_t)c->D * c->ldq * sizeof(double), c->stream));
+  dct1::k_scatter<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, c->D, c->ldq, c->dct_mask, (const double*)c->V,
+                                                          reinterpret_cast<double2*>(c->bufA));
+  c->launches++;
+  CK(cudaGetLastError());
+  return dct1_forward_post(c, (double*)c->tmpD);
+}
+
 // ---- the two contractions ----------------------------------------------
 // fwd: V (Np x qpc dense) = Phi * src[:, qoff:qoff+qpc]  (src Dp x lds)
 template <typename T, int QP, typename PhiT>
@@ -1223,6 +1331,7 @@ template <typename T>
 int system_apply_dev(cofem_ctx* c, double beta, const Status* st) {
   if constexpr (std::is_same<T, double>::value) {
     if (c->kind == 2) return dct_system_apply(c, beta, st);
+    if (c->kind == 3) return dct1_system_apply(c, beta, st);
     if (c->conv_fft) return conv_fft_system_apply(c, beta, st);
   }
   Scalars sc = c->sc();
@@ -1828,6 +1937,14 @@ int apply_impl(cofem_ctx* c, const double* V, int64_t q, double* out) {
     CKR(conv_fft_pass(c, (const double*)c->P, (double*)c->V, false, nullptr));
     return download_block<T>(c, c->V, c->N, q, ldq, 0, out);
   }
+  if (c->kind == 3) {
+    CKR(dct1_inverse(c, (const double*)c->P));
+    dct1::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, c->Np, c->D, ldq, c->dct_mask,
+                                                           reinterpret_cast<const double2*>(c->bufA), (double*)c->V);
+    c->launches++;
+    CK(cudaGetLastError());
+    return download_block<T>(c, c->V, c->N, q, ldq, 0, out);
+  }
   if (c->kind == 2) {
     CKR(dct_forward_dev(c, (const double*)c->P, nullptr));
     dctf::k_gather<<<8 * c->sm_count, 256, 0, c->stream>>>(c->N, ldq, c->dct_mask, c->bufB, (double*)c->V);
@@ -1859,9 +1976,9 @@ int adjoint_impl(cofem_ctx* c, const double* U, int64_t q, double* out) {
     CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, nullptr));
     return download_block<T>(c, c->tmpD, c->D, q, ldq, 0, out);
   }
-  if (c->kind == 2) {
+  if (c->kind == 2 || c->kind == 3) {
     CKR(upload_block<T>(c, U, c->N, q, c->Np, ldq, c->V));
-    CKR(dct_adjoint_from_V(c));
+    CKR(c->kind == 2 ? dct_adjoint_from_V(c) : dct1_adjoint_from_V(c));
     return download_block<T>(c, c->tmpD, c->D, q, ldq, 0, out);
   }
   std::vector<double> chunk;
@@ -1912,7 +2029,7 @@ int compute_aty(cofem_ctx* c, const double* y_host) {
   // y goes up as N doubles and aty is gathered on the device (no host
   // staging of the Np x ldq blocks).
   CKR(ensure_ws(c, std::max(c->ldq, 8)));
-  const bool whole = c->kind == 2 || c->conv_fft;
+  const bool whole = c->kind == 2 || c->kind == 3 || c->conv_fft;
   const int ld = whole ? c->ldq : 8;
   if (!c->ybuf) CK(cudaMalloc(&c->ybuf, c->Np * sizeof(double)));
   CK(cudaMemcpyAsync(c->ybuf, y_host, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -1921,6 +2038,7 @@ int compute_aty(cofem_ctx* c, const double* y_host) {
     k_put_col0<double><<<g, 256, 0, c->stream>>>(c->ybuf, c->N, c->Np, ld, (double*)c->V);
     c->launches++;
     if (c->conv_fft) CKR(conv_fft_pass(c, (const double*)c->V, (double*)c->tmpD, true, nullptr));
+    else if (c->kind == 3) CKR(dct1_adjoint_from_V(c));
     else CKR(dct_adjoint_from_V(c));
     k_get_col0<double><<<g, 256, 0, c->stream>>>((const double*)c->tmpD, c->D, c->Dp, ld, c->aty);
     c->launches++;
@@ -1963,7 +2081,8 @@ int em_prepare(cofem_ctx* c, const double* y, double beta, const cofem_em_config
   std::vector<double> a(c->Dp, 1.0);
   CK(h2d_sync(c, c->alpha, a.data(), c->Dp * sizeof(double)));
   if (em->theta_policy == COFEM_THETA_JACOBI) {
-    if (c->kind == 2) return fail(COFEM_EINVAL, "jacobi on a DCT dictionary: pass its column norms as custom theta");
+    if (c->kind == 2 || c->kind == 3)
+      return fail(COFEM_EINVAL, "jacobi on a DCT dictionary: pass its column norms as custom theta");
     if (c->kind == 0) {
       CKR(dense_colsq(c));
     }
@@ -2455,6 +2574,72 @@ int cofem_create_convolution(cofem_ctx** out, int device, int64_t dim, const dou
   return 0;
 }
 
+int cofem_create_dct1(cofem_ctx** out, int device, int64_t dim, const int64_t* mask, int64_t nmask, int precision) {
+  if (!out || !mask) return fail(COFEM_EINVAL, "null argument");
+  *out = nullptr;
+  if (dim < 2 || dim > ((int64_t)1 << 30)) return fail(COFEM_EINVAL, "need 2 <= dim <= 2^30");
+  if (nmask < 1 || nmask > dim) return fail(COFEM_EINVAL, "need 1 <= mask size <= dim");
+  if (precision == COFEM_OZAKI24 || precision == COFEM_OZAKI) precision = COFEM_FP64;
+  if (precision != COFEM_FP64) return fail(COFEM_EINVAL, "1-D DCT dictionaries run in FP64 (cuFFT double complex)");
+  std::vector<uint8_t> grid((size_t)dim, 0);
+  for (int64_t m = 0; m < nmask; ++m) {
+    if (mask[m] < 0 || mask[m] >= dim) return fail(COFEM_EINVAL, "mask indices must lie in [0, dim)");
+    if (grid[mask[m]]) return fail(COFEM_EINVAL, "mask indices must be distinct");
+    grid[mask[m]] = 1;
+  }
+  CKR(cufft_load());
+  cofem_ctx* c = new cofem_ctx();
+  c->kind = 3;
+  c->device = device;
+  c->prec = COFEM_FP64;
+  c->N = nmask;
+  c->D = dim;
+  c->Np = round_up(nmask, PAD);
+  c->Dp = round_up(dim, PAD);
+  c->global_cols = dim;
+  auto bail = [&](int rc) {
+    cofem_destroy(c);
+    return rc;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(COFEM_ECUDA, "stream create failed"));
+  double** dvecs[] = {&c->alpha, &c->minv, &c->theta, &c->colsq, &c->mu, &c->s, &c->aty};
+  for (double** p : dvecs) {
+    if (cudaMalloc(p, c->Dp * sizeof(double)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "vector allocation"));
+    cudaMemsetAsync(*p, 0, c->Dp * sizeof(double), c->stream);
+  }
+  if (cudaMalloc(&c->tickets, 8 * sizeof(unsigned)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "tickets"));
+  cudaMemsetAsync(c->tickets, 0, 8 * sizeof(unsigned), c->stream);
+  if (cudaMalloc(&c->st, sizeof(Status)) != cudaSuccess) return bail(fail(COFEM_ENOMEM, "status"));
+  if (cudaHostAlloc(&c->h_st, LAG * sizeof(Status), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->d_hst, c->h_st, 0) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "pinned status"));
+  for (int i = 0; i < LAG; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  if (cudaMalloc(&c->colmax, 1024 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(COFEM_ENOMEM, "colmax"));
+  // the mask sorted (row order of Phi) and in Makhoul order: mv[m] = grid[sigma(m)]
+  std::vector<int64_t> sorted(mask, mask + nmask);
+  std::sort(sorted.begin(), sorted.end());
+  std::vector<uint8_t> mv((size_t)dim);
+  for (int64_t m = 0; m < dim; ++m) mv[m] = grid[m < (dim + 1) / 2 ? 2 * m : 2 * (dim - 1 - m) + 1];
+  if (cudaMalloc(&c->dct_mask, nmask * sizeof(int64_t)) || cudaMalloc(&c->dct1_mv, (size_t)dim))
+    return bail(fail(COFEM_ENOMEM, "DCT tables"));
+  h2d_sync(c, c->dct_mask, sorted.data(), nmask * sizeof(int64_t));
+  h2d_sync(c, c->dct1_mv, mv.data(), (size_t)dim);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
+  c->have_phi = true;
+  c->oz_ready = true;
+  cudaStreamSynchronize(c->stream);
+  *out = c;
+  return 0;
+}
+
 int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mask, int64_t nmask, int precision) {
   if (!out || !mask) return fail(COFEM_EINVAL, "null argument");
   *out = nullptr;
@@ -2548,7 +2733,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -2557,6 +2742,7 @@ int cofem_destroy(cofem_ctx* c) {
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
   for (cudaEvent_t e : c->evpool) cudaEventDestroy(e);
+  if (c->fft_plan_hc && g_cufft.ok) g_cufft.destroy(c->fft_plan);
   if (c->comm && g_nccl.ok) g_nccl.commDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -2686,7 +2872,7 @@ int cofem_set_shard(cofem_ctx* c, int64_t col_offset, int64_t global_cols) {
   if (!c) return fail(COFEM_EINVAL, "null context");
   if (col_offset < 0 || col_offset + c->D > global_cols || col_offset % 4 != 0)
     return fail(COFEM_EINVAL, "shard must be 4-aligned and inside the global columns");
-  if (c->kind == 2 && (col_offset != 0 || global_cols != c->D))
+  if ((c->kind == 2 || c->kind == 3) && (col_offset != 0 || global_cols != c->D))
     return fail(COFEM_EINVAL, "2-D DCT dictionaries are not sharded");
   if (c->kind == 1) {
     // time shard [t0, t0 + D) of a length-global_cols sequence: boundaries on
@@ -2714,7 +2900,7 @@ namespace {
 int attach_ranks(cofem_ctx* c, int nranks, int rank) {
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(COFEM_EINVAL, "bad rank / nranks");
   if (nranks > 1) {
-    if (c->kind == 2) return fail(COFEM_EINVAL, "2-D DCT dictionaries run on one GPU (not sharded)");
+    if (c->kind == 2 || c->kind == 3) return fail(COFEM_EINVAL, "DCT dictionaries run on one GPU (not sharded)");
     if (c->kind == 1 && c->conv_fft) return fail(COFEM_EINVAL, "the FP64 FFT convolution path runs on one GPU");
     if (c->kind == 1 && c->col_offset + c->D < c->global_cols && rank == nranks - 1)
       return fail(COFEM_EINVAL, "the last rank must hold the end of the sequence");
@@ -2866,7 +3052,8 @@ int cofem_column_sq_norms(cofem_ctx* c, double* out) {
     CK(cudaMemcpy(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost));
     return 0;
   }
-  if (c->kind == 2) return fail(COFEM_EINVAL, "DCT column norms are computed by the host (pass a custom theta)");
+  if (c->kind == 2 || c->kind == 3)
+    return fail(COFEM_EINVAL, "DCT column norms are computed by the host (pass a custom theta)");
   CKR(dense_colsq(c));
   CK(cudaMemcpyAsync(out, c->colsq, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));

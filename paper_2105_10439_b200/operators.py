@@ -171,43 +171,116 @@ class DenseOperator(LinearOperator):
         return self.apply_context().column_sq_norms()
 
 
+MATERIALIZE_DCT_MAX = 8192  # SubsampledDctOperator: dims up to this run as a materialised dense dictionary
+
+
+def _dct_mask(dim, mask):
+    mask = np.asarray(mask, dtype=np.int64)
+    if mask.ndim != 1 or mask.size < 1:
+        raise ValueError("mask must be a nonempty 1-D index array")
+    if np.unique(mask).size != mask.size:
+        raise ValueError("mask indices must be distinct")
+    if mask.min() < 0 or mask.max() >= dim:
+        raise ValueError(f"mask indices must lie in [0, {dim})")
+    mask = np.sort(mask)
+    mask.flags.writeable = False
+    return mask
+
+
+def _dct1_column_sq_norms(dim, mask):
+    """||Phi e_j||^2 = c_j^2 sum_i cos^2(pi (2 m_i + 1) j / 2D) (operators.py:165-179)
+    = c_j^2 (N + Re(e^{i pi j / D} sum_i e^{2 pi i m_i j / D})) / 2: one FFT of
+    the mask indicator instead of the reference's O(N D) cosine table."""
+    scale = np.full(dim, 2.0 / dim)
+    scale[0] = 1.0 / dim
+    ind = np.zeros(dim)
+    ind[mask] = 1.0
+    j = np.arange(dim)
+    s = np.real(np.exp(1j * np.pi * j / dim) * (dim * np.fft.ifft(ind)))
+    return scale * (0.5 * mask.size + 0.5 * s)
+
+
 class SubsampledDctOperator(DenseOperator):
     """Phi = M Omega^{-1}: inverse orthonormal DCT-II rows selected by a mask
-    (operators.py:132-179).  Materialised once (float64, N x D) and run as a
-    dense dictionary on the GPU -- the int8 digit planes are built from the
-    float64 entries -- so D is limited to dense-friendly sizes (<= 32768)."""
+    (operators.py:132-179).  Small dims (<= MATERIALIZE_DCT_MAX) are
+    materialised once (float64, N x D) and run as a dense dictionary (exact
+    float64 contractions under "auto"); larger ones -- or ``fast=True`` --
+    construct a :class:`FastSubsampledDctOperator`, the O(D log D) device
+    path (same interface, no N x D matrix)."""
+
+    kind = "undersampled-dct"
+
+    def __new__(cls, dim, mask, device=0, fast=None):
+        if fast or (fast is None and dim > MATERIALIZE_DCT_MAX):
+            return FastSubsampledDctOperator(dim, mask, device)
+        return super().__new__(cls)
+
+    def __init__(self, dim, mask, device=0, fast=None):
+        from scipy.fft import idct
+
+        mask = _dct_mask(dim, mask)
+        super().__init__(idct(np.eye(dim), axis=0, norm="ortho")[mask, :], device=device)
+        self.mask = mask
+
+    def resolve_precision(self, precision):
+        # exact float64 contractions: orthonormal-row DCT dictionaries make CG's
+        # step count sensitive to any rounding of Phi (DESIGN.md "Parity")
+        return "fp64" if check_precision(precision) == "auto" else precision
+
+    def column_sq_norms(self):
+        """Analytic column norms, operators.py:165-179."""
+        return _dct1_column_sq_norms(self.n_cols, self.mask)
+
+
+class FastSubsampledDctOperator(LinearOperator):
+    """The reference's SubsampledDctOperator (operators.py:132-179) without a
+    materialised matrix, any D: on the GPU Phi V = DCT-III(V)[mask], Phi^T U =
+    DCT-II(scatter(U)) and Phi^T Phi = DCT-II(mask .* DCT-III(.)), each a
+    batched complex length-D FFT with Makhoul's packing of two real columns
+    (csrc/dct1.cuh; cuFFT double complex for the FFTs themselves) -- O(D log D)
+    per column instead of O(N D).  Float64 whatever the precision mode."""
 
     kind = "undersampled-dct"
 
     def __init__(self, dim, mask, device=0):
-        from scipy.fft import idct
-
-        mask = np.asarray(mask, dtype=np.int64)
-        if mask.ndim != 1 or mask.size < 1:
-            raise ValueError("mask must be a nonempty 1-D index array")
-        if np.unique(mask).size != mask.size:
-            raise ValueError("mask indices must be distinct")
-        if mask.min() < 0 or mask.max() >= dim:
-            raise ValueError(f"mask indices must lie in [0, {dim})")
-        if dim > 32768:
-            raise ValueError("SubsampledDctOperator is materialised; use PartialDct2Operator for large D")
-        mask = np.sort(mask)
-        super().__init__(idct(np.eye(dim), axis=0, norm="ortho")[mask, :], device=device)
-        mask.flags.writeable = False
+        mask = _dct_mask(dim, mask)
+        super().__init__(mask.size, dim)
         self.mask = mask
+        self.device = device
+        self._ctx = {}
+
+    def resolve_precision(self, precision):
+        return "fp64" if check_precision(precision) == "auto" else precision
+
+    def context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
+        ctx = self._ctx.get("fft")
+        if ctx is None:
+            ctx = self._ctx["fft"] = self.new_context(precision)
+        return ctx
+
+    def apply_context(self):
+        return self.context()
+
+    def new_context(self, precision="auto"):
+        precision = self.resolve_precision(precision)
+        if precision == "fp32":
+            raise NotImplementedError("1-D DCT dictionaries run the float64 FFT path")
+        return _lib.Context.dct1(self.n_cols, self.mask, _lib.FP64, self.device)
+
+    def release(self):
+        for ctx in self._ctx.values():
+            ctx.close()
+        self._ctx.clear()
+
+    def _apply(self, V):
+        return self.context().apply(V)
+
+    def _apply_adjoint(self, U):
+        return self.context().apply_adjoint(U)
 
     def column_sq_norms(self):
-        """Analytic column norms, operators.py:165-179."""
-        dim = self.n_cols
-        pts = (2.0 * self.mask + 1.0) * (np.pi / (2.0 * dim))
-        scale = np.full(dim, 2.0 / dim)
-        scale[0] = 1.0 / dim
-        out = np.empty(dim)
-        for start in range(0, dim, 512):
-            stop = min(start + 512, dim)
-            c = np.cos(np.outer(np.arange(start, stop), pts))
-            out[start:stop] = scale[start:stop] * np.einsum("ji,ji->j", c, c)
-        return out
+        return _dct1_column_sq_norms(self.n_cols, self.mask)
 
 
 def build_undersampled_dct(dim, n_rows, rng):

@@ -176,6 +176,78 @@ def test_dct_step_sensitivity_is_a_reference_property():
     assert np.abs(O.ozaki_dictionary(phi) - phi).max() <= 2.0**-31
 
 
+def _dct1_packed(D):
+    """Makhoul's packed two-columns-per-complex-FFT DCT-II / DCT-III (the
+    algorithm of csrc/dct1.cuh, numpy FFTs): exact, but rounded differently
+    from scipy's dct / idct."""
+    m = np.arange(D)
+    sig = np.where(m < (D + 1) // 2, 2 * m, 2 * (D - 1 - m) + 1)
+    k = np.arange(D)
+    c = np.full(D, np.sqrt(2.0 / D))
+    c[0] = np.sqrt(1.0 / D)
+    tw = np.exp(-1j * np.pi * k / (2 * D))
+
+    def dct2(a, b):
+        Z = np.fft.fft(a[sig] + 1j * b[sig])
+        Zn = np.conj(Z[(-k) % D])
+        return (tw * (Z + Zn) / 2).real * c, (tw * (Z - Zn) / 2j).real * c
+
+    def idct2(a, b):
+        def spec(X):
+            Xn = np.where(k == 0, 0.0, X[(-k) % D] / c[(-k) % D])
+            return np.conj(tw) * (X / c - 1j * Xn) / D
+        v = np.fft.ifft(spec(a) + 1j * spec(b)) * D
+        xa, xb = np.empty(D), np.empty(D)
+        xa[sig], xb[sig] = v.real, v.imag
+        return xa, xb
+
+    def pairs(f, M):
+        out = np.empty_like(M)
+        for j in range(0, M.shape[1], 2):
+            b = M[:, j + 1] if j + 1 < M.shape[1] else np.zeros(D)
+            ra, rb = f(M[:, j], b)
+            out[:, j] = ra
+            if j + 1 < M.shape[1]:
+                out[:, j + 1] = rb
+        return out
+
+    return (lambda M: pairs(dct2, M)), (lambda M: pairs(idct2, M))
+
+
+def test_dct1_rounding_sensitivity_is_a_reference_property():
+    """The reference recursion on its undersampled-DCT workload
+    (test_cofem.py:257-265, CG tolerance 1e-4) with the dictionary applied by
+    the packed-FFT algorithm of the device's O(D log D) path (exact to 1e-15
+    against scipy) takes a different CG step count in one of the 30 E-steps and
+    lands alpha ~3e-5 away: the basis of the fast path's alpha tolerance in
+    test_gpu_parity::test_reference_dct1d_workload_fast_path."""
+    from scipy.fft import dct, idct
+
+    from conftest import golden
+
+    g = golden("reference_workloads.npz")
+    D = 1024
+    mask = np.sort(g["dct_mask"])
+    fdct, fidct = _dct1_packed(D)
+    V = np.random.default_rng(0).standard_normal((D, 3))
+    assert np.abs(fdct(V) - dct(V, axis=0, norm="ortho")).max() <= 1e-14
+    assert np.abs(fidct(V) - idct(V, axis=0, norm="ortho")).max() <= 1e-14
+    base = O.dct_op(D, mask)
+
+    def adj(U):
+        full = np.zeros((D, U.shape[1]))
+        full[mask] = U
+        return fdct(full)
+
+    op = O.Op(base.n_rows, D, lambda M: fidct(M)[mask], adj, base.col_sq_norms, base.materialize, "dct")
+    cfg = O.CofemConfig(iterations=30, probes=20, seed=0)
+    alpha, mu, _, diag = O.run_cofem(op, g["dct_y"], float(g["dct_beta"]), cfg)
+    steps = np.array([d["cg_steps"] for d in diag])
+    ea = np.linalg.norm(alpha - g["dct_alpha"]) / np.linalg.norm(g["dct_alpha"])
+    assert np.any(steps != g["dct_steps"]) and np.abs(steps - g["dct_steps"]).max() <= 2
+    assert 1e-5 < ea < 3e-4, ea
+
+
 def test_ozaki_model_is_close_to_exact():
     rng = np.random.default_rng(3)
     phi = rng.standard_normal((40, 70)).astype(np.float32).astype(np.float64)
