@@ -343,7 +343,9 @@ class ConvolutionOperator(LinearOperator):
         if check_precision(precision) != "auto":
             return precision
         short = self.n_cols <= AUTO_FP64_CONV_DIM and self.fft_taps().size <= 512
-        return "fp64" if short else "ozaki"
+        # long: the banded int8 tensor-core kernels with 24-bit taps (config 3 at
+        # full size: mu / alpha within 2.3e-6 of the reference's float64 run)
+        return "fp64" if short else "ozaki24"
 
     def context(self, precision="auto"):
         precision = self.resolve_precision(precision)

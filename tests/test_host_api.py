@@ -312,7 +312,7 @@ def test_auto_precision_policy():
     assert DenseOperator(np.zeros((4, 4), dtype=np.float32)).resolve_precision("ozaki") == "ozaki"
     assert ConvolutionOperator(512, 0.04).resolve_precision("auto") == "fp64"
     h = np.exp(-np.arange(256) / 20.0)
-    assert ConvolutionOperator.from_taps(2**22, h).resolve_precision("auto") == "ozaki"
+    assert ConvolutionOperator.from_taps(2**22, h).resolve_precision("auto") == "ozaki24"
     assert PartialDct2Operator(64, np.arange(100)).resolve_precision("auto") == "fp64"
 
 
