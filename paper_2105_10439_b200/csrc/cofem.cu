@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "nccl.h"
 #include "dct.cuh"
+#include "dct1024.cuh"
 #include "dct1.cuh"
 #include <cufft.h>
 #include "ozaki.cuh"
@@ -310,7 +311,10 @@ struct cofem_ctx {
   uint8_t* dct_grid = nullptr;      // n x n 0/1 mask grid [k][l]
   uint8_t* dct_gridT = nullptr;     // its transpose [l][k] (the column pass reads one l at a time)
   double *bufA = nullptr, *bufB = nullptr;  // n x n ldq pass buffers
-  double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n}
+  double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n} / sqrt(2n)
+  // n = 1024 warp-per-FFT passes (dct1024.cuh): lane-contiguous step twiddles and the pair-mask bytes
+  double2* dct_twF = nullptr;
+  uint8_t* dct_pm = nullptr;
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
   // 1-D subsampled DCT (kind 3, dct1.cuh): length D = N_cols, N = mask size;
@@ -1014,7 +1018,7 @@ int conv_bwd_comb(cofem_ctx* c, const double* v, int qoff, double beta, const St
 // dst (D x ldq) = Phi src (adj: Phi^T src) for all ldq columns at once
 int conv_fft_pass(cofem_ctx* c, const double* src, double* dst, bool adj, const Status* stt) {
   constexpr int N1 = 32, N2 = 32, FPI = DCT_FPI, NT = FPI * N2;
-  constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2);
+  constexpr size_t smem = (size_t)FPI * dctf::region_entries(N1, N2) * sizeof(double2);
   static DeviceFlags flags;
   CKR(smem_attr_once(flags, dctf::k_conv_fft_pass<N1, N2>, smem));
   const int L = c->conv_L, valid = CONV_FFT_N - (L - 1);
@@ -1063,7 +1067,7 @@ template <int N1, int N2, int MODE>
 int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
   const int64_t n = c->dct_n, ldq = c->ldq;
   constexpr int FPI = DCT_FPI, NT = FPI * N2;
-  constexpr size_t smem = (size_t)FPI * N1 * (N2 + 1) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
+  constexpr size_t smem = (size_t)FPI * dctf::region_entries(N1, N2) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
   static DeviceFlags flags;
   CKR(smem_attr_once(flags, dctf::k_dct_pass<N1, N2, MODE>, smem));
   const int items = (int)(n * (ldq / (2 * FPI)));
@@ -1077,8 +1081,28 @@ int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const St
   return 0;
 }
 
+// n = 1024: one warp per complex FFT, data in registers (dct1024.cuh)
+template <int MODE>
+int dct_pass_w(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+  const int64_t n = c->dct_n, ldq = c->ldq;
+  static DeviceFlags flags;
+  CKR(smem_attr_once(flags, dctw::k_pass<MODE>, dctw::SMEM));
+  const int items = (int)(n * (ldq / 2));
+  const int grid = std::min((items + dctw::WARPS - 1) / dctw::WARPS, c->sm_count);
+  dctw::k_pass<MODE><<<grid, 32 * dctw::WARPS, dctw::SMEM, c->stream>>>(
+      src, dst, (int)((rows ? n * ldq : ldq) / 2), (int)((rows ? ldq : n * ldq) / 2), (int)n, (int)(ldq / 2), c->dct_twF,
+      c->dct_tw, c->dct_pm, stt);
+  c->launches++;
+  return 0;
+}
+
 template <int MODE>
 int dct_pass(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+  if (c->dct_n == 1024 && c->dct_pm) {
+    CKR((dct_pass_w<MODE>(c, src, dst, rows, stt)));
+    CK(cudaGetLastError());
+    return 0;
+  }
   switch (c->dct_n) {
     case 64: CKR((dct_pass_t<8, 8, MODE>(c, src, dst, rows, stt))); break;
     case 128: CKR((dct_pass_t<8, 16, MODE>(c, src, dst, rows, stt))); break;
@@ -2695,7 +2719,8 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   std::vector<double> cn(n);
   for (int64_t j = 0; j < n; ++j) {
     wN[j] = make_double2(std::cos(2.0 * M_PI * j / n), -std::sin(2.0 * M_PI * j / n));
-    tw[j] = make_double2(std::cos(M_PI * j / (2.0 * n)), -std::sin(M_PI * j / (2.0 * n)));
+    // the Makhoul twiddles carry the pair steps' common scale c_k / 2 = 1 / (c_k n) = 1 / sqrt(2n)
+    tw[j] = make_double2(std::cos(M_PI * j / (2.0 * n)) / std::sqrt(2.0 * n), -std::sin(M_PI * j / (2.0 * n)) / std::sqrt(2.0 * n));
     cn[j] = j == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n);
   }
   for (int j = 0; j < 64; ++j) w64[j] = make_double2(std::cos(2.0 * M_PI * j / 64), -std::sin(2.0 * M_PI * j / 64));
@@ -2715,6 +2740,25 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   for (int64_t k = 0; k < n; ++k)
     for (int64_t l = 0; l < n; ++l) gridT[l * n + k] = grid[k * n + l];
   h2d_sync(c, c->dct_gridT, gridT.data(), gridT.size());
+  if (n == 1024 && getenv("COFEM_DCT_WARP")) {  // tables of the warp-per-FFT passes (dct1024.cuh)
+    std::vector<double2> twF(1024);
+    for (int k2 = 0; k2 < 32; ++k2)
+      for (int lt = 0; lt < 32; ++lt) twF[k2 * 32 + lt] = wN[lt * k2];
+    std::vector<uint8_t> pm((size_t)n * 512);
+    for (int64_t o = 0; o < n; ++o)
+      for (int lt = 0; lt < 32; ++lt)
+        for (int k1 = 0; k1 < 16; ++k1) {
+          const int k = lt + 32 * k1;
+          uint8_t b = gridT[o * n + k];
+          if (k > 0) b |= gridT[o * n + (n - k)] << 1;
+          if (k == 0) b |= gridT[o * n + 512] << 2;
+          pm[(o * 32 + lt) * 16 + k1] = b;
+        }
+    if (cudaMalloc(&c->dct_twF, 1024 * sizeof(double2)) || cudaMalloc(&c->dct_pm, pm.size()))
+      return bail(fail(COFEM_ENOMEM, "DCT tables"));
+    h2d_sync(c, c->dct_twF, twF.data(), 1024 * sizeof(double2));
+    h2d_sync(c, c->dct_pm, pm.data(), pm.size());
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return bail(fail(COFEM_ECUDA, cudaGetErrorString(e)));
   c->have_phi = true;
@@ -2733,7 +2777,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

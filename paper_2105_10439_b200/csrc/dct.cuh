@@ -76,10 +76,13 @@ __device__ __forceinline__ void dft_reg(double2 (&x)[R]) {
         const double2 a = x[b + j], c = x[b + j + s / 2];
         x[b + j] = cadd(a, c);
         const double2 d = csub(a, c);
-        if (j == 0) {
+        const int tj = j * (64 / s);  // twiddle e^{-+ 2 pi i tj / 64}
+        if (tj == 0) {
           x[b + j + s / 2] = d;
+        } else if (tj == 16) {  // -i (forward), +i (inverse): no multiplication
+          x[b + j + s / 2] = SIGN < 0 ? make_double2(d.y, -d.x) : make_double2(-d.y, d.x);
         } else {
-          const double2 w = c_w64[j * (64 / s)];
+          const double2 w = c_w64[tj];
           x[b + j + s / 2] = cmul(d, SIGN < 0 ? w : conj2(w));
         }
       }
@@ -101,6 +104,13 @@ struct Tw1 {
   const double2* wN;
 };
 
+// a group of N2 = 32 threads is one warp and the region is its own: warp-level barriers inside
+template <int N2>
+__device__ __forceinline__ void group_sync() {
+  if (N2 == 32) __syncwarp();
+  else __syncthreads();
+}
+
 template <int N1, int N2, int SIGN>
 __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1) {
   constexpr int B2 = ilog2(N2), B1 = ilog2(N1);
@@ -111,7 +121,7 @@ __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1)
       for (int n2 = 0; n2 < N2; ++n2) r[n2] = z[lt + N1 * n2];
       dft_reg<N2, SIGN>(r);
     }
-    __syncthreads();
+    group_sync<N2>();
     if (lt < N1) {
       const double2 w1 = SIGN < 0 ? tw1.w1 : conj2(tw1.w1);
       double2 cur = make_double2(1.0, 0.0);
@@ -126,13 +136,13 @@ __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1)
         z[lt * (N2 + 1) + k2] = k2 == 0 ? v : cmul(v, cur);
       }
     }
-    __syncthreads();
+    group_sync<N2>();
   }
   double2 s[N1];
 #pragma unroll
   for (int n1 = 0; n1 < N1; ++n1) s[n1] = z[n1 * (N2 + 1) + lt];
   dft_reg<N1, SIGN>(s);
-  __syncthreads();
+  group_sync<N2>();
 #pragma unroll
   for (int k1 = 0; k1 < N1; ++k1) z[lt + N2 * k1] = s[brev(k1, B1)];
   __syncthreads();
@@ -140,34 +150,47 @@ __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1)
 
 enum { P_FWD = 0, P_INV = 1, P_FMI = 2 };  // DCT-II; DCT-III; DCT-II -> mask -> DCT-III
 
-// Orthonormal DCT-II coefficients at k and n-k of the two real vectors
-// packed in the spectrum Z (Z[k], Z[n-k] given): x = (vector a, vector b).
-__device__ __forceinline__ void fwd_post(double2 zk, double2 znk, double2 twk, double2 twnk, double ck, double cnk,
-                                         double2& xk, double2& xnk) {
-  // V_a = (Z[k] + conj Z[n-k]) / 2, V_b = (Z[k] - conj Z[n-k]) / 2i; V[n-k] = conj V[k]
-  const double2 va = make_double2(0.5 * (zk.x + znk.x), 0.5 * (zk.y - znk.y));
-  const double2 vb = make_double2(0.5 * (zk.y + znk.y), -0.5 * (zk.x - znk.x));
-  xk = make_double2(ck * (twk.x * va.x - twk.y * va.y), ck * (twk.x * vb.x - twk.y * vb.y));
-  xnk = make_double2(cnk * (twnk.x * va.x + twnk.y * va.y), cnk * (twnk.x * vb.x + twnk.y * vb.y));
+__device__ __forceinline__ double2 cmulc(double2 a, double2 t) {  // a conj(t)
+  return make_double2(fma(a.x, t.x, a.y * t.y), fma(a.y, t.x, -a.x * t.y));
 }
 
-// Inverse-FFT input at k of one real coefficient vector X:
-// spec(X)[k] = e^{i pi k / 2n} (X[k] / c_k - i X[n-k] / c_{n-k}) / n, X[n] = 0
-__device__ __forceinline__ double2 inv_pre1(double xk, double xnk, double2 twk, double ick, double icnk, double inv_n,
-                                            bool k0) {
-  const double re = xk * ick, im = k0 ? 0.0 : -xnk * icnk;
-  return make_double2((twk.x * re + twk.y * im) * inv_n, (twk.x * im - twk.y * re) * inv_n);
+// The Makhoul pre / post step on one coefficient pair (k, n - k) of the two
+// real vectors packed in a complex FFT; z = value at k, y = value at n - k,
+// t = e^{-i pi k / 2n} / sqrt(2n) (c_k / 2 = 1 / (c_k n) = 1 / sqrt(2n) for k >= 1).
+//   P_FWD: spectrum Z -> orthonormal DCT-II coefficients (X_a, X_b) at k and n - k:
+//          V_a = (Z[k] + conj Z[n-k]) / 2, V_b = (Z[k] - conj Z[n-k]) / 2i,
+//          X[k] = c_k Re(e^{..} V[k]), X[n-k] = -c_k Im(e^{..} V[k])
+//   P_INV: coefficients -> input W of the unnormalised inverse FFT,
+//          W[k] = conj(t) ((a_k + b_{n-k}) + i (b_k - a_{n-k})), W[n-k] = t ((a_k - b_{n-k}) + i (a_{n-k} + b_k))
+//   P_FMI: both with the mask in between.  c_k cancels, and with u = t (2 V[k]):
+//          W_a[k] = conj(t) (m_k Re u_a, m_{n-k} Im u_a), W[n-k] = conj(W[k]) per vector
+// (derivation and a lane-level emulation against scipy: scratch/dctw_emul.py).
+template <int MODE>
+__device__ __forceinline__ void pair_op(double2 z, double2 y, double2 t, bool mk, bool mnk, double2& ok, double2& onk) {
+  if (MODE == P_INV) {
+    const double2 p = make_double2(z.x + y.y, z.y - y.x), q = make_double2(z.x - y.y, y.x + z.y);
+    ok = cmulc(p, t);
+    onk = cmul(q, t);
+    return;
+  }
+  const double2 sa = make_double2(z.x + y.x, z.y - y.y), sb = make_double2(z.y + y.y, y.x - z.x);
+  if (MODE == P_FWD) {
+    ok = make_double2(fma(t.x, sa.x, -t.y * sa.y), fma(t.x, sb.x, -t.y * sb.y));
+    onk = make_double2(-fma(t.y, sa.x, t.x * sa.y), -fma(t.y, sb.x, t.x * sb.y));
+    return;
+  }
+  double2 ua = cmul(sa, t), ub = cmul(sb, t);
+  if (!mk) ua.x = ub.x = 0.0;
+  if (!mnk) ua.y = ub.y = 0.0;
+  const double2 wa = cmulc(ua, t), wb = cmulc(ub, t);
+  ok = make_double2(wa.x - wb.y, wa.y + wb.x);
+  onk = make_double2(wa.x + wb.y, wb.x - wa.y);
 }
-// W = spec(a) + i spec(b) at k and n - k from the coefficient pairs x = (a, b)
-__device__ __forceinline__ void inv_pre(double2 xk, double2 xnk, double2 twk, double2 twnk, double ick, double icnk,
-                                        double inv_n, bool k0, double2& wk, double2& wnk) {
-  const double2 sa = inv_pre1(xk.x, xnk.x, twk, ick, icnk, inv_n, k0);
-  const double2 sb = inv_pre1(xk.y, xnk.y, twk, ick, icnk, inv_n, k0);
-  wk = make_double2(sa.x - sb.y, sa.y + sb.x);
-  const double2 ta = inv_pre1(xnk.x, xk.x, twnk, icnk, ick, inv_n, false);
-  const double2 tb = inv_pre1(xnk.y, xk.y, twnk, icnk, ick, inv_n, false);
-  wnk = make_double2(ta.x - tb.y, ta.y + tb.x);
-}
+
+// complex entries per FFT region: the padded transpose, plus 4 so that the
+// FPI regions start 16 banks apart (adjacent lanes of the pair loops work on
+// the same k in adjacent regions)
+__host__ __device__ constexpr int region_entries(int n1, int n2) { return n1 * (n2 + 1) + 4; }
 
 // One pass over an (nouter x n x ldq) float64 block: item (o, g) transforms
 // the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
@@ -179,25 +202,21 @@ __device__ __forceinline__ void inv_pre(double2 xk, double2 xnk, double2 twk, do
 template <int N1, int N2, int MODE, int FPI = DCT_FPI>
 __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
-               int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tw,
+               int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tws,
                const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
   constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
-  constexpr int ZS = N1 * (N2 + 1);  // complex entries per FFT region (padded transpose)
-  constexpr int KS = NT / FPI;       // k stride between a thread's loop iterations
+  constexpr int ZS = region_entries(N1, N2);
   if (stt && stt->done) return;
   extern __shared__ double2 zsm[];  // [FPI][ZS], then the item's mask column (P_FMI)
   uint8_t* mcol = reinterpret_cast<uint8_t*>(zsm + FPI * ZS);
   const int t = threadIdx.x;
   const int f_own = t / TPF, lt = t % TPF;
-  const double inv_n = 1.0 / N;
-  // thread constants: step-1 twiddles, Makhoul twiddle at k0 = t / FPI and its
-  // step e^{-i pi KS / 2n}; orthonormal scales in closed form
+  // thread constants: step-1 twiddles; the scaled Makhoul twiddles tws[k] = e^{-i pi k / 2n} / sqrt(2n)
+  // come from their (L1-resident) table
   Tw1<N2> tw1;
   tw1.w1 = __ldg(wN + (lt < N1 ? lt : 0));
   tw1.wN = wN;
-  const int k0 = t / FPI;
-  const double2 tw0 = __ldg(tw + k0), tws = __ldg(tw + KS);
-  const double c_0 = sqrt(1.0 / N), c_k = sqrt(2.0 / N);
+  const double dc = 1.0 / sqrt((double)N);  // c_0 = 1 / (c_0 n); folds at compile time
   for (int item = blockIdx.x; item < nouter * ngroups; item += gridDim.x) {
     const int o = item / ngroups, g = item % ngroups;
     const int64_t base = (int64_t)o * stride_o + g * (2 * FPI);
@@ -215,52 +234,54 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    // The pair loops: slot e = (f, kk), kk < n / 2; kk >= 1 is the pair (kk, n - kk), kk = 0
+    // carries the two unpaired coefficients k = 0 and k = n / 2.  In place (pairs are disjoint).
     if (MODE == P_INV) {
-      // W at the pairs (k, n - k), in place (pairs are disjoint across threads)
-      double2 twk = tw0;
-      for (int e = t; e < FPI * (N / 2 + 1); e += NT, twk = cmul(twk, tws)) {
-        const int f = e % FPI, k = e / FPI;
+#pragma unroll(N1 * N2 >= 1024 ? 4 : 2)
+      for (int e = t; e < FPI * (N / 2); e += NT) {
+        const int f = e % FPI, kk = e / FPI;
         double2* z = zsm + f * ZS;
-        const int nk = (N - k) & (N - 1);
-        const double2 twnk = make_double2(-twk.y, -twk.x);  // e^{-i pi (n-k) / 2n} = -i conj(tw_k)
-        double2 wk, wnk;
-        inv_pre(z[k], z[nk], twk, twnk, k == 0 ? 1.0 / c_0 : 1.0 / c_k, nk == 0 ? 1.0 / c_0 : 1.0 / c_k, inv_n,
-                k == 0, wk, wnk);
-        z[k] = wk;
-        if (k != 0 && k != N / 2) z[nk] = wnk;
+        const int k = kk == 0 ? N / 2 : kk, nk = N - k;
+        double2 ok, onk;
+        pair_op<P_INV>(z[k], z[nk], __ldg(tws + k), true, true, ok, onk);
+        z[k] = ok;
+        if (kk == 0) z[0] = make_double2(dc * z[0].x, dc * z[0].y);
+        else z[nk] = onk;
       }
       __syncthreads();
     }
     fft4step<N1, N2, (MODE == P_INV) ? 1 : -1>(zsm + f_own * ZS, lt, tw1);
     if (MODE == P_FWD) {
-      double2 twk = tw0;
-      for (int e = t; e < FPI * N; e += NT, twk = cmul(twk, tws)) {
-        const int f = e % FPI, k = e / FPI;
+#pragma unroll(N1 * N2 >= 1024 ? 4 : 2)
+      for (int e = t; e < FPI * (N / 2); e += NT) {
+        const int f = e % FPI, kk = e / FPI;
         const double2* z = zsm + f * ZS;
-        const int nk = (N - k) & (N - 1);
-        double2 xk, xnk;
-        fwd_post(z[k], z[nk], twk, make_double2(-twk.y, -twk.x), k == 0 ? c_0 : c_k, nk == 0 ? c_0 : c_k, xk, xnk);
-        st_out(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), xk);
+        const int k = kk == 0 ? N / 2 : kk, nk = N - k;
+        double2 ok, onk;
+        pair_op<P_FWD>(z[k], z[nk], __ldg(tws + k), true, true, ok, onk);
+        st_out(reinterpret_cast<double2*>(dst + base + k * stride_m + 2 * f), ok);
+        if (kk == 0) onk = make_double2(dc * z[0].x, dc * z[0].y);
+        st_out(reinterpret_cast<double2*>(dst + base + (kk == 0 ? 0 : nk) * stride_m + 2 * f), onk);
       }
       continue;
     }
     if (MODE == P_FMI) {
-      // coefficients at (k, n - k) -> mask -> inverse-FFT input, in place per pair
-      double2 twk = tw0;
-      for (int e = t; e < FPI * (N / 2 + 1); e += NT, twk = cmul(twk, tws)) {
-        const int f = e % FPI, k = e / FPI;
+      // spectrum -> coefficients -> mask -> inverse-FFT input, in place per pair
+      const double dcm = 1.0 / N;
+#pragma unroll(N1 * N2 >= 1024 ? 4 : 2)
+      for (int e = t; e < FPI * (N / 2); e += NT) {
+        const int f = e % FPI, kk = e / FPI;
         double2* z = zsm + f * ZS;
-        const int nk = (N - k) & (N - 1);
-        const double2 twnk = make_double2(-twk.y, -twk.x);
-        const double ck = k == 0 ? c_0 : c_k, cnk = nk == 0 ? c_0 : c_k;
-        double2 xk, xnk;
-        fwd_post(z[k], z[nk], twk, twnk, ck, cnk, xk, xnk);
-        if (!mcol[k]) xk = make_double2(0.0, 0.0);
-        if (!mcol[nk]) xnk = make_double2(0.0, 0.0);
-        double2 wk, wnk;
-        inv_pre(xk, xnk, twk, twnk, 1.0 / ck, 1.0 / cnk, inv_n, k == 0, wk, wnk);
-        z[k] = wk;
-        if (k != 0 && k != N / 2) z[nk] = wnk;
+        const int k = kk == 0 ? N / 2 : kk, nk = N - k;
+        double2 ok, onk;
+        pair_op<P_FMI>(z[k], z[nk], __ldg(tws + k), mcol[k] != 0, mcol[nk] != 0, ok, onk);
+        z[k] = ok;
+        if (kk == 0) {
+          const double m0 = mcol[0] ? dcm : 0.0;
+          z[0] = make_double2(m0 * z[0].x, m0 * z[0].y);
+        } else {
+          z[nk] = onk;
+        }
       }
       __syncthreads();
       fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, tw1);
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
                     int nblocks, int valid, int in_shift, int keep0, const double2* __restrict__ spec,
                     const double2* __restrict__ wN, const Status* __restrict__ stt) {
   constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
-  constexpr int ZS = N1 * (N2 + 1);
+  constexpr int ZS = region_entries(N1, N2);
   if (stt && stt->done) return;
   extern __shared__ double2 zsm[];
   const int t = threadIdx.x;
