@@ -1913,8 +1913,136 @@ int upload_block(cofem_ctx* c, const double* h, int64_t rows, int64_t q, int64_t
   return 0;
 }
 
+// Host -> device upload of a pitched row block from pageable memory: host
+// threads copy row chunks into two pinned staging buffers while the copy
+// engine drains the other one (pageable cudaMemcpy stages through one driver
+// buffer at ~11 GB/s; this runs at the PCIe rate).
+// the staging buffers (2 x 64 MB) are pinned once per process and reused:
+// page-locking them costs ~70 ms, the upload of a 4.3 GB dictionary then runs
+// at ~42 GB/s; one upload at a time
+struct PinnedPool {
+  std::mutex m;
+  void* buf[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+};
+PinnedPool g_pin;
+
+int upload_rows(cofem_ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch, size_t row_bytes,
+                int64_t rows) {
+  constexpr size_t CHUNK = (size_t)64 << 20;
+  if ((size_t)rows * row_bytes < 2 * CHUNK) {  // small: one pageable copy
+    CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice, c->stream));
+    return 0;
+  }
+  const int64_t rpc = std::max<int64_t>(1, (int64_t)(CHUNK / row_bytes));
+  std::lock_guard<std::mutex> lk(g_pin.m);
+  if (g_pin.bytes < (size_t)rpc * row_bytes) {
+    for (int b = 0; b < 2; ++b)
+      if (g_pin.buf[b]) cudaFreeHost(g_pin.buf[b]);
+    g_pin.buf[0] = g_pin.buf[1] = nullptr;
+    g_pin.bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&g_pin.buf[b], (size_t)rpc * row_bytes, cudaHostAllocPortable) != cudaSuccess)
+        return fail(COFEM_ENOMEM, "pinned staging buffers");
+    g_pin.bytes = (size_t)rpc * row_bytes;
+  }
+  void* pin[2] = {g_pin.buf[0], g_pin.buf[1]};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int rc = 0;
+  for (int b = 0; b < 2 && !rc; ++b) {
+    if (cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(COFEM_ECUDA, "staging events");
+  }
+  const int nthr = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  for (int64_t r0 = 0, i = 0; r0 < rows && !rc; r0 += rpc, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t nr = std::min(rpc, rows - r0);
+    if (i >= 2 && cudaEventSynchronize(ev[b]) != cudaSuccess) rc = fail(COFEM_ECUDA, "staging event");
+    if (rc) break;
+    auto copy = [&](int t) {
+      for (int64_t r = r0 + t; r < r0 + nr; r += nthr)
+        memcpy((char*)pin[b] + (size_t)(r - r0) * row_bytes, (const char*)src + (size_t)r * spitch, row_bytes);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthr; ++t) pool.emplace_back(copy, t);
+    copy(0);
+    for (auto& th : pool) th.join();
+    if (cudaMemcpy2DAsync((char*)dst + (size_t)r0 * dpitch, dpitch, pin[b], row_bytes, row_bytes, nr,
+                          cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaEventRecord(ev[b], c->stream) != cudaSuccess)
+      rc = fail(COFEM_ECUDA, "staged upload");
+  }
+  cudaStreamSynchronize(c->stream);
+  for (int b = 0; b < 2; ++b)
+    if (ev[b]) cudaEventDestroy(ev[b]);
+  return rc;
+}
+
+// Device -> host download of a pitched row block into packed pageable rows, the mirror of
+// upload_rows: the copy engine fills one pinned staging buffer (rows packed by the 2-D copy)
+// while host threads move the other one into the caller's buffer -- a fresh numpy array is
+// untouched memory, and one thread taking its page faults ran a 1 GB block at 1.4 GB/s.
+int download_rows(cofem_ctx* c, void* dst, const void* src, size_t spitch, size_t row_bytes, int64_t rows) {
+  constexpr size_t CHUNK = (size_t)64 << 20;
+  const int64_t rpc = std::max<int64_t>(1, (int64_t)(CHUNK / row_bytes));
+  std::lock_guard<std::mutex> lk(g_pin.m);
+  if (g_pin.bytes < (size_t)rpc * row_bytes) {
+    for (int b = 0; b < 2; ++b)
+      if (g_pin.buf[b]) cudaFreeHost(g_pin.buf[b]);
+    g_pin.buf[0] = g_pin.buf[1] = nullptr;
+    g_pin.bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&g_pin.buf[b], (size_t)rpc * row_bytes, cudaHostAllocPortable) != cudaSuccess)
+        return fail(COFEM_ENOMEM, "pinned staging buffers");
+    g_pin.bytes = (size_t)rpc * row_bytes;
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b)
+    if (cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess) return fail(COFEM_ECUDA, "staging events");
+  const int nthr = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const int64_t nchunks = (rows + rpc - 1) / rpc;
+  int rc = 0;
+  auto issue = [&](int64_t i) {
+    const int b = (int)(i & 1);
+    const int64_t r0 = i * rpc, nr = std::min(rpc, rows - r0);
+    if (cudaMemcpy2DAsync(g_pin.buf[b], row_bytes, (const char*)src + (size_t)r0 * spitch, spitch, row_bytes, nr,
+                          cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaEventRecord(ev[b], c->stream) != cudaSuccess)
+      rc = fail(COFEM_ECUDA, "staged download");
+  };
+  issue(0);
+  for (int64_t i = 0; i < nchunks && !rc; ++i) {
+    const int b = (int)(i & 1);
+    const int64_t r0 = i * rpc, nr = std::min(rpc, rows - r0);
+    if (i + 1 < nchunks) issue(i + 1);  // the other buffer: its previous contents were consumed in trip i - 1
+    if (rc) break;
+    if (cudaEventSynchronize(ev[b]) != cudaSuccess) {
+      rc = fail(COFEM_ECUDA, "staging event");
+      break;
+    }
+    const size_t total = (size_t)nr * row_bytes;
+    char* out = (char*)dst + (size_t)r0 * row_bytes;
+    const char* in = (const char*)g_pin.buf[b];
+    auto copy = [&](int t) {
+      const size_t per = (total / nthr + 4095) & ~(size_t)4095;
+      const size_t a = std::min(total, (size_t)t * per), e = std::min(total, a + per);
+      if (e > a) memcpy(out + a, in + a, e - a);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthr; ++t) pool.emplace_back(copy, t);
+    copy(0);
+    for (auto& th : pool) th.join();
+  }
+  cudaStreamSynchronize(c->stream);
+  for (int b = 0; b < 2; ++b)
+    if (ev[b]) cudaEventDestroy(ev[b]);
+  return rc;
+}
+
 template <typename T>
 int download_block(cofem_ctx* c, const void* src, int64_t rows, int64_t q, int ldq, int qoff, double* h) {
+  if (std::is_same<T, double>::value && (size_t)rows * q * sizeof(double) >= ((size_t)32 << 20))
+    return download_rows(c, h, (const double*)src + qoff, (size_t)ldq * sizeof(double), (size_t)q * sizeof(double), rows);
   std::vector<T> tmp((size_t)rows * ldq);
   CK(cudaMemcpyAsync(tmp.data(), src, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -2793,72 +2921,7 @@ int cofem_destroy(cofem_ctx* c) {
   return 0;
 }
 
-namespace {
-// Host -> device upload of a pitched row block from pageable memory: host
-// threads copy row chunks into two pinned staging buffers while the copy
-// engine drains the other one (pageable cudaMemcpy stages through one driver
-// buffer at ~11 GB/s; this runs at the PCIe rate).
-// the staging buffers (2 x 64 MB) are pinned once per process and reused:
-// page-locking them costs ~70 ms, the upload of a 4.3 GB dictionary then runs
-// at ~42 GB/s; one upload at a time
-struct PinnedPool {
-  std::mutex m;
-  void* buf[2] = {nullptr, nullptr};
-  size_t bytes = 0;
-};
-PinnedPool g_pin;
 
-int upload_rows(cofem_ctx* c, void* dst, size_t dpitch, const void* src, size_t spitch, size_t row_bytes,
-                int64_t rows) {
-  constexpr size_t CHUNK = (size_t)64 << 20;
-  if ((size_t)rows * row_bytes < 2 * CHUNK) {  // small: one pageable copy
-    CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, row_bytes, rows, cudaMemcpyHostToDevice, c->stream));
-    return 0;
-  }
-  const int64_t rpc = std::max<int64_t>(1, (int64_t)(CHUNK / row_bytes));
-  std::lock_guard<std::mutex> lk(g_pin.m);
-  if (g_pin.bytes < (size_t)rpc * row_bytes) {
-    for (int b = 0; b < 2; ++b)
-      if (g_pin.buf[b]) cudaFreeHost(g_pin.buf[b]);
-    g_pin.buf[0] = g_pin.buf[1] = nullptr;
-    g_pin.bytes = 0;
-    for (int b = 0; b < 2; ++b)
-      if (cudaHostAlloc(&g_pin.buf[b], (size_t)rpc * row_bytes, cudaHostAllocPortable) != cudaSuccess)
-        return fail(COFEM_ENOMEM, "pinned staging buffers");
-    g_pin.bytes = (size_t)rpc * row_bytes;
-  }
-  void* pin[2] = {g_pin.buf[0], g_pin.buf[1]};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  int rc = 0;
-  for (int b = 0; b < 2 && !rc; ++b) {
-    if (cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess)
-      rc = fail(COFEM_ECUDA, "staging events");
-  }
-  const int nthr = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  for (int64_t r0 = 0, i = 0; r0 < rows && !rc; r0 += rpc, ++i) {
-    const int b = (int)(i & 1);
-    const int64_t nr = std::min(rpc, rows - r0);
-    if (i >= 2 && cudaEventSynchronize(ev[b]) != cudaSuccess) rc = fail(COFEM_ECUDA, "staging event");
-    if (rc) break;
-    auto copy = [&](int t) {
-      for (int64_t r = r0 + t; r < r0 + nr; r += nthr)
-        memcpy((char*)pin[b] + (size_t)(r - r0) * row_bytes, (const char*)src + (size_t)r * spitch, row_bytes);
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nthr; ++t) pool.emplace_back(copy, t);
-    copy(0);
-    for (auto& th : pool) th.join();
-    if (cudaMemcpy2DAsync((char*)dst + (size_t)r0 * dpitch, dpitch, pin[b], row_bytes, row_bytes, nr,
-                          cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-        cudaEventRecord(ev[b], c->stream) != cudaSuccess)
-      rc = fail(COFEM_ECUDA, "staged upload");
-  }
-  cudaStreamSynchronize(c->stream);
-  for (int b = 0; b < 2; ++b)
-    if (ev[b]) cudaEventDestroy(ev[b]);
-  return rc;
-}
-}  // namespace
 
 int cofem_set_dictionary(cofem_ctx* c, const float* phi, int64_t ld, int on_device) {
   CKR(check_ctx(c, false));

@@ -164,7 +164,7 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 t) {  // a conj(t)
 //          W[k] = conj(t) ((a_k + b_{n-k}) + i (b_k - a_{n-k})), W[n-k] = t ((a_k - b_{n-k}) + i (a_{n-k} + b_k))
 //   P_FMI: both with the mask in between.  c_k cancels, and with u = t (2 V[k]):
 //          W_a[k] = conj(t) (m_k Re u_a, m_{n-k} Im u_a), W[n-k] = conj(W[k]) per vector
-// (derivation and a lane-level emulation against scipy: scratch/dctw_emul.py).
+// (derivation and a lane-level emulation against scipy: tools/dctw_emul.py).
 template <int MODE>
 __device__ __forceinline__ void pair_op(double2 z, double2 y, double2 t, bool mk, bool mnk, double2& ok, double2& onk) {
   if (MODE == P_INV) {
