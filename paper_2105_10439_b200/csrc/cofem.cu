@@ -314,6 +314,7 @@ struct cofem_ctx {
   double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n} / sqrt(2n)
   // n = 1024 warp-per-FFT passes (dct1024.cuh): lane-contiguous step twiddles and the pair-mask bytes
   double2* dct_twF = nullptr;
+  double2* dct_wT = nullptr;  // step twiddles of the N1 x N2 four-step FFT, [k2][lt] = w_n^{lt k2}
   uint8_t* dct_pm = nullptr;
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
@@ -1076,7 +1077,7 @@ int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const St
   const int grid = std::min(items, per_sm * c->sm_count);
   dctf::k_dct_pass<N1, N2, MODE><<<grid, NT, smem, c->stream>>>(
       src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / (2 * FPI)), c->dct_wN, c->dct_tw,
-      c->dct_gridT, stt);
+      c->dct_gridT, stt, c->dct_wT);
   c->launches++;
   return 0;
 }
@@ -1983,7 +1984,9 @@ int upload_rows(cofem_ctx* c, void* dst, size_t dpitch, const void* src, size_t 
 // while host threads move the other one into the caller's buffer -- a fresh numpy array is
 // untouched memory, and one thread taking its page faults ran a 1 GB block at 1.4 GB/s.
 int download_rows(cofem_ctx* c, void* dst, const void* src, size_t spitch, size_t row_bytes, int64_t rows) {
-  constexpr size_t CHUNK = (size_t)64 << 20;
+  // 16 MB chunks: when no dictionary upload has pinned the pool yet, page-locking 2 x 64 MB
+  // (~70 ms) would cost more than the download itself
+  constexpr size_t CHUNK = (size_t)16 << 20;
   const int64_t rpc = std::max<int64_t>(1, (int64_t)(CHUNK / row_bytes));
   std::lock_guard<std::mutex> lk(g_pin.m);
   if (g_pin.bytes < (size_t)rpc * row_bytes) {
@@ -2868,6 +2871,14 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
   for (int64_t k = 0; k < n; ++k)
     for (int64_t l = 0; l < n; ++l) gridT[l * n + k] = grid[k * n + l];
   h2d_sync(c, c->dct_gridT, gridT.data(), gridT.size());
+  {
+    const int n1 = n == 64 ? 8 : n == 128 ? 8 : n == 256 ? 16 : n == 512 ? 16 : 32, n2 = (int)n / n1;
+    std::vector<double2> wT(n);
+    for (int k2 = 0; k2 < n2; ++k2)
+      for (int lt = 0; lt < n1; ++lt) wT[k2 * n1 + lt] = wN[lt * k2];
+    if (cudaMalloc(&c->dct_wT, n * sizeof(double2))) return bail(fail(COFEM_ENOMEM, "DCT tables"));
+    h2d_sync(c, c->dct_wT, wT.data(), n * sizeof(double2));
+  }
   if (n == 1024 && getenv("COFEM_DCT_WARP")) {  // tables of the warp-per-FFT passes (dct1024.cuh)
     std::vector<double2> twF(1024);
     for (int k2 = 0; k2 < 32; ++k2)
@@ -2905,7 +2916,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm, c->dct_wT};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

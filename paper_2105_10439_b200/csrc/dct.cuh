@@ -98,10 +98,13 @@ __device__ __forceinline__ void dft_reg(double2 (&x)[R]) {
 // the block must call it.
 // Step-1 twiddles w_N^{lt k2} of one thread: the table value every 8th k2,
 // powers of the thread constant w1 = w_N^{lt} in between (<= 7 products).
+// With TABLE every twiddle comes from the lane-contiguous table
+// wT[k2 * N1 + lt] instead (independent L1 loads; see DCT_TWT).
 template <int N2>
 struct Tw1 {
   double2 w1;
   const double2* wN;
+  const double2* wT;
 };
 
 // a group of N2 = 32 threads is one warp and the region is its own: warp-level barriers inside
@@ -111,7 +114,7 @@ __device__ __forceinline__ void group_sync() {
   else __syncthreads();
 }
 
-template <int N1, int N2, int SIGN>
+template <int N1, int N2, int SIGN, bool TABLE = false>
 __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1) {
   constexpr int B2 = ilog2(N2), B1 = ilog2(N1);
   {
@@ -127,11 +130,17 @@ __device__ __forceinline__ void fft4step(double2* z, int lt, const Tw1<N2>& tw1)
       double2 cur = make_double2(1.0, 0.0);
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) {
-        if (k2 % 8 == 0) {
+        if (TABLE) {
+          if (k2 > 0) {
+            const double2 w = __ldg(tw1.wT + k2 * N1 + lt);
+            cur = SIGN < 0 ? w : conj2(w);
+          }
+        } else if (k2 % 8 == 0) {
           const double2 w = __ldg(tw1.wN + lt * k2);
           cur = SIGN < 0 ? w : conj2(w);
+        } else {
+          cur = cmul(cur, w1);
         }
-        else cur = cmul(cur, w1);
         const double2 v = r[brev(k2, B2)];
         z[lt * (N2 + 1) + k2] = k2 == 0 ? v : cmul(v, cur);
       }
@@ -196,6 +205,10 @@ __host__ __device__ constexpr int region_entries(int n1, int n2) { return n1 * (
 // the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
 //   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(mask .* DCT-II)
 //   with the transposed 0/1 grid gridT[o n + k] (outer index o, coefficient k along m)
+#ifndef DCT_TWT
+#define DCT_TWT false  // true: every step twiddle from the lane-contiguous table -- measured 13 % slower (column
+                       // pass 0.189 vs 0.167 ms): 31 more L1 loads per FFT cost more than the 28 complex products
+#endif
 #ifndef DCT_FPI
 #define DCT_FPI 2  // complex FFTs (column pairs) per item / block: 2 measured best (4: -7 %, 1: -16 %)
 #endif
@@ -203,7 +216,7 @@ template <int N1, int N2, int MODE, int FPI = DCT_FPI>
 __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
                int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tws,
-               const uint8_t* __restrict__ grid, const Status* __restrict__ stt) {
+               const uint8_t* __restrict__ grid, const Status* __restrict__ stt, const double2* __restrict__ wT) {
   constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
   constexpr int ZS = region_entries(N1, N2);
   if (stt && stt->done) return;
@@ -216,6 +229,7 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
   Tw1<N2> tw1;
   tw1.w1 = __ldg(wN + (lt < N1 ? lt : 0));
   tw1.wN = wN;
+  tw1.wT = wT;
   const double dc = 1.0 / sqrt((double)N);  // c_0 = 1 / (c_0 n); folds at compile time
   for (int item = blockIdx.x; item < nouter * ngroups; item += gridDim.x) {
     const int o = item / ngroups, g = item % ngroups;
@@ -250,7 +264,7 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
       }
       __syncthreads();
     }
-    fft4step<N1, N2, (MODE == P_INV) ? 1 : -1>(zsm + f_own * ZS, lt, tw1);
+    fft4step<N1, N2, (MODE == P_INV) ? 1 : -1, DCT_TWT>(zsm + f_own * ZS, lt, tw1);
     if (MODE == P_FWD) {
 #pragma unroll(N1 * N2 >= 1024 ? 4 : 2)
       for (int e = t; e < FPI * (N / 2); e += NT) {
@@ -284,7 +298,7 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
         }
       }
       __syncthreads();
-      fft4step<N1, N2, 1>(zsm + f_own * ZS, lt, tw1);
+      fft4step<N1, N2, 1, DCT_TWT>(zsm + f_own * ZS, lt, tw1);
     }
     // ---- DCT-III output: x[m] = v[p(m)] (real part: vector 2f, imaginary: 2f + 1)
 #pragma unroll 4
@@ -344,6 +358,7 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
   Tw1<N2> tw1;
   tw1.w1 = __ldg(wN + (lt < N1 ? lt : 0));
   tw1.wN = wN;
+  tw1.wT = nullptr;
   for (int item = blockIdx.x; item < nblocks * ngroups; item += gridDim.x) {
     const int b = item / ngroups, g = item % ngroups;
     const int64_t w0 = (int64_t)b * valid - in_shift;  // first window row

@@ -808,6 +808,25 @@ def test_run_cofem_returns_cg_report_and_wall_times():
     assert all(w > 0 for w in walls) and len(set(walls)) > 1
 
 
+def test_large_solution_block_comes_back_through_the_staged_download():
+    """Result blocks >= 32 MB return through the pinned staging pool (2-D D2H
+    copies, threaded fill of the caller's array; cofem.cu download_rows):
+    config 5's 2^20 x 21 block (176 MB, ldq = 24 on the device) must be the
+    block mu and s were read from."""
+    from paper_2105_10439_b200 import draw_probe_blocks
+
+    c = S.DCT_CONFIGS["dct-large"]
+    prob, _ = S.dct2_problem(c)
+    T = 2
+    st, est, diag = run_cofem(prob, c.cofem_config("auto", iterations=T))
+    prob.op.release()
+    rep = est.cg_report
+    assert rep.solution.shape == (c.D, c.K + 1) and rep.solution.flags.c_contiguous
+    np.testing.assert_allclose(est.mu, c.beta * rep.solution[:, c.K], rtol=1e-13, atol=0)
+    probes = draw_probe_blocks(c.D, c.K, T, c.seed)[-1].astype(np.float64)
+    np.testing.assert_allclose(est.s, (probes * rep.solution[:, :c.K]).mean(axis=1), rtol=1e-10, atol=1e-18)
+
+
 def test_two_devices_threaded_shards():
     """kernels' raised shared-memory limits are per device; shards
     on two GPUs of one process (in-process group, peer reads) must run."""
