@@ -339,3 +339,21 @@ def test_float64_workload_alpha_is_summation_order_sensitive():
     rel_a = np.linalg.norm(a1 - a0) / np.linalg.norm(a0)
     assert 1e-4 < rel_a < 5e-4
     assert np.linalg.norm(mu1 - mu0) / np.linalg.norm(mu0) < 1e-4
+
+
+def test_dct_pair_step_algebra_against_scipy():
+    """The pair-once Makhoul steps the DCT passes implement (csrc/dct.cuh
+    pair_op: c_k cancels in the masked pair, one twiddle scaled 1/sqrt(2n)
+    serves DCT-II post, DCT-III pre and the fused mask step), emulated in
+    numpy in the warp-per-FFT lane / slot distribution, equal scipy's
+    orthonormal DCT-II / DCT-III and DCT-III(mask * DCT-II)."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "dctw_emul.py")
+    spec = importlib.util.spec_from_file_location("dctw_emul", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    for seed in (0, 1):
+        for name, err in mod.check(seed).items():
+            assert err <= 1e-12, (name, err)

@@ -1,4 +1,7 @@
-"""numpy emulation of the warp-per-FFT DCT pass (lane/slot algorithm of csrc/dct1024.cuh)."""
+"""numpy emulation of the Makhoul pair steps of the 2-D DCT passes (csrc/dct.cuh pair_op) in the
+lane / slot distribution of the warp-per-FFT passes (csrc/dct1024.cuh): lane lt holds the 32
+values lt + 32 r, the pair (k, n - k) meets by a lane exchange, lane 0 through a side buffer.
+Test infrastructure (tests/test_host_api.py); nothing in the package imports it."""
 import numpy as np
 from scipy.fft import dct, idct
 N = 1024
@@ -93,15 +96,23 @@ def fmi_item(xa, xb, mask):
     W = pair_loop(s, fn, fix0)
     v = fft_warp(W, +1, 2.0 / N)
     return store_v(v)
-rng = np.random.default_rng(0)
-xa, xb = rng.standard_normal(N), rng.standard_normal(N)
-Xa, Xb = fwd_item(xa, xb)
-print("fwd", np.abs(Xa - dct(xa, norm="ortho")).max(), np.abs(Xb - dct(xb, norm="ortho")).max())
-ya, yb = inv_item(xa, xb)
-print("inv", np.abs(ya - idct(xa, norm="ortho")).max(), np.abs(yb - idct(xb, norm="ortho")).max())
-mask = (rng.random(N) < 0.3).astype(np.uint8)
-za, zb = fmi_item(xa, xb, mask)
-print("fmi", np.abs(za - idct(mask * dct(xa, norm="ortho"), norm="ortho")).max(), np.abs(zb - idct(mask * dct(xb, norm="ortho"), norm="ortho")).max())
-for mm in (np.ones(N, np.uint8), np.zeros(N, np.uint8)):
-    za, zb = fmi_item(xa, xb, mm)
-    print("fmi const", np.abs(za - mm[0] * xa).max())
+def check(seed=0):
+    """max abs errors of the three emulated passes against scipy (orthonormal DCT-II / III)."""
+    rng = np.random.default_rng(seed)
+    xa, xb = rng.standard_normal(N), rng.standard_normal(N)
+    out = {}
+    Xa, Xb = fwd_item(xa, xb)
+    out["fwd"] = max(np.abs(Xa - dct(xa, norm="ortho")).max(), np.abs(Xb - dct(xb, norm="ortho")).max())
+    ya, yb = inv_item(xa, xb)
+    out["inv"] = max(np.abs(ya - idct(xa, norm="ortho")).max(), np.abs(yb - idct(xb, norm="ortho")).max())
+    for name, mask in (("fmi", (rng.random(N) < 0.3).astype(np.uint8)), ("fmi_ones", np.ones(N, np.uint8)),
+                       ("fmi_zeros", np.zeros(N, np.uint8))):
+        za, zb = fmi_item(xa, xb, mask)
+        out[name] = max(np.abs(za - idct(mask * dct(xa, norm="ortho"), norm="ortho")).max(),
+                        np.abs(zb - idct(mask * dct(xb, norm="ortho"), norm="ortho")).max())
+    return out
+
+
+if __name__ == "__main__":
+    for k, v in check().items():
+        print(k, v)
