@@ -378,6 +378,7 @@ struct cofem_ctx {
     s.frozen = frozen;
     s.partials = partials;
     s.ticket = tickets;
+    s.rev_rows = kind == 2 ? 1 : 0;
     return s;
   }
   size_t tsize() const { return prec == COFEM_FP32 ? 4 : 8; }

@@ -24,6 +24,14 @@ struct Scalars {
   int* frozen;      // breakdown flags
   double* partials; // nblocks x 2 x ldq scratch
   unsigned* ticket; // last-block counters (one per reduction site)
+  // Row sweep of k_combine and k_direction: descending when set.  For blocks larger than L2
+  // (the 2-D DCT's 201 MB) the passes alternate direction -- row pass 3 writes Z ascending,
+  // k_combine reads it descending, k_update reads Psi ascending (k_combine finished at the low
+  // rows), k_direction reads R descending, the next row pass reads P ascending -- so every
+  // kernel starts on the rows its producer wrote last (the part of them still in L2:
+  // measured +0.6 % on dct-large, 39.4 -> 39.6 EM it/s; write-back instead of streaming
+  // stores in the passes changes nothing).
+  int rev_rows;
 };
 
 template <typename T>
@@ -166,8 +174,8 @@ __global__ void k_combine(int64_t rows, int ldq, int qoff, int qpc, int nsplit, 
     double al[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {  // issue every load of UNR rows first
-      const int64_t j = j0 + (int64_t)u * m.rstep;
-      if (j < rows) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
         const int64_t e = j * qpc + m.q;
         acc[u] = ppart[e];
         for (int s = 1; s < nsplit; ++s) acc[u] += ppart[(int64_t)s * n + e];
@@ -177,8 +185,8 @@ __global__ void k_combine(int64_t rows, int ldq, int qoff, int qpc, int nsplit, 
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t j = j0 + (int64_t)u * m.rstep;
-      if (j < rows) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
         const T psi = T(beta) * acc[u] + T(al[u]) * p[u];
         Psi[j * ldq + qoff + m.q] = psi;
         s_pi += dd(p[u]) * dd(psi);
@@ -377,8 +385,8 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
     double mv[UNR], pr[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t j = j0 + (int64_t)u * m.rstep;
-      if (j < rows) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
         const int64_t e = j * ldq + q;
         r[u] = R[e];
         p[u] = P[e];
@@ -391,14 +399,14 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
     if (upd_x) {
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const int64_t j = j0 + (int64_t)u * m.rstep;
-        if (j < rows) X[j * ldq + q] = (pair ? x[u] + pp[u] * gp : x[u]) + p[u] * gm;
+        const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+        if (ja < rows) X[j * ldq + q] = (pair ? x[u] + pp[u] * gp : x[u]) + p[u] * gm;
       }
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t j = j0 + (int64_t)u * m.rstep;
-      if (j < rows) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
         const T w = (q < q_real) ? T(dd(r[u]) * mv[u]) : T(0);
         const T pn = p[u] * et + (printed ? r[u] : w);
         Pdst[j * ldq + q] = pn;
