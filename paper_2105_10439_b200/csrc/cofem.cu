@@ -314,7 +314,9 @@ struct cofem_ctx {
   double2 *dct_wN = nullptr, *dct_tw = nullptr;  // e^{-2 pi i j / n}, e^{-i pi k / 2n} / sqrt(2n)
   // n = 1024 warp-per-FFT passes (dct1024.cuh): lane-contiguous step twiddles and the pair-mask bytes
   double2* dct_twF = nullptr;
-  double2* dct_wT = nullptr;  // step twiddles of the N1 x N2 four-step FFT, [k2][lt] = w_n^{lt k2}
+  double2* dct_wT = nullptr;
+  // Psi-free DCT step: vv | <P, alpha P> (VV_MAXQ each) and the last row pass's per-block partial sums
+  double *dct_fscal = nullptr, *dct_partials = nullptr;  // step twiddles of the N1 x N2 four-step FFT, [k2][lt] = w_n^{lt k2}
   uint8_t* dct_pm = nullptr;
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
@@ -1065,20 +1067,22 @@ int conv_fft_system_apply(cofem_ctx* c, double beta, const Status* stt) {
 // ---- 2-D partial DCT: fused float64 FFT passes (dct.cuh) ------------------
 // pass over an n x n x ldq block; row passes run along j (outer i), column
 // passes along i (outer j / l)
-template <int N1, int N2, int MODE>
-int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt) {
+template <int N1, int N2, int MODE, bool VV = false>
+int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const Status* stt,
+               const dctf::VvArgs& vv = dctf::VvArgs()) {
   const int64_t n = c->dct_n, ldq = c->ldq;
   constexpr int FPI = DCT_FPI, NT = FPI * N2;
   constexpr size_t smem = (size_t)FPI * dctf::region_entries(N1, N2) * sizeof(double2) + N1 * N2;  // FFT regions + mask column
+  static_assert(!VV || (size_t)N1 * N2 >= ((NT + 31) / 32) * dctf::VV_MAXQ * sizeof(double), "vv accumulators reuse the mask column");
   static DeviceFlags flags;
-  CKR(smem_attr_once(flags, dctf::k_dct_pass<N1, N2, MODE>, smem));
+  CKR(smem_attr_once(flags, dctf::k_dct_pass<N1, N2, MODE, FPI, VV>, smem));
   const int items = (int)(n * (ldq / (2 * FPI)));
   int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));  // blocks that fit one SM's shared memory
   if (per_sm > 16) per_sm = 16;
   const int grid = std::min(items, per_sm * c->sm_count);
-  dctf::k_dct_pass<N1, N2, MODE><<<grid, NT, smem, c->stream>>>(
+  dctf::k_dct_pass<N1, N2, MODE, FPI, VV><<<grid, NT, smem, c->stream>>>(
       src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / (2 * FPI)), c->dct_wN, c->dct_tw,
-      c->dct_gridT, stt, c->dct_wT);
+      c->dct_gridT, stt, c->dct_wT, vv);
   c->launches++;
   return 0;
 }
@@ -1155,6 +1159,38 @@ int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
       c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->bufA, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
       stt);
   c->launches++;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// The Psi-free PCG step of a 2-D DCT system (one GPU, K + 1 <= 32, n >= 512): the three
+// passes with vv = ||Z||^2 out of the last one, then k_update_psi (pcg.cuh) instead of
+// k_combine + k_update.  bufA <- Z = Phi^T Phi P.  Opt-in (COFEM_DCT_PSIFREE): it moves
+// 0.4 GB less per step and its kernels sum to 55 us less under ncu (735 vs 790 us,
+// profiles/r2af_*), but the live step measured 1.4 % SLOWER (1189 vs 1206 PCG steps/s, also
+// with blocking launches: profiles/r2ag_*) -- unexplained, so the default stays the
+// three-kernel tail.  Parity-green (config 5: alpha 5.4e-5, same steps).
+bool dct_psifree_eligible(const cofem_ctx* c) {
+  return c->kind == 2 && c->nranks <= 1 && c->ldq <= dctf::VV_MAXQ && c->dct_n >= 512 && !c->dct_pm && c->dct_fscal &&
+         getenv("COFEM_DCT_PSIFREE");
+}
+
+int dct_apply_vv(cofem_ctx* c, const Status* stt) {
+  CKR((dct_pass<dctf::P_FWD>(c, (const double*)c->P, c->bufA, true, stt)));
+  if (c->time_kernels) cudaEventRecord(next_event(c), c->stream);
+  CKR((dct_pass<dctf::P_FMI>(c, c->bufA, c->bufB, false, stt)));
+  if (c->time_kernels) {
+    cudaEventRecord(next_event(c), c->stream);
+    c->timed.push_back({0, c->evnext - 2});
+    c->fwd_launches++;
+  }
+  dctf::VvArgs vv;
+  vv.partials = c->dct_partials;
+  vv.ticket = c->tickets + 3;
+  vv.out = c->dct_fscal;
+  vv.ldq = c->ldq;
+  if (c->dct_n == 1024) CKR((dct_pass_t<32, 32, dctf::P_INV, true>(c, c->bufB, c->bufA, true, stt, vv)));
+  else CKR((dct_pass_t<16, 32, dctf::P_INV, true>(c, c->bufB, c->bufA, true, stt, vv)));
   CK(cudaGetLastError());
   return 0;
 }
@@ -1724,6 +1760,9 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
   }
   unsigned long long* pmax = (oz && c->kind != 2) ? c->colmax : nullptr;
   const bool fused = std::is_same<T, double>::value && conv_fused_eligible(c, ngroups);
+  const bool psifree = std::is_same<T, double>::value && dct_psifree_eligible(c);
+  Scalars sc_asc = sc;  // the Psi-free step's direction kernel sweeps ascending (k_update_psi ends at the low rows)
+  sc_asc.rev_rows = 0;
   if (fused) {
     // first direction P(1) = M^-1 B with its planes: the bound is max |M^-1 B| (max |P(0)| = 0)
     CK(cudaMemsetAsync(c->fz_max, 0, 4 * 32 * sizeof(unsigned long long), c->stream));
@@ -1733,6 +1772,12 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
         c->D, ldq, 0, ldq, (const double*)c->R, cg->printed_recursion ? nullptr : c->minv, c->fz_max + 64, c->st);
     c->launches++;
     CKR(conv_fused(c, 3, 0, beta, q_real, cg));
+  } else if (psifree) {
+    k_direction_pap<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+        c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
+        ngroups, groups, sc_asc, c->colscale, pmax, c->st, nullptr, nullptr, nullptr, nullptr, c->alpha,
+        c->dct_fscal + dctf::VV_MAXQ);
+    c->launches++;
   } else {
     k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
@@ -1758,6 +1803,23 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
       CKR(conv_fused(c, 2, u, beta, q_real, cg));
       CKR(conv_fused(c, 3, u, beta, q_real, cg, c->d_hst + slot));
       std::swap(c->P, c->P2);
+      CK(cudaEventRecord(c->ev[slot], c->stream));
+      continue;
+    }
+    if (psifree) {
+      const int slot = u % LAG;
+      CKR(dct_apply_vv(c, c->st));
+      k_update_psi<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
+          c->Dp, ldq, q_real, u & 1, (T*)c->R, (const T*)c->P, (const T*)c->bufA, beta, c->alpha, c->minv, ngroups,
+          groups, c->dct_fscal, c->dct_fscal + dctf::VV_MAXQ, sc, c->st);
+      c->launches++;
+      k_direction_pap<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+          c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
+          c->minv, ngroups, groups, sc_asc, c->colscale, pmax, c->st, c->d_hst + slot, (T*)c->X, (T*)c->P2,
+          (const T*)c->P2, c->alpha, c->dct_fscal + dctf::VV_MAXQ);
+      std::swap(c->P, c->P2);
+      c->launches++;
+      CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev[slot], c->stream));
       continue;
     }
@@ -2880,6 +2942,10 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
     if (cudaMalloc(&c->dct_wT, n * sizeof(double2))) return bail(fail(COFEM_ENOMEM, "DCT tables"));
     h2d_sync(c, c->dct_wT, wT.data(), n * sizeof(double2));
   }
+  if (cudaMalloc(&c->dct_fscal, 2 * dctf::VV_MAXQ * sizeof(double)) ||
+      cudaMalloc(&c->dct_partials, (size_t)16 * c->sm_count * dctf::VV_MAXQ * sizeof(double)))
+    return bail(fail(COFEM_ENOMEM, "DCT step scalars"));
+  cudaMemsetAsync(c->dct_fscal, 0, 2 * dctf::VV_MAXQ * sizeof(double), c->stream);
   if (n == 1024 && getenv("COFEM_DCT_WARP")) {  // tables of the warp-per-FFT passes (dct1024.cuh)
     std::vector<double2> twF(1024);
     for (int k2 = 0; k2 < 32; ++k2)
@@ -2917,7 +2983,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm, c->dct_wT};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm, c->dct_wT, c->dct_fscal, c->dct_partials};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);

@@ -205,6 +205,27 @@ __host__ __device__ constexpr int region_entries(int n1, int n2) { return n1 * (
 // the 8 vectors src[o stride_o + g 8 + m stride_m + v], v < 8, m < n.
 //   P_FWD: dst = DCT-II;  P_INV: dst = DCT-III;  P_FMI: dst = DCT-III(mask .* DCT-II)
 //   with the transposed 0/1 grid gridT[o n + k] (outer index o, coefficient k along m)
+// The last row pass of a PCG apply can also return vv_q = ||Z_q||^2 per column (VV): with
+// orthonormal rows, ||Phi^T Phi P||^2 = ||Phi P||^2, so pi = beta vv + <P, alpha P> is known
+// before Psi exists and the residual update needs no Psi block (k_update_psi, pcg.cuh).
+// A thread's columns are (4 g + 2 f, + 1) with f = lane parity and g changing per item: an
+// item ends with a shuffle fold over the lanes of equal parity into the warp's accumulators
+// in shared memory; the block folds its warps in order, the last block folds the blocks in
+// order (deterministic: the item -> block map is static).
+constexpr int VV_MAXQ = 32;
+struct VvArgs {
+  double* partials = nullptr;  // [grid][ldq]
+  unsigned* ticket = nullptr;
+  double* out = nullptr;       // vv[ldq]
+  int ldq = 0;
+};
+// fold v over the lanes of this lane's parity
+__device__ __forceinline__ double parity_fold(double v) {
+#pragma unroll
+  for (int d = 16; d >= 2; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
 #ifndef DCT_TWT
 #define DCT_TWT false  // true: every step twiddle from the lane-contiguous table -- measured 13 % slower (column
                        // pass 0.189 vs 0.167 ms): 31 more L1 loads per FFT cost more than the 28 complex products
@@ -212,18 +233,24 @@ __host__ __device__ constexpr int region_entries(int n1, int n2) { return n1 * (
 #ifndef DCT_FPI
 #define DCT_FPI 2  // complex FFTs (column pairs) per item / block: 2 measured best (4: -7 %, 1: -16 %)
 #endif
-template <int N1, int N2, int MODE, int FPI = DCT_FPI>
+template <int N1, int N2, int MODE, int FPI = DCT_FPI, bool VV = false>
 __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
     k_dct_pass(const double* __restrict__ src, double* __restrict__ dst, int64_t stride_o, int64_t stride_m,
                int nouter, int ngroups, const double2* __restrict__ wN, const double2* __restrict__ tws,
-               const uint8_t* __restrict__ grid, const Status* __restrict__ stt, const double2* __restrict__ wT) {
+               const uint8_t* __restrict__ grid, const Status* __restrict__ stt, const double2* __restrict__ wT,
+               VvArgs vv = VvArgs()) {
   constexpr int N = N1 * N2, TPF = N2, NT = FPI * TPF;
   constexpr int ZS = region_entries(N1, N2);
+  constexpr int NW = (NT + 31) / 32;
+  static_assert(!VV || (MODE == P_INV && FPI == 2 && NT % 32 == 0), "vv: last row pass, f = lane parity");
   if (stt && stt->done) return;
-  extern __shared__ double2 zsm[];  // [FPI][ZS], then the item's mask column (P_FMI)
+  extern __shared__ double2 zsm[];  // [FPI][ZS], then the item's mask column (P_FMI) / the vv accumulators
   uint8_t* mcol = reinterpret_cast<uint8_t*>(zsm + FPI * ZS);
+  double* wacc = reinterpret_cast<double*>(mcol);  // [NW][VV_MAXQ] (VV: the mask column is unused)
   const int t = threadIdx.x;
   const int f_own = t / TPF, lt = t % TPF;
+  if (VV)
+    for (int i = t; i < NW * VV_MAXQ; i += NT) wacc[i] = 0.0;  // visible after the first item's barriers
   // thread constants: step-1 twiddles; the scaled Makhoul twiddles tws[k] = e^{-i pi k / 2n} / sqrt(2n)
   // come from their (L1-resident) table
   Tw1<N2> tw1;
@@ -301,12 +328,39 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
       fft4step<N1, N2, 1, DCT_TWT>(zsm + f_own * ZS, lt, tw1);
     }
     // ---- DCT-III output: x[m] = v[p(m)] (real part: vector 2f, imaginary: 2f + 1)
+    double sqa = 0.0, sqb = 0.0;
 #pragma unroll 4
     for (int e = t; e < FPI * N; e += NT) {
       const int f = e % FPI, m = e / FPI;
       const double2 v = zsm[f * ZS + ((m & 1) ? N - 1 - (m >> 1) : (m >> 1))];
-      st_out(reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f), v);
+      if (VV) {
+        sqa = fma(v.x, v.x, sqa);
+        sqb = fma(v.y, v.y, sqb);
+        *reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f) = v;  // read again right away: no streaming hint
+      } else {
+        st_out(reinterpret_cast<double2*>(dst + base + m * stride_m + 2 * f), v);
+      }
     }
+    if (VV) {
+      sqa = parity_fold(sqa);
+      sqb = parity_fold(sqb);
+      if ((t & 31) < 2) {  // lane = f
+        double* a = wacc + (t >> 5) * VV_MAXQ + g * (2 * FPI) + 2 * (t & 31);
+        a[0] += sqa;
+        a[1] += sqb;
+      }
+    }
+  }
+  if (VV) {
+    __syncthreads();
+    for (int q = t; q < vv.ldq; q += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += wacc[w * VV_MAXQ + q];
+      vv.partials[(int64_t)blockIdx.x * vv.ldq + q] = s;
+    }
+    double* outs[1] = {vv.out};
+    last_block_reduce(vv.ticket, vv.partials, vv.ldq, 1, outs, reinterpret_cast<double*>(zsm));
   }
 }
 

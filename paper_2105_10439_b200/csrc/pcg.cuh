@@ -281,6 +281,63 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
   last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs, sm_upd);
 }
 
+// ---- the Psi-free residual update of dictionaries with orthonormal rows (the 2-D DCT):
+// pi = beta vv + <P, alpha P> (vv = ||Phi^T Phi P||^2 = ||Phi P||^2 from the last FFT pass, the
+// second term from k_direction<T, true>), gamma = rho / pi, and in ONE pass over Z = Phi^T Phi P,
+// P and R:  R -= gamma (beta Z + alpha .* P), rn2, rho_new -- what k_combine (Psi, pi) and
+// k_update do in two passes and a D x ldq round trip of Psi.
+template <typename T>
+__global__ void k_update_psi(int64_t rows, int ldq, int q_real, int parity, T* R, const T* P, const T* Z, double beta,
+                             const double* alpha, const double* minv, int ngroups, const int* group_of_col,
+                             const double* vv, const double* pap, Scalars sc, const Status* st) {
+  if (st && st->done) return;
+  extern __shared__ double sm_upd[];
+  const ColMap m(ldq);
+  const int q = m.q;
+  const int g = group_of_col ? group_of_col[q] : 0;
+  const double pi = beta * vv[q] + pap[q];
+  const double gamma = safe_ratio(sc.rho[parity][q], pi);
+  if (blockIdx.x == 0 && threadIdx.x < ldq) {
+    if (q < q_real && pi == 0.0) sc.frozen[q] = 1;
+    sc.pi[q] = pi;
+    sc.gam[parity][q] = gamma;  // k_direction's (batched) X update
+  }
+  const T gm = T(gamma);
+  double s_rn = 0.0, s_rho = 0.0;
+  for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
+    T p[UNR], r[UNR], z[UNR];
+    double mv[UNR], al[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
+        const int64_t e = j * ldq + q;
+        p[u] = P[e];
+        r[u] = R[e];
+        z[u] = Z[e];
+        al[u] = alpha[j];
+        mv[u] = minv[j * ngroups + g];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
+      if (ja < rows) {
+        const T psi = T(beta) * z[u] + T(al[u]) * p[u];
+        const T rn = r[u] - psi * gm;
+        R[j * ldq + q] = rn;
+        const double rd = dd(rn);
+        s_rn += rd * rd;
+        if (q < q_real) s_rho += rd * (rd * mv[u]);
+      }
+    }
+  }
+  double vals[2] = {s_rho, s_rn};
+  block_col_reduce(sm_upd, ldq, 2, vals, sc.partials + (int64_t)blockIdx.x * 2 * ldq);
+  double* outs[2] = {sc.rho_new, sc.rn2};
+  last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs, sm_upd);
+}
+
 // ---- convergence test (cg.py:141-148) + direction update (kernels.py
 // step_direction): eta = rho_new / rho (0 when rho == 0), P = P eta + W
 // (or R for the printed recursion), rho <- rho_new.  step == 0 is the
@@ -295,12 +352,14 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
 // steps.  The stopping step applies whatever is pending.  P(u+1) goes to
 // Pdst (nullptr: in place); the host swaps the two direction buffers, so at
 // an even step Pdst == Pprev (each element read before it is overwritten).
-template <typename T>
-__global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
-                            T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
-                            const double* pre, unsigned long long* colmax, Status* st,
-                            const double* agg = nullptr, Status* mirror = nullptr, T* X = nullptr,
-                            T* Pdst = nullptr, const T* Pprev = nullptr) {
+// PAP: also pap_out[q] = <P(u+1)_q, alpha .* P(u+1)_q> (block partials + last-block fold,
+// ticket 5), the second term of pi in the Psi-free step (k_update_psi).
+template <typename T, bool PAP>
+__device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol,
+                                               int printed, T* P, const T* R, const double* minv, int ngroups,
+                                               const int* group_of_col, Scalars sc, const double* pre,
+                                               unsigned long long* colmax, Status* st, const double* agg, Status* mirror,
+                                               T* X, T* Pdst, const T* Pprev, const double* pap_alpha, double* pap_out) {
   // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
   // mirror: host-mapped status slot the host polls (no copy in the stream)
   {
@@ -379,10 +438,10 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
   const bool pair = upd_x && Pprev;
   const T gm = upd_x ? T(sc.gam[cur][q]) : T(0);
   const T gp = pair ? T(sc.gam[nxt][q]) : T(0);
-  double pmax = 0.0;
+  double pmax = 0.0, s_pap = 0.0;
   for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
     T r[UNR], p[UNR], x[UNR], pp[UNR];
-    double mv[UNR], pr[UNR];
+    double mv[UNR], pr[UNR], pa[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
@@ -394,6 +453,7 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
         if (pair) pp[u] = Pprev[e];
         mv[u] = minv[j * ngroups + g];
         pr[u] = colmax ? pre[j] : 0.0;
+        if (PAP) pa[u] = pap_alpha[j];
       }
     }
     if (upd_x) {
@@ -410,6 +470,7 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
         const T w = (q < q_real) ? T(dd(r[u]) * mv[u]) : T(0);
         const T pn = p[u] * et + (printed ? r[u] : w);
         Pdst[j * ldq + q] = pn;
+        if (PAP) s_pap += dd(pn) * (pa[u] * dd(pn));
         if (colmax) {
           const double v = fabs(dd(pn) * pr[u]);
           pmax = (v > pmax || v != v) ? v : pmax;
@@ -419,6 +480,32 @@ __global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max
   }
   if (blockIdx.x == 0 && threadIdx.x < ldq) sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
   if (colmax) block_col_max(sm_dir, ldq, pmax, colmax);
+  if (PAP) {
+    __syncthreads();
+    block_col_reduce(sm_dir, ldq, 1, &s_pap, sc.partials + (int64_t)blockIdx.x * ldq);
+    double* outs[1] = {pap_out};
+    last_block_reduce(sc.ticket + 5, sc.partials, ldq, 1, outs, sm_dir);
+  }
+}
+
+template <typename T>
+__global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed, T* P,
+                            const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
+                            const double* pre, unsigned long long* colmax, Status* st, const double* agg = nullptr,
+                            Status* mirror = nullptr, T* X = nullptr, T* Pdst = nullptr, const T* Pprev = nullptr) {
+  direction_body<T, false>(rows, ldq, q_real, step, max_steps, tol, printed, P, R, minv, ngroups, group_of_col, sc, pre,
+                           colmax, st, agg, mirror, X, Pdst, Pprev, nullptr, nullptr);
+}
+
+// with pap_out; at most 256 threads, and 3 blocks / SM like the plain kernel (one resident wave)
+template <typename T>
+__global__ void __launch_bounds__(256, 3)
+    k_direction_pap(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed, T* P,
+                    const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc, const double* pre,
+                    unsigned long long* colmax, Status* st, Status* mirror, T* X, T* Pdst, const T* Pprev,
+                    const double* pap_alpha, double* pap_out) {
+  direction_body<T, true>(rows, ldq, q_real, step, max_steps, tol, printed, P, R, minv, ngroups, group_of_col, sc, pre,
+                          colmax, st, nullptr, mirror, X, Pdst, Pprev, pap_alpha, pap_out);
 }
 
 // ---- multi-task glue (cofem.py:160-214) -------------------------------------
