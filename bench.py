@@ -454,9 +454,20 @@ def run_ours_conv(args):
             from paper_2105_10439_b200.distributed import run_cofem_sharded
 
             dist.barrier()
+        prof = None
+        if os.environ.get("BENCH_E2E_PROFILE"):  # where the host time of the e2e call goes (stderr)
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         t0 = time.perf_counter()
         st, est, diag = run_cofem_sharded(prob, cfg, device) if dist else run_cofem(prob, cfg)
         el = time.perf_counter() - t0
+        if prof:
+            import pstats
+
+            prof.disable()
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(8)
         if dist:
             t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{device}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
