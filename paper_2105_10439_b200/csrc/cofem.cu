@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -316,7 +317,8 @@ struct cofem_ctx {
   double2* dct_twF = nullptr;
   double2* dct_wT = nullptr;
   // Psi-free DCT step: vv | <P, alpha P> (VV_MAXQ each) and the last row pass's per-block partial sums
-  double *dct_fscal = nullptr, *dct_partials = nullptr;  // step twiddles of the N1 x N2 four-step FFT, [k2][lt] = w_n^{lt k2}
+  double *dct_fscal = nullptr, *dct_partials = nullptr, *dct_partials4 = nullptr;
+  int dct_vv_blocks = 0;  // step twiddles of the N1 x N2 four-step FFT, [k2][lt] = w_n^{lt k2}
   uint8_t* dct_pm = nullptr;
   double* dct_cn = nullptr;                      // orthonormal DCT-II scales c_k
 
@@ -365,6 +367,10 @@ struct cofem_ctx {
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
   std::vector<std::pair<int, size_t>> timed;  // (kind 0 fwd / 1 bwd, event index)
+  // COFEM_TICKS (bench runs): an event after every kernel of the 2-D DCT PCG step; (segment id, event before, event after)
+  bool ticks_on = false;
+  long tick_prev = -1;
+  std::vector<std::array<long, 3>> ticks;
   int64_t launches = 0, fwd_launches = 0, bwd_launches = 0, pcg_steps = 0;
 
   Scalars sc() const {
@@ -411,6 +417,17 @@ cudaEvent_t next_event(cofem_ctx* c) {
     c->evpool.push_back(e);
   }
   return c->evpool[c->evnext++];
+}
+
+// live per-kernel timing of a PCG step (COFEM_TICKS=1 with cofem_bench_iterations(time_kernels)):
+// the segment since the previous tick is charged to `id`; id < 0 only restarts the chain
+void tick(cofem_ctx* c, int id) {
+  if (!c->ticks_on) return;
+  cudaEvent_t e = next_event(c);
+  cudaEventRecord(e, c->stream);
+  const long cur = (long)c->evnext - 1;
+  if (id >= 0 && c->tick_prev >= 0) c->ticks.push_back({(long)id, c->tick_prev, cur});
+  c->tick_prev = cur;
 }
 
 void free_ws(cofem_ctx* c) {
@@ -1080,6 +1097,7 @@ int dct_pass_t(cofem_ctx* c, const double* src, double* dst, bool rows, const St
   int per_sm = std::max(1, (int)((228 * 1024) / (smem + 1024)));  // blocks that fit one SM's shared memory
   if (per_sm > 16) per_sm = 16;
   const int grid = std::min(items, per_sm * c->sm_count);
+  if (VV) c->dct_vv_blocks = grid;
   dctf::k_dct_pass<N1, N2, MODE, FPI, VV><<<grid, NT, smem, c->stream>>>(
       src, dst, rows ? n * ldq : ldq, rows ? ldq : n * ldq, (int)n, (int)(ldq / (2 * FPI)), c->dct_wN, c->dct_tw,
       c->dct_gridT, stt, c->dct_wT, vv);
@@ -1136,7 +1154,9 @@ int dct_adjoint_dev(cofem_ctx* c, double* out, const Status* stt) {
 // Psi = beta Phi^T Phi P + alpha .* P for all ldq columns at once, pi on the
 // fly: row DCT-II, fused column DCT-II / mask / DCT-III, row DCT-III + combine
 int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
+  tick(c, -1);
   CKR((dct_pass<dctf::P_FWD>(c, (const double*)c->P, c->bufA, true, stt)));
+  tick(c, 0);
   cudaEvent_t e0 = nullptr;
   if (c->time_kernels) {
     e0 = next_event(c);
@@ -1150,33 +1170,37 @@ int dct_system_apply(cofem_ctx* c, double beta, const Status* stt) {
     c->fwd_launches++;
   }
   (void)e0;
+  tick(c, 1);
   // the row DCT-III writes Z; Psi = beta Z + alpha .* P and pi in the streaming
   // combine (fusing it into the pass stalls the FFT pipeline on the P loads)
   CKR((dct_pass<dctf::P_INV>(c, c->bufB, c->bufA, true, stt)));
+  tick(c, 2);
   Scalars sc = c->sc();
   const int bs = elem_block(c->ldq);
   k_combine<double><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
       c->Dp, c->ldq, 0, c->ldq, 1, (const double*)c->bufA, beta, c->alpha, (const double*)c->P, (double*)c->Psi, sc,
       stt);
   c->launches++;
+  tick(c, 3);
   CK(cudaGetLastError());
   return 0;
 }
 
 // The Psi-free PCG step of a 2-D DCT system (one GPU, K + 1 <= 32, n >= 512): the three
 // passes with vv = ||Z||^2 out of the last one, then k_update_psi (pcg.cuh) instead of
-// k_combine + k_update.  bufA <- Z = Phi^T Phi P.  Opt-in (COFEM_DCT_PSIFREE): it moves
-// 0.4 GB less per step and its kernels sum to 55 us less under ncu (735 vs 790 us,
-// profiles/r2af_*), but the live step measured 1.4 % SLOWER (1189 vs 1206 PCG steps/s, also
-// with blocking launches: profiles/r2ag_*) -- unexplained, so the default stays the
-// three-kernel tail.  Parity-green (config 5: alpha 5.4e-5, same steps).
+// k_combine + k_update.  bufA <- Z = Phi^T Phi P.  0.4 GB less per step.  (A first version
+// took <P, alpha P> from a direction kernel with one more reduction: that kernel ran 77 us
+// slower live than under ncu -- COFEM_TICKS, profiles/r2aj_* -- and the step lost 1.4 %; now
+// the term follows the direction recurrence from two inner products of k_update_psi.)
 bool dct_psifree_eligible(const cofem_ctx* c) {
   return c->kind == 2 && c->nranks <= 1 && c->ldq <= dctf::VV_MAXQ && c->dct_n >= 512 && !c->dct_pm && c->dct_fscal &&
-         getenv("COFEM_DCT_PSIFREE");
+         !getenv("COFEM_DCT_PSI");
 }
 
 int dct_apply_vv(cofem_ctx* c, const Status* stt) {
+  tick(c, -1);
   CKR((dct_pass<dctf::P_FWD>(c, (const double*)c->P, c->bufA, true, stt)));
+  tick(c, 0);
   if (c->time_kernels) cudaEventRecord(next_event(c), c->stream);
   CKR((dct_pass<dctf::P_FMI>(c, c->bufA, c->bufB, false, stt)));
   if (c->time_kernels) {
@@ -1184,13 +1208,13 @@ int dct_apply_vv(cofem_ctx* c, const Status* stt) {
     c->timed.push_back({0, c->evnext - 2});
     c->fwd_launches++;
   }
+  tick(c, 1);
   dctf::VvArgs vv;
   vv.partials = c->dct_partials;
-  vv.ticket = c->tickets + 3;
-  vv.out = c->dct_fscal;
   vv.ldq = c->ldq;
   if (c->dct_n == 1024) CKR((dct_pass_t<32, 32, dctf::P_INV, true>(c, c->bufB, c->bufA, true, stt, vv)));
   else CKR((dct_pass_t<16, 32, dctf::P_INV, true>(c, c->bufB, c->bufA, true, stt, vv)));
+  tick(c, 2);
   CK(cudaGetLastError());
   return 0;
 }
@@ -1773,11 +1797,13 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     c->launches++;
     CKR(conv_fused(c, 3, 0, beta, q_real, cg));
   } else if (psifree) {
-    k_direction_pap<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+    k_pap_init<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+        c->Dp, ldq, q_real, cg->printed_recursion, (const T*)c->R, c->alpha, c->minv, ngroups, groups, c->dct_fscal,
+        c->dct_partials4, sc);
+    k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
-        ngroups, groups, sc_asc, c->colscale, pmax, c->st, nullptr, nullptr, nullptr, nullptr, c->alpha,
-        c->dct_fscal + dctf::VV_MAXQ);
-    c->launches++;
+        ngroups, groups, sc_asc, c->colscale, pmax, c->st);
+    c->launches += 2;
   } else {
     k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
         c->Dp, ldq, q_real, 0, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R, c->minv,
@@ -1809,16 +1835,18 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
     if (psifree) {
       const int slot = u % LAG;
       CKR(dct_apply_vv(c, c->st));
-      k_update_psi<T><<<c->nblk_elem, bs, 2 * bs * sizeof(double), c->stream>>>(
-          c->Dp, ldq, q_real, u & 1, (T*)c->R, (const T*)c->P, (const T*)c->bufA, beta, c->alpha, c->minv, ngroups,
-          groups, c->dct_fscal, c->dct_fscal + dctf::VV_MAXQ, sc, c->st);
+      k_update_psi<T><<<c->nblk_elem, bs, 4 * bs * sizeof(double), c->stream>>>(
+          c->Dp, ldq, q_real, u, cg->printed_recursion, (T*)c->R, (const T*)c->P, (const T*)c->bufA, beta, c->alpha,
+          c->minv, ngroups, groups, c->dct_partials, c->dct_vv_blocks, c->dct_fscal, c->dct_partials4, sc, c->st);
       c->launches++;
-      k_direction_pap<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
+      tick(c, 4);
+      k_direction<T><<<c->nblk_elem, bs, bs * sizeof(double), c->stream>>>(
           c->Dp, ldq, q_real, u, cg->max_steps, cg->tolerance, cg->printed_recursion, (T*)c->P, (const T*)c->R,
-          c->minv, ngroups, groups, sc_asc, c->colscale, pmax, c->st, c->d_hst + slot, (T*)c->X, (T*)c->P2,
-          (const T*)c->P2, c->alpha, c->dct_fscal + dctf::VV_MAXQ);
+          c->minv, ngroups, groups, sc_asc, c->colscale, pmax, c->st, nullptr, c->d_hst + slot, (T*)c->X, (T*)c->P2,
+          (const T*)c->P2);
       std::swap(c->P, c->P2);
       c->launches++;
+      tick(c, 5);
       CK(cudaGetLastError());
       CK(cudaEventRecord(c->ev[slot], c->stream));
       continue;
@@ -1829,6 +1857,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
         c->Dp, ldq, q_real, u & 1, nullptr, (T*)c->R, (const T*)c->P, (const T*)c->Psi, c->minv, ngroups, groups,
         sc, pmax, c->st);
     c->launches++;
+    tick(c, 4);
     CK(cudaGetLastError());
     CKR(allreduce(c, sc.rho_new, 2 * ldq, ncclFloat64));  // rho_new | rn2
     const int slot = u % LAG;
@@ -1839,6 +1868,7 @@ int pcg_device(cofem_ctx* c, double beta, int q_real, int ngroups, const int* gr
         (const T*)c->P2);
     std::swap(c->P, c->P2);  // P(u+1) is the next step's direction
     c->launches++;
+    tick(c, 5);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[slot], c->stream));
   }
@@ -2942,10 +2972,11 @@ int cofem_create_dct2(cofem_ctx** out, int device, int64_t n, const int64_t* mas
     if (cudaMalloc(&c->dct_wT, n * sizeof(double2))) return bail(fail(COFEM_ENOMEM, "DCT tables"));
     h2d_sync(c, c->dct_wT, wT.data(), n * sizeof(double2));
   }
-  if (cudaMalloc(&c->dct_fscal, 2 * dctf::VV_MAXQ * sizeof(double)) ||
-      cudaMalloc(&c->dct_partials, (size_t)16 * c->sm_count * dctf::VV_MAXQ * sizeof(double)))
+  if (cudaMalloc(&c->dct_fscal, 4 * PSQ * sizeof(double)) ||
+      cudaMalloc(&c->dct_partials, (size_t)16 * c->sm_count * dctf::VV_MAXQ * sizeof(double)) ||
+      cudaMalloc(&c->dct_partials4, (size_t)3 * c->sm_count * 4 * PSQ * sizeof(double)))
     return bail(fail(COFEM_ENOMEM, "DCT step scalars"));
-  cudaMemsetAsync(c->dct_fscal, 0, 2 * dctf::VV_MAXQ * sizeof(double), c->stream);
+  cudaMemsetAsync(c->dct_fscal, 0, 4 * PSQ * sizeof(double), c->stream);
   if (n == 1024 && getenv("COFEM_DCT_WARP")) {  // tables of the warp-per-FFT passes (dct1024.cuh)
     std::vector<double2> twF(1024);
     for (int k2 = 0; k2 < 32; ++k2)
@@ -2983,7 +3014,7 @@ int cofem_destroy(cofem_ctx* c) {
                   c->probes, c->probe_store, c->groups, c->tickets, c->st, c->phiq, c->phiqT, c->rowscale, c->colscale,
                   c->pq_base ? c->pq_base : c->pq, c->vq, c->opscale, c->colmax, c->vcolmax, c->band_fwd, c->band_adj, c->hrows,
                   c->dct_mask, c->dct_grid, c->dct_gridT, c->bufA, c->bufB, c->dct_wN, c->dct_tw, c->dct_cn,
-                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm, c->dct_wT, c->dct_fscal, c->dct_partials};
+                  c->cf_H, c->cf_Hr, c->lg_tmp, c->fz_max, c->dct1_mv, c->dct_twF, c->dct_pm, c->dct_wT, c->dct_fscal, c->dct_partials, c->dct_partials4};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -3447,6 +3478,9 @@ int cofem_bench_iterations(cofem_ctx* c, int n_iter, int time_kernels, cofem_tim
   c->time_kernels = time_kernels != 0;
   c->evnext = 0;
   c->timed.clear();
+  c->ticks.clear();
+  c->tick_prev = -1;
+  c->ticks_on = time_kernels && c->kind == 2 && getenv("COFEM_TICKS");
   c->launches = c->fwd_launches = c->bwd_launches = c->pcg_steps = 0;
   c->ph_fwd_ms = c->ph_bwd_ms = 0;
   c->solve_launches = 0;
@@ -3471,6 +3505,20 @@ int cofem_bench_iterations(cofem_ctx* c, int n_iter, int time_kernels, cofem_tim
     if (tk.first == 0) out->fwd_ms += d;
     else if (tk.first == 1) out->bwd_ms += d;
     else out->solve_ms += d;
+  }
+  if (c->ticks_on) {  // live per-kernel times of the DCT step, kernels that ran (early exits excluded)
+    static const char* names[] = {"row DCT-II", "column pass", "row DCT-III", "k_combine", "k_update(_psi)", "k_direction(_pap)"};
+    double sum[6] = {0}, all = 0;
+    long n[6] = {0};
+    for (auto& tk : c->ticks) {
+      float d = 0;
+      cudaEventElapsedTime(&d, c->evpool[tk[1]], c->evpool[tk[2]]);
+      if (d > 0.02f) sum[tk[0]] += d, n[tk[0]]++;
+    }
+    for (int i = 0; i < 6; ++i)
+      if (n[i]) fprintf(stderr, "[ticks] %-18s n=%5ld avg %7.1f us\n", names[i], n[i], 1e3 * sum[i] / n[i]), all += sum[i] / n[i];
+    fprintf(stderr, "[ticks] step (sum of averages) %7.1f us\n", 1e3 * all);
+    c->ticks_on = false;
   }
   out->fwd_ms += c->ph_fwd_ms;  // contraction phases of persistent solves (globaltimer stamps)
   out->bwd_ms += c->ph_bwd_ms;

@@ -210,13 +210,12 @@ __host__ __device__ constexpr int region_entries(int n1, int n2) { return n1 * (
 // before Psi exists and the residual update needs no Psi block (k_update_psi, pcg.cuh).
 // A thread's columns are (4 g + 2 f, + 1) with f = lane parity and g changing per item: an
 // item ends with a shuffle fold over the lanes of equal parity into the warp's accumulators
-// in shared memory; the block folds its warps in order, the last block folds the blocks in
-// order (deterministic: the item -> block map is static).
+// in shared memory; the block folds its warps in order and writes partials[block][q]; the
+// consumer (k_update_psi) folds the blocks in order (deterministic: the item -> block map is
+// static; a last-block fold by this kernel's 64-thread blocks cost 20 us of serial tail).
 constexpr int VV_MAXQ = 32;
 struct VvArgs {
   double* partials = nullptr;  // [grid][ldq]
-  unsigned* ticket = nullptr;
-  double* out = nullptr;       // vv[ldq]
   int ldq = 0;
 };
 // fold v over the lanes of this lane's parity
@@ -359,8 +358,6 @@ __global__ void __launch_bounds__(FPI * N2, (N2 >= 32 ? 12 / FPI : 16 / FPI))
       for (int w = 0; w < NW; ++w) s += wacc[w * VV_MAXQ + q];
       vv.partials[(int64_t)blockIdx.x * vv.ldq + q] = s;
     }
-    double* outs[1] = {vv.out};
-    last_block_reduce(vv.ticket, vv.partials, vv.ldq, 1, outs, reinterpret_cast<double*>(zsm));
   }
 }
 

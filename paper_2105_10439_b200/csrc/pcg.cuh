@@ -281,29 +281,59 @@ __global__ void k_update(int64_t rows, int ldq, int q_real, int parity, T* X, T*
   last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs, sm_upd);
 }
 
-// ---- the Psi-free residual update of dictionaries with orthonormal rows (the 2-D DCT):
-// pi = beta vv + <P, alpha P> (vv = ||Phi^T Phi P||^2 = ||Phi P||^2 from the last FFT pass, the
-// second term from k_direction<T, true>), gamma = rho / pi, and in ONE pass over Z = Phi^T Phi P,
-// P and R:  R -= gamma (beta Z + alpha .* P), rn2, rho_new -- what k_combine (Psi, pi) and
-// k_update do in two passes and a D x ldq round trip of Psi.
+// ---- the Psi-free residual update of dictionaries with orthonormal rows (the 2-D DCT).
+// pi = beta vv + pap with vv = ||Phi^T Phi P||^2 = ||Phi P||^2 (per-block sums of Z^2 from the
+// last FFT pass, folded here in block order by every block: no serial fold at the pass's end) and
+// pap = <P, alpha P>, carried by the direction recurrence P(u+1) = eta P(u) + W(u):
+//   pap(u+1) = eta^2 pap(u) + 2 eta <P(u), alpha W(u)> + <W(u), alpha W(u)>
+// whose two inner products this kernel returns (it holds P, the new R and alpha anyway; W =
+// M^-1 R, or R for the printed recursion), so the direction kernel is unchanged.  Then
+// gamma = rho / pi and, in ONE pass over Z, P and R:  R -= gamma (beta Z + alpha .* P), rn2,
+// rho_new -- what k_combine (Psi, pi) and k_update do in two passes and a D x ldq round trip.
+// State `ps` (per column, stride PSQ): pap by step parity [0], [1]; s1 [2]; s2 [3].
+constexpr int PSQ = 32;
 template <typename T>
-__global__ void k_update_psi(int64_t rows, int ldq, int q_real, int parity, T* R, const T* P, const T* Z, double beta,
-                             const double* alpha, const double* minv, int ngroups, const int* group_of_col,
-                             const double* vv, const double* pap, Scalars sc, const Status* st) {
+__global__ void k_update_psi(int64_t rows, int ldq, int q_real, int step, int printed, T* R, const T* P, const T* Z,
+                             double beta, const double* alpha, const double* minv, int ngroups,
+                             const int* group_of_col, const double* vv_partials, int vv_blocks, double* ps,
+                             double* partials4, Scalars sc, const Status* st) {
   if (st && st->done) return;
   extern __shared__ double sm_upd[];
   const ColMap m(ldq);
-  const int q = m.q;
+  const int q = m.q, parity = step & 1;
   const int g = group_of_col ? group_of_col[q] : 0;
-  const double pi = beta * vv[q] + pap[q];
+  // vv_q: the pass's block partials, thread-row rs sums blocks rs, rs + rpb, ..., then the rows in order
+  {
+    const int rpb = blockDim.x / ldq, rs = threadIdx.x / ldq;
+    double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // 8 independent L2 loads in flight
+    int b2 = rs;
+    for (; b2 + 7 * rpb < vv_blocks; b2 += 8 * rpb) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a8[u] += __ldcg(vv_partials + (int64_t)(b2 + u * rpb) * ldq + q);
+    }
+    for (int u = 0; b2 < vv_blocks; b2 += rpb, ++u) a8[u] += __ldcg(vv_partials + (int64_t)b2 * ldq + q);
+    sm_upd[threadIdx.x] = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+    __syncthreads();
+    double v = 0.0;
+    for (int r2 = 0; r2 < rpb; ++r2) v += sm_upd[r2 * ldq + q];
+    __syncthreads();
+    sm_upd[threadIdx.x] = v;  // every thread of column q holds vv_q
+  }
+  const double vvq = sm_upd[threadIdx.x];
+  __syncthreads();
+  // eta of the previous direction step: rho(u) / rho(u-1), both still in the parity buffers
+  const double eta = safe_ratio(sc.rho[parity][q], sc.rho[parity ^ 1][q]);
+  const double pap = step == 1 ? ps[3 * PSQ + q] : (eta * eta) * ps[(parity ^ 1) * PSQ + q] + (2.0 * eta) * ps[2 * PSQ + q] + ps[3 * PSQ + q];
+  const double pi = beta * vvq + pap;
   const double gamma = safe_ratio(sc.rho[parity][q], pi);
   if (blockIdx.x == 0 && threadIdx.x < ldq) {
     if (q < q_real && pi == 0.0) sc.frozen[q] = 1;
     sc.pi[q] = pi;
     sc.gam[parity][q] = gamma;  // k_direction's (batched) X update
+    ps[parity * PSQ + q] = pap;
   }
   const T gm = T(gamma);
-  double s_rn = 0.0, s_rho = 0.0;
+  double s_rn = 0.0, s_rho = 0.0, s1 = 0.0, s2 = 0.0;
   for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
     T p[UNR], r[UNR], z[UNR];
     double mv[UNR], al[UNR];
@@ -328,14 +358,40 @@ __global__ void k_update_psi(int64_t rows, int ldq, int q_real, int parity, T* R
         R[j * ldq + q] = rn;
         const double rd = dd(rn);
         s_rn += rd * rd;
-        if (q < q_real) s_rho += rd * (rd * mv[u]);
+        const double w = q < q_real ? rd * mv[u] : 0.0;
+        s_rho += rd * w;
+        const double wd = printed ? rd : w, aw = al[u] * wd;
+        s1 += dd(p[u]) * aw;
+        s2 += wd * aw;
       }
     }
   }
-  double vals[2] = {s_rho, s_rn};
-  block_col_reduce(sm_upd, ldq, 2, vals, sc.partials + (int64_t)blockIdx.x * 2 * ldq);
-  double* outs[2] = {sc.rho_new, sc.rn2};
-  last_block_reduce(sc.ticket + 2, sc.partials, ldq, 2, outs, sm_upd);
+  double vals[4] = {s_rho, s_rn, s1, s2};
+  block_col_reduce(sm_upd, ldq, 4, vals, partials4 + (int64_t)blockIdx.x * 4 * ldq);
+  double* outs[4] = {sc.rho_new, sc.rn2, ps + 2 * PSQ, ps + 3 * PSQ};
+  last_block_reduce(sc.ticket + 2, partials4, ldq, 4, outs, sm_upd);
+}
+
+// start of a Psi-free solve: s2 = <W, alpha W> of W = M^-1 B (B for the printed recursion), the
+// first direction; pap(0) = s1 = 0
+template <typename T>
+__global__ void k_pap_init(int64_t rows, int ldq, int q_real, int printed, const T* R, const double* alpha,
+                           const double* minv, int ngroups, const int* group_of_col, double* ps, double* partials4,
+                           Scalars sc) {
+  extern __shared__ double sm_upd[];
+  const ColMap m(ldq);
+  const int q = m.q;
+  const int g = group_of_col ? group_of_col[q] : 0;
+  double s2 = 0.0;
+  for (int64_t j = m.r0; j < rows; j += m.rstep) {
+    const double rd = dd(R[j * ldq + q]);
+    const double wd = printed ? rd : (q < q_real ? rd * minv[j * ngroups + g] : 0.0);
+    s2 += wd * (alpha[j] * wd);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ldq) ps[q] = ps[PSQ + q] = ps[2 * PSQ + q] = 0.0;
+  block_col_reduce(sm_upd, ldq, 1, &s2, partials4 + (int64_t)blockIdx.x * ldq);
+  double* outs[1] = {ps + 3 * PSQ};
+  last_block_reduce(sc.ticket + 5, partials4, ldq, 1, outs, sm_upd);
 }
 
 // ---- convergence test (cg.py:141-148) + direction update (kernels.py
@@ -352,14 +408,12 @@ __global__ void k_update_psi(int64_t rows, int ldq, int q_real, int parity, T* R
 // steps.  The stopping step applies whatever is pending.  P(u+1) goes to
 // Pdst (nullptr: in place); the host swaps the two direction buffers, so at
 // an even step Pdst == Pprev (each element read before it is overwritten).
-// PAP: also pap_out[q] = <P(u+1)_q, alpha .* P(u+1)_q> (block partials + last-block fold,
-// ticket 5), the second term of pi in the Psi-free step (k_update_psi).
-template <typename T, bool PAP>
-__device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol,
-                                               int printed, T* P, const T* R, const double* minv, int ngroups,
-                                               const int* group_of_col, Scalars sc, const double* pre,
-                                               unsigned long long* colmax, Status* st, const double* agg, Status* mirror,
-                                               T* X, T* Pdst, const T* Pprev, const double* pap_alpha, double* pap_out) {
+template <typename T>
+__global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed,
+                            T* P, const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
+                            const double* pre, unsigned long long* colmax, Status* st,
+                            const double* agg = nullptr, Status* mirror = nullptr, T* X = nullptr,
+                            T* Pdst = nullptr, const T* Pprev = nullptr) {
   // agg (multi-task solves): {sum ||R||^2, sum ||B||^2} over every task's columns
   // mirror: host-mapped status slot the host polls (no copy in the stream)
   {
@@ -438,10 +492,10 @@ __device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real
   const bool pair = upd_x && Pprev;
   const T gm = upd_x ? T(sc.gam[cur][q]) : T(0);
   const T gp = pair ? T(sc.gam[nxt][q]) : T(0);
-  double pmax = 0.0, s_pap = 0.0;
+  double pmax = 0.0;
   for (int64_t j0 = m.r0; j0 < rows; j0 += UNR * (int64_t)m.rstep) {
     T r[UNR], p[UNR], x[UNR], pp[UNR];
-    double mv[UNR], pr[UNR], pa[UNR];
+    double mv[UNR], pr[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int64_t ja = j0 + (int64_t)u * m.rstep, j = sc.rev_rows ? rows - 1 - ja : ja;
@@ -453,7 +507,6 @@ __device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real
         if (pair) pp[u] = Pprev[e];
         mv[u] = minv[j * ngroups + g];
         pr[u] = colmax ? pre[j] : 0.0;
-        if (PAP) pa[u] = pap_alpha[j];
       }
     }
     if (upd_x) {
@@ -470,7 +523,6 @@ __device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real
         const T w = (q < q_real) ? T(dd(r[u]) * mv[u]) : T(0);
         const T pn = p[u] * et + (printed ? r[u] : w);
         Pdst[j * ldq + q] = pn;
-        if (PAP) s_pap += dd(pn) * (pa[u] * dd(pn));
         if (colmax) {
           const double v = fabs(dd(pn) * pr[u]);
           pmax = (v > pmax || v != v) ? v : pmax;
@@ -480,32 +532,6 @@ __device__ __forceinline__ void direction_body(int64_t rows, int ldq, int q_real
   }
   if (blockIdx.x == 0 && threadIdx.x < ldq) sc.rho[nxt][threadIdx.x] = sc.rho_new[threadIdx.x];
   if (colmax) block_col_max(sm_dir, ldq, pmax, colmax);
-  if (PAP) {
-    __syncthreads();
-    block_col_reduce(sm_dir, ldq, 1, &s_pap, sc.partials + (int64_t)blockIdx.x * ldq);
-    double* outs[1] = {pap_out};
-    last_block_reduce(sc.ticket + 5, sc.partials, ldq, 1, outs, sm_dir);
-  }
-}
-
-template <typename T>
-__global__ void k_direction(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed, T* P,
-                            const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc,
-                            const double* pre, unsigned long long* colmax, Status* st, const double* agg = nullptr,
-                            Status* mirror = nullptr, T* X = nullptr, T* Pdst = nullptr, const T* Pprev = nullptr) {
-  direction_body<T, false>(rows, ldq, q_real, step, max_steps, tol, printed, P, R, minv, ngroups, group_of_col, sc, pre,
-                           colmax, st, agg, mirror, X, Pdst, Pprev, nullptr, nullptr);
-}
-
-// with pap_out; at most 256 threads, and 3 blocks / SM like the plain kernel (one resident wave)
-template <typename T>
-__global__ void __launch_bounds__(256, 3)
-    k_direction_pap(int64_t rows, int ldq, int q_real, int step, int max_steps, double tol, int printed, T* P,
-                    const T* R, const double* minv, int ngroups, const int* group_of_col, Scalars sc, const double* pre,
-                    unsigned long long* colmax, Status* st, Status* mirror, T* X, T* Pdst, const T* Pprev,
-                    const double* pap_alpha, double* pap_out) {
-  direction_body<T, true>(rows, ldq, q_real, step, max_steps, tol, printed, P, R, minv, ngroups, group_of_col, sc, pre,
-                          colmax, st, nullptr, mirror, X, Pdst, Pprev, pap_alpha, pap_out);
 }
 
 // ---- multi-task glue (cofem.py:160-214) -------------------------------------
