@@ -479,6 +479,31 @@ def test_run_cofem_dct2_parity_with_oracle():
     np.testing.assert_array_equal(st.alpha < PRUNE, alpha < PRUNE)
 
 
+def test_dct2_psifree_step_matches_three_kernel_tail(monkeypatch):
+    """The Psi-free PCG step of the 2-D DCT (n >= 512: vv = ||Z||^2 from the
+    last row pass, <P, alpha P> by the direction recurrence, k_update_psi)
+    against the three-kernel tail (COFEM_DCT_PSI: k_combine, k_update,
+    k_direction) and the float64 oracle, at n = 512 (the <16, 32> passes)."""
+    c = S.Dct2Config("dct-512", 512, 0.25, 0.03, 0.01, 20, 3, 200, 1e-5)
+    prob, z = S.dct2_problem(c)
+    cfg = c.cofem_config()
+    st1, est1, d1 = run_cofem(prob, cfg)
+    prob.op.release()
+    monkeypatch.setenv("COFEM_DCT_PSI", "1")
+    st2, est2, d2 = run_cofem(prob, cfg)
+    prob.op.release()
+    monkeypatch.delenv("COFEM_DCT_PSI")
+    s1, s2 = [d["cg_steps"] for d in d1], [d["cg_steps"] for d in d2]
+    assert np.all(np.abs(np.array(s1) - s2) <= 1), (s1, s2)
+    assert rel(est1.mu, est2.mu) <= 1e-6 and rel(st1.alpha, st2.alpha) <= 1e-6
+    ocfg = O.CofemConfig(iterations=c.T, probes=c.K, seed=c.seed, cg=O.CgConfig(max_steps=c.U, tolerance=c.tol))
+    alpha, mu, s, odiag = O.run_cofem(O.dct2_op(c.n, prob.op.mask), np.asarray(prob.y), c.beta, ocfg)
+    # vs the oracle: the north_star bar (CG's stopping step moves by one on orthonormal-row
+    # dictionaries, DESIGN.md "Parity", and the solves stop at a 1e-5 residual)
+    assert rel(est1.mu, mu) <= 1e-4 and rel(st1.alpha, alpha) <= 1e-4
+    assert np.all(np.abs(np.array(s1) - [d["cg_steps"] for d in odiag]) <= 2)
+
+
 # --------------------------------------------- the reference's own workloads --
 @pytest.mark.parametrize("precision", ["auto", "ozaki", "fp64"])
 def test_reference_dct1d_recovery_parity(precision):
