@@ -357,3 +357,42 @@ def test_dct_pair_step_algebra_against_scipy():
     for seed in (0, 1):
         for name, err in mod.check(seed).items():
             assert err <= 1e-12, (name, err)
+
+
+def test_psifree_step_identities_on_a_partial_dct_system():
+    """The two identities behind the Psi-free 2-D DCT step (csrc/pcg.cuh
+    k_update_psi), checked in numpy along a Jacobi-preconditioned CG run on
+    a partial 2-D DCT system: with orthonormal rows pi = <P, A P> equals
+    beta ||Phi^T Phi P||^2 + <P, alpha P>, and <P, alpha P> follows the
+    direction recurrence P' = eta P + W as eta^2 pap + 2 eta <P, alpha W> +
+    <W, alpha W>."""
+    from scipy.fft import dctn, idctn
+
+    rng = np.random.default_rng(5)
+    n, Q, beta = 32, 5, 1e4
+    mask = rng.random((n, n)) < 0.3
+    alpha = rng.random(n * n) + 0.5
+    gram = lambda X: idctn(mask[..., None] * dctn(X.reshape(n, n, Q), axes=(0, 1), norm="ortho"), axes=(0, 1),
+                           norm="ortho").reshape(n * n, Q)  # noqa: E731  Phi^T Phi X
+    minv = 1.0 / (beta * 0.3 + alpha)
+    B = rng.standard_normal((n * n, Q))
+    X, R = np.zeros_like(B), B.copy()
+    W = minv[:, None] * R
+    P, rho = W.copy(), (R * W).sum(0)
+    pap = (W * (alpha[:, None] * W)).sum(0)
+    for _ in range(12):
+        Z = gram(P)
+        pi_direct = (P * (beta * Z + alpha[:, None] * P)).sum(0)
+        pi_psifree = beta * (Z * Z).sum(0) + pap
+        np.testing.assert_allclose(pi_psifree, pi_direct, rtol=1e-12)
+        np.testing.assert_allclose(pap, (P * (alpha[:, None] * P)).sum(0), rtol=1e-12)
+        gamma = rho / pi_psifree
+        X += gamma * P
+        R -= gamma * (beta * Z + alpha[:, None] * P)
+        W = minv[:, None] * R
+        rho_new = (R * W).sum(0)
+        eta = rho_new / rho
+        s1, s2 = (P * (alpha[:, None] * W)).sum(0), (W * (alpha[:, None] * W)).sum(0)
+        pap = eta * eta * pap + 2.0 * eta * s1 + s2
+        P, rho = eta * P + W, rho_new
+    assert np.linalg.norm(R) <= 1e-2 * np.linalg.norm(B)  # and it is a converging CG run
