@@ -504,6 +504,25 @@ def test_dct2_psifree_step_matches_three_kernel_tail(monkeypatch):
     assert np.all(np.abs(np.array(s1) - [d["cg_steps"] for d in odiag]) <= 2)
 
 
+@pytest.mark.parametrize("n", [512, 1024])
+def test_dct2_runs_are_bitwise_repeatable(n):
+    """Warp-level barriers inside the 4-step FFT, per-warp column sums folded in
+    fixed order, every reduction by block partials: two runs of the Psi-free
+    2-D DCT path give the same bits (a shared-memory race or an order-dependent
+    fold would not)."""
+    c = S.Dct2Config(f"dct-{n}", n, 0.25, 0.03, 0.01, 20, 2, 200, 1e-5)
+    prob, z = S.dct2_problem(c)
+    cfg = c.cofem_config()
+    runs = []
+    for _ in range(2):
+        st, est, diag = run_cofem(prob, cfg)
+        prob.op.release()
+        runs.append((st.alpha, est.mu, est.s, est.cg_report.solution, [d["cg_steps"] for d in diag]))
+    for a, b in zip(runs[0][:4], runs[1][:4]):
+        np.testing.assert_array_equal(a, b)
+    assert runs[0][4] == runs[1][4]
+
+
 # --------------------------------------------- the reference's own workloads --
 @pytest.mark.parametrize("precision", ["auto", "ozaki", "fp64"])
 def test_reference_dct1d_recovery_parity(precision):
