@@ -8,22 +8,28 @@
 //   row pass    DCT-II along j                        P    -> T1
 //   column pass DCT-II along i, mask, DCT-III along i  T1   -> T2  (fused)
 //   row pass    DCT-III along j                        T2   -> Z
-// (then the streaming PCG combine Psi = beta Z + alpha .* P, pi = <P, Psi>).
-// Each pass streams one n^2 x ldq float64 block in and one out: HBM-bound,
-// O(log n) arithmetic per element (a dense C X C^T would be O(n)).
+// then either the streaming PCG combine Psi = beta Z + alpha .* P, pi = <P, Psi>
+// (k_combine), or -- the Psi-free step, n >= 512 -- the last pass also returns
+// ||Z||^2 per column (= ||Phi P||^2: orthonormal rows) and k_update_psi
+// (pcg.cuh) updates the residual straight from Z.
+// Each pass streams one n^2 x ldq float64 block in and one out,
+// O(log n) arithmetic per element (a dense C X C^T would be O(n)); measured
+// latency-bound at 12 warps / SM (0.33 of HBM on the column pass).
 //
 // Every 1-D transform is Makhoul's: DCT-II of real x is Re(e^{-i pi k / 2n}
 // FFT_n(v)[k]) of the even/odd reordering v, and DCT-III inverts it with an
 // inverse FFT of e^{i pi k / 2n}(X[k] - i X[n-k]).  Two real vectors ride in
-// one complex FFT (real / imaginary part), and the length-n FFT is a
-// four-step N1 x N2 decomposition: register DFTs of size N2 and N1, one
-// twiddle multiply and two padded shared-memory transposes.
+// one complex FFT (real / imaginary part); the pre / post steps work once per
+// coefficient pair (k, n - k) (pair_op).  The length-n FFT is a four-step
+// N1 x N2 decomposition: register DFTs of size N2 and N1, one twiddle
+// multiply and two padded shared-memory transposes.
 //
 // Block layout (ldq = padded column count, Q images interleaved):
 //   P[(i n + j) ldq + q]       pixel-major, as every PCG block
 //   T1[(i n + l) ldq + q]      after the row pass (l = j frequency)
 //   Y[(k n + l) ldq + q]       coefficient grid after the column pass
-// A pass item is (outer index o, q-group of 8 columns): 4 complex FFTs.
+// A pass item is (outer index o, q-group of 2 FPI = 4 columns): FPI = 2 complex FFTs,
+// one warp each at n >= 512.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
