@@ -325,9 +325,20 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         else:
+            prof = None
+            if os.environ.get("BENCH_E2E_PROFILE"):  # where the host time of the e2e call goes (stderr)
+                import cProfile
+
+                prof = cProfile.Profile()
+                prof.enable()
             t0 = time.perf_counter()
             st, est, diag = run_cofem(prob, cfg)
             el = time.perf_counter() - t0
+            if prof:
+                import pstats
+
+                prof.disable()
+                pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(8)
             prob.op.release()
         h2d = (4.0 * c.N * c.D + 8.0 * c.N + 32.0) / args.steps
         d2h = 8.0 * 3 * c.D / args.steps + 12.0
